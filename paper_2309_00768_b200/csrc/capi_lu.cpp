@@ -1,0 +1,124 @@
+// extern "C" entry points: error state and the generic batched sparse LU
+// (drop-in for reference LUFactor, pkg/src/stmhd/linalg.py:71-96).
+#include <cstring>
+
+#include "nd.hpp"
+
+namespace stmhd {
+static thread_local std::string g_last_error;
+static thread_local std::string g_last_block;
+void set_last_error(const std::string &msg, const std::string &block) {
+  g_last_error = msg;
+  g_last_block = block;
+}
+}  // namespace stmhd
+
+using namespace stmhd;
+
+struct stmhd_lu_s {
+  NDPlan plan;
+  NDDevice dev;
+  NDFactor fac;
+};
+
+#define CAPI_BEGIN try {
+#define CAPI_END                                   \
+  return STMHD_OK;                                 \
+  }                                                \
+  catch (const stmhd::Error &e) {                  \
+    stmhd::set_last_error(e.what(), e.block);      \
+    return e.status;                               \
+  }                                                \
+  catch (const std::exception &e) {                \
+    stmhd::set_last_error(e.what());               \
+    return STMHD_CONFIG;                           \
+  }
+
+extern "C" {
+
+int stmhd_abi_version(void) { return 1; }
+const char *stmhd_last_error(void) { return g_last_error.c_str(); }
+const char *stmhd_last_block(void) { return g_last_block.c_str(); }
+
+int stmhd_lu_create(int64_t n, const int32_t *rowptr, const int32_t *col, const int32_t *gx,
+                    const int32_t *gy, int nbatch, int leaf_max, stmhd_lu *out) {
+  CAPI_BEGIN
+  require(n > 0 && rowptr && col && out && nbatch >= 1, "stmhd_lu_create: bad arguments");
+  auto *lu = new stmhd_lu_s();
+  try {
+    lu->plan = nd_analyze(n, rowptr, col, gx, gy, leaf_max > 0 ? leaf_max : 64, nullptr);
+    lu->dev.build(lu->plan, 0);
+    STMHD_CUDA_CHECK(cudaStreamSynchronize(0));
+    lu->fac.dev = &lu->dev;
+    lu->fac.nbatch = nbatch;
+  } catch (...) {
+    delete lu;
+    throw;
+  }
+  *out = lu;
+  CAPI_END
+}
+
+int stmhd_lu_destroy(stmhd_lu lu) {
+  CAPI_BEGIN
+  delete lu;
+  CAPI_END
+}
+
+int stmhd_lu_factor(stmhd_lu lu, void *stream, const double *values, int64_t value_stride,
+                    const int32_t *value_map_host) {
+  CAPI_BEGIN
+  require(lu && values, "stmhd_lu_factor: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (value_map_host) {
+    // remap the scatter sources once (rebuild plan's device scatter list)
+    std::vector<int64_t> src(lu->plan.scat_src.size());
+    for (size_t i = 0; i < src.size(); ++i) src[i] = value_map_host[lu->plan.scat_src[i]];
+    lu->dev.scat_src = upload_vec(src, s);
+  }
+  lu->fac.factor(values, value_stride, s);
+  int st = lu->fac.check_status(s);
+  if (st) throw Error(STMHD_SINGULAR, "LU factorisation hit a zero pivot (supernode " + std::to_string(st - 1) + ")");
+  CAPI_END
+}
+
+int stmhd_lu_solve(stmhd_lu lu, void *stream, const double *rhs, int64_t ld_rhs, double *x,
+                   int64_t ld_x, int nrhs) {
+  CAPI_BEGIN
+  require(lu && rhs && x && nrhs >= 1, "stmhd_lu_solve: bad arguments");
+  require(lu->fac.factors.ptr, "stmhd_lu_solve: not factored");
+  lu->fac.solve(rhs, ld_rhs, x, ld_x, nrhs, (cudaStream_t)stream);
+  STMHD_LAUNCH_CHECK();
+  CAPI_END
+}
+
+int stmhd_lu_info(stmhd_lu lu, int64_t *info) {
+  CAPI_BEGIN
+  require(lu && info, "stmhd_lu_info: bad arguments");
+  info[0] = lu->plan.factor_size;
+  info[1] = lu->plan.nsn;
+  info[2] = lu->plan.nlevels;
+  info[3] = lu->plan.max_front;
+  info[4] = lu->plan.sym_nnz;
+  CAPI_END
+}
+
+int stmhd_nd_plan_info(int64_t n, const int32_t *rowptr, const int32_t *col, const int32_t *gx,
+                       const int32_t *gy, int leaf_max, int64_t *info) {
+  CAPI_BEGIN
+  require(n > 0 && rowptr && col && info, "stmhd_nd_plan_info: bad arguments");
+  NDPlan p = nd_analyze(n, rowptr, col, gx, gy, leaf_max > 0 ? leaf_max : 64, nullptr);
+  info[0] = p.factor_size;
+  info[1] = p.nsn;
+  info[2] = p.nlevels;
+  info[3] = p.max_front;
+  info[4] = p.sym_nnz;
+  info[5] = p.front_size;
+  info[6] = p.cbv_size;
+  int64_t items = 0;
+  for (int s = 0; s < p.nsn; ++s) items += (p.ns[s] + p.nb[s] + 63) / 64;
+  info[7] = items;
+  CAPI_END
+}
+
+}  // extern "C"
