@@ -1,0 +1,427 @@
+// K1: space-time residual and Jacobian-value assembly on the device.
+//
+// Reference: residual (spacetime.py:65-85, _slab_galerkin :42-62),
+// linearize_slab (spacetime.py:99-112), the state-dependent blocks of
+// fem.py:341-472, F_p (precond.py:80-84) and the Alfven scaling
+// (precond.py:46-57).  Every value is a contraction of the element state with
+// exact per-orientation tensors (see fem.py in this package); rows and CSR
+// entries gather their element contributions in a fixed order, so the
+// assembly is deterministic (no atomics).
+#include "disc.hpp"
+
+namespace stmhd {
+
+struct TOff {
+  int MV, KV, TV, MX, G1, M1, K1, MP, KP, TP, BD, total;
+};
+
+__host__ __device__ constexpr TOff toff(int NV, int NP) {
+  TOff o{};
+  o.MV = 0;
+  o.KV = o.MV + NV * NV;
+  o.TV = o.KV + 2 * NV * NV;
+  o.MX = o.TV + 2 * NV * NV * NV * 2;
+  o.G1 = o.MX + NV * 3;
+  o.M1 = o.G1 + 12;
+  o.K1 = o.M1 + 9;
+  o.MP = o.K1 + 18;
+  o.KP = o.MP + NP * NP;
+  o.TP = o.KP + 2 * NP * NP;
+  o.BD = o.TP + 2 * NP * NV * NP * 2;
+  o.total = o.BD + 2 * NP * NV * 2;
+  return o;
+}
+
+struct AsmArgs {
+  int nt, n_u, n_p, n_j, n_a, nnv, nn1, ne, p_pin;
+  int64_t slab;
+  double dt, mu, eta, mu0;
+  const double *tensors;
+  const int *elem_v, *elem_p, *elem_1;
+  const int *ne_v_ptr, *ne_v, *ne_p_ptr, *ne_p, *ne_1_ptr, *ne_1;
+  const int *u_bc_mask, *a_bc_mask;
+  const double *u_bc_val, *a_bc_val, *flux, *e_load;
+  const double *state, *ic_u, *ic_a;
+  const double *sc;  // clamped state
+  double *res;
+};
+
+__global__ void clamp_kernel(AsmArgs a, double *out) {
+  const int64_t N = (int64_t)a.nt * a.slab;
+  const int o_a = a.n_u + a.n_p + a.n_j;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(t % a.slab);
+    double v = a.state[t];
+    if (i < a.n_u) {
+      if (a.u_bc_mask[i]) v = a.u_bc_val[i];
+    } else if (i >= o_a) {
+      if (a.a_bc_mask[i - o_a]) v = a.a_bc_val[i - o_a];
+    }
+    out[t] = v;
+  }
+}
+
+template <int NV, int NP>
+__device__ __forceinline__ void load_u(const AsmArgs &a, const double *s, int e, double (&u)[2][NV]) {
+#pragma unroll
+  for (int m = 0; m < NV; ++m) {
+    int g = a.elem_v[e * NV + m];
+    u[0][m] = s[g];
+    u[1][m] = s[a.nnv + g];
+  }
+}
+
+template <int NV, int NP>
+__global__ void __launch_bounds__(256) residual_kernel(AsmArgs a) {
+  extern __shared__ double T[];
+  constexpr TOff O = toff(NV, NP);
+  for (int t = threadIdx.x; t < O.total; t += blockDim.x) T[t] = a.tensors[t];
+  __syncthreads();
+  const int k = blockIdx.y;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.slab) return;
+  const int o_p = a.n_u, o_j = a.n_u + a.n_p, o_a = o_j + a.n_j;
+  const double *s = a.sc + (int64_t)k * a.slab;
+  const double *raw = a.state + (int64_t)k * a.slab;
+  // previous slab: clamped k-1, or the raw initial condition for k = 0
+  const double *pu = k ? a.sc + (int64_t)(k - 1) * a.slab : a.ic_u;
+  const double *pa = k ? a.sc + (int64_t)(k - 1) * a.slab + o_a : a.ic_a;
+  const double idt = 1.0 / a.dt;
+  double out = 0.0;
+  if (r < a.n_u) {
+    if (a.u_bc_mask[r]) {
+      out = raw[r] - a.u_bc_val[r];
+    } else {
+      const int d = r / a.nnv, node = r % a.nnv;
+      double mass = 0.0, visc = 0.0, pres = 0.0, adv = 0.0, lor = 0.0;
+      for (int q = a.ne_v_ptr[node]; q < a.ne_v_ptr[node + 1]; ++q) {
+        const int code = a.ne_v[q], e = code >> 4, il = code & 15, o = e & 1;
+        double u[2][NV], up[2][NV];
+        load_u<NV, NP>(a, s, e, u);
+        load_u<NV, NP>(a, pu, e, up);
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          mass += T[O.MV + il * NV + j] * (u[d][j] - up[d][j]);
+          visc += T[O.KV + (o * NV + il) * NV + j] * u[d][j];
+        }
+#pragma unroll
+        for (int n = 0; n < NP; ++n)
+          pres += T[O.BD + ((o * NP + n) * NV + il) * 2 + d] * s[o_p + a.elem_p[e * NP + n]];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int m = 0; m < NV; ++m) {
+            double acc = 0.0;
+#pragma unroll
+            for (int n = 0; n < NV; ++n) acc += T[O.TV + (((o * NV + il) * NV + m) * NV + n) * 2 + c] * u[d][n];
+            adv += u[c][m] * acc;
+          }
+        double ga = 0.0, jm = 0.0;
+#pragma unroll
+        for (int n = 0; n < 3; ++n) {
+          int g = a.elem_1[e * 3 + n];
+          ga += s[o_a + g] * T[O.G1 + (o * 3 + n) * 2 + d];
+          jm += s[o_j + g] * T[O.MX + il * 3 + n];
+        }
+        lor += ga * jm;
+      }
+      out = mass * idt + a.mu * visc + pres + adv + lor;
+    }
+  } else if (r < o_j) {
+    const int m = r - o_p;
+    if (m == a.p_pin) return;  // mean-constraint row: pin_row_kernel
+    double acc = 0.0;
+    for (int q = a.ne_p_ptr[m]; q < a.ne_p_ptr[m + 1]; ++q) {
+      const int code = a.ne_p[q], e = code >> 4, ml = code & 15, o = e & 1;
+      double u[2][NV];
+      load_u<NV, NP>(a, s, e, u);
+#pragma unroll
+      for (int n = 0; n < NV; ++n)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) acc += T[O.BD + ((o * NP + ml) * NV + n) * 2 + c] * u[c][n];
+    }
+    out = acc;
+  } else if (r < o_a) {
+    const int m = r - o_j;
+    double mj = 0.0, kj = 0.0;
+    for (int q = a.ne_1_ptr[m]; q < a.ne_1_ptr[m + 1]; ++q) {
+      const int code = a.ne_1[q], e = code >> 4, ml = code & 15, o = e & 1;
+#pragma unroll
+      for (int n = 0; n < 3; ++n) {
+        int g = a.elem_1[e * 3 + n];
+        mj += T[O.M1 + ml * 3 + n] * s[o_j + g];
+        kj += T[O.K1 + (o * 3 + ml) * 3 + n] * s[o_a + g];
+      }
+    }
+    out = mj + kj / a.mu0 - a.flux[m];
+  } else {
+    const int m = r - o_a;
+    if (a.a_bc_mask[m]) {
+      out = raw[r] - a.a_bc_val[m];
+    } else {
+      double mass = 0.0, diff = 0.0, adv = 0.0;
+      for (int q = a.ne_1_ptr[m]; q < a.ne_1_ptr[m + 1]; ++q) {
+        const int code = a.ne_1[q], e = code >> 4, ml = code & 15, o = e & 1;
+        double gx = 0.0, gy = 0.0;
+#pragma unroll
+        for (int n = 0; n < 3; ++n) {
+          int g = a.elem_1[e * 3 + n];
+          double av = s[o_a + g];
+          mass += T[O.M1 + ml * 3 + n] * (av - pa[g]);
+          diff += T[O.K1 + (o * 3 + ml) * 3 + n] * av;
+          gx += av * T[O.G1 + (o * 3 + n) * 2 + 0];
+          gy += av * T[O.G1 + (o * 3 + n) * 2 + 1];
+        }
+        double u[2][NV];
+        load_u<NV, NP>(a, s, e, u);
+        double mx = 0.0, my = 0.0;
+#pragma unroll
+        for (int n = 0; n < NV; ++n) {
+          mx += T[O.MX + n * 3 + ml] * u[0][n];
+          my += T[O.MX + n * 3 + ml] * u[1][n];
+        }
+        adv += gx * mx + gy * my;
+      }
+      out = mass * idt + (a.eta / a.mu0) * diff + adv + a.e_load[m];
+    }
+  }
+  a.res[(int64_t)k * a.slab + r] = out;
+}
+
+// r_p[pin] = w . p_raw - target  (spacetime.py:78), one block per slab
+__global__ void pin_row_kernel(const double *state, const double *w, int n_p, int64_t slab, int o_p,
+                               int pin, double target, double *res) {
+  __shared__ double sh[32];
+  const int k = blockIdx.x;
+  const double *p = state + (int64_t)k * slab + o_p;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n_p; i += blockDim.x) acc += w[i] * p[i];
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) res[(int64_t)k * slab + o_p + pin] = acc - target;
+}
+
+// s_k = |mean grad A_k|^2 / mu0 on the clamped potential (precond.py:46-57)
+__global__ void alfven_kernel(AsmArgs a, const double *g1, double elem_area, double area, double *out) {
+  extern __shared__ double T[];
+  __shared__ double sh[32];
+  constexpr int G1off = 0;
+  for (int t = threadIdx.x; t < 12; t += blockDim.x) T[t] = g1[t];
+  __syncthreads();
+  const int k = blockIdx.x;
+  const int o_a = a.n_u + a.n_p + a.n_j;
+  const double *s = a.sc + (int64_t)k * a.slab + o_a;
+  double gx = 0.0, gy = 0.0;
+  for (int e = threadIdx.x; e < a.ne; e += blockDim.x) {
+    int o = e & 1;
+#pragma unroll
+    for (int n = 0; n < 3; ++n) {
+      double av = s[a.elem_1[e * 3 + n]];
+      gx += av * T[G1off + (o * 3 + n) * 2 + 0];
+      gy += av * T[G1off + (o * 3 + n) * 2 + 1];
+    }
+  }
+  gx = block_sum(gx, sh) * elem_area / area;
+  gy = block_sum(gy, sh) * elem_area / area;
+  if (threadIdx.x == 0) out[k] = (gx * gx + gy * gy) / a.mu0;
+}
+
+struct ValArgs {
+  int nnz, nt;
+  const int *kind, *cptr, *contrib;
+  int64_t out_stride;
+  double *out;
+  int is_fp;
+};
+
+// Per-slab Jacobian values in the fixed merged pattern (linearize_slab) or F_p.
+template <int NV, int NP>
+__global__ void __launch_bounds__(256) values_kernel(AsmArgs a, ValArgs v) {
+  extern __shared__ double T[];
+  constexpr TOff O = toff(NV, NP);
+  for (int t = threadIdx.x; t < O.total; t += blockDim.x) T[t] = a.tensors[t];
+  __syncthreads();
+  const int ent = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ent >= v.nnz) return;
+  const int kind = v.is_fp ? 6 : v.kind[ent];
+  const int kd = kind & 15, d = (kind >> 4) & 1, c = (kind >> 5) & 1;
+  const int q0 = v.cptr[ent], q1 = v.cptr[ent + 1];
+  const int o_j = a.n_u + a.n_p, o_a = o_j + a.n_j, o_p = a.n_u;
+  const double idt = 1.0 / a.dt;
+  const double ceta = a.eta / a.mu0;
+  (void)o_p;
+  for (int k = blockIdx.y; k < a.nt; k += gridDim.y) {
+    const double *s = a.sc + (int64_t)k * a.slab;
+    double val = 0.0;
+    if (kd == 0) {
+      val = 1.0;
+    } else {
+      for (int q = q0; q < q1; ++q) {
+        const int code = v.contrib[q], e = code >> 8, il = (code >> 4) & 15, jl = code & 15, o = e & 1;
+        if (kd == 1) {  // f_u (d,c): M/dt + mu K + transport + reaction
+          double u[2][NV];
+          load_u<NV, NP>(a, s, e, u);
+          double t = 0.0;
+          if (d == c) {
+            double tr = 0.0;
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+              for (int m = 0; m < NV; ++m) tr += u[cc][m] * T[O.TV + (((o * NV + il) * NV + m) * NV + jl) * 2 + cc];
+            t = T[O.MV + il * NV + jl] * idt + a.mu * T[O.KV + (o * NV + il) * NV + jl] + tr;
+          }
+          double re = 0.0;
+#pragma unroll
+          for (int m = 0; m < NV; ++m) re += u[d][m] * T[O.TV + (((o * NV + il) * NV + jl) * NV + m) * 2 + c];
+          val += t + re;
+        } else if (kd == 2) {  // z_j: (d_d A) int phi_i psi_n
+          double ga = 0.0;
+#pragma unroll
+          for (int n = 0; n < 3; ++n) ga += s[o_a + a.elem_1[e * 3 + n]] * T[O.G1 + (o * 3 + n) * 2 + d];
+          val += ga * T[O.MX + il * 3 + jl];
+        } else if (kd == 3) {  // z_a: (int j phi_i) d_d psi_n
+          double jm = 0.0;
+#pragma unroll
+          for (int n = 0; n < 3; ++n) jm += s[o_j + a.elem_1[e * 3 + n]] * T[O.MX + il * 3 + n];
+          val += jm * T[O.G1 + (o * 3 + jl) * 2 + d];
+        } else if (kd == 4) {  // y: (d_c A) int psi_m phi_n
+          double ga = 0.0;
+#pragma unroll
+          for (int n = 0; n < 3; ++n) ga += s[o_a + a.elem_1[e * 3 + n]] * T[O.G1 + (o * 3 + n) * 2 + c];
+          val += ga * T[O.MX + jl * 3 + il];
+        } else if (kd == 5) {  // f_a: M/dt + (eta/mu0) K + int psi_m u.grad psi_n
+          double u[2][NV];
+          load_u<NV, NP>(a, s, e, u);
+          double mx = 0.0, my = 0.0;
+#pragma unroll
+          for (int l = 0; l < NV; ++l) {
+            mx += u[0][l] * T[O.MX + l * 3 + il];
+            my += u[1][l] * T[O.MX + l * 3 + il];
+          }
+          val += T[O.M1 + il * 3 + jl] * idt + ceta * T[O.K1 + (o * 3 + il) * 3 + jl] +
+                 (T[O.G1 + (o * 3 + jl) * 2 + 0] * mx + T[O.G1 + (o * 3 + jl) * 2 + 1] * my);
+        } else {  // F_p: M_p/dt + W_p(u) + mu K_p
+          double u[2][NV];
+          load_u<NV, NP>(a, s, e, u);
+          double w = 0.0;
+#pragma unroll
+          for (int l = 0; l < NV; ++l)
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) w += u[cc][l] * T[O.TP + (((o * NP + il) * NV + l) * NP + jl) * 2 + cc];
+          val += T[O.MP + il * NP + jl] * idt + w + a.mu * T[O.KP + (o * NP + il) * NP + jl];
+        }
+      }
+    }
+    v.out[(int64_t)k * v.out_stride + ent] = val;
+  }
+}
+
+static AsmArgs make_args(const stmhd_disc_s *d) {
+  AsmArgs a{};
+  a.nt = (int)d->I("nt");
+  a.n_u = (int)d->I("n_u");
+  a.n_p = (int)d->I("n_p");
+  a.n_j = (int)d->I("n_j");
+  a.n_a = (int)d->I("n_a");
+  a.nnv = (int)d->I("nnv");
+  a.nn1 = (int)d->I("nn1");
+  a.ne = (int)d->I("ne");
+  a.p_pin = (int)d->I("p_pin");
+  a.slab = d->slab();
+  a.dt = d->R("dt");
+  a.mu = d->R("mu");
+  a.eta = d->R("eta");
+  a.mu0 = d->R("mu0");
+  a.tensors = d->D<double>("tensors");
+  a.elem_v = d->D<int>("elem_v");
+  a.elem_p = d->D<int>("elem_p");
+  a.elem_1 = d->D<int>("elem_1");
+  a.ne_v_ptr = d->D<int>("ne_v_ptr");
+  a.ne_v = d->D<int>("ne_v");
+  a.ne_p_ptr = d->D<int>("ne_p_ptr");
+  a.ne_p = d->D<int>("ne_p");
+  a.ne_1_ptr = d->D<int>("ne_1_ptr");
+  a.ne_1 = d->D<int>("ne_1");
+  a.u_bc_mask = d->D<int>("u_bc_mask");
+  a.a_bc_mask = d->D<int>("a_bc_mask");
+  a.u_bc_val = d->D<double>("u_bc_val");
+  a.a_bc_val = d->D<double>("a_bc_val");
+  a.flux = d->D<double>("flux");
+  a.e_load = d->D<double>("e_load");
+  return a;
+}
+
+template <int NV, int NP>
+static void assemble_t(stmhd_disc_s *d, cudaStream_t s, const double *state, const double *ic_u,
+                       const double *ic_a, double *res, double *js, double *fp, double *alf) {
+  AsmArgs a = make_args(d);
+  a.state = state;
+  a.ic_u = ic_u;
+  a.ic_a = ic_a;
+  a.res = res;
+  const int64_t N = (int64_t)a.nt * a.slab;
+  if (d->clamped.bytes < (size_t)N * sizeof(double)) d->clamped.alloc(N * sizeof(double));
+  double *sc = d->clamped.as<double>();
+  a.sc = sc;
+  clamp_kernel<<<std::min<int64_t>(cdiv(N, 256), 8 * num_sms()), 256, 0, s>>>(a, sc);
+  STMHD_LAUNCH_CHECK();
+  constexpr TOff O = toff(NV, NP);
+  const size_t smem = O.total * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    STMHD_CUDA_CHECK(cudaFuncSetAttribute(residual_kernel<NV, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    STMHD_CUDA_CHECK(cudaFuncSetAttribute(values_kernel<NV, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    attr = true;
+  }
+  if (res) {
+    residual_kernel<NV, NP><<<dim3(cdiv(a.slab, 256), a.nt), 256, smem, s>>>(a);
+    STMHD_LAUNCH_CHECK();
+    pin_row_kernel<<<a.nt, 256, 0, s>>>(state, d->D<double>("p_mean_row"), a.n_p, a.slab, a.n_u, a.p_pin,
+                                         d->R("p_mean_target"), res);
+    STMHD_LAUNCH_CHECK();
+  }
+  const int ychunks = std::max(1, std::min(a.nt, 8));
+  if (js) {
+    ValArgs v{};
+    v.nnz = (int)d->I("nnz_js");
+    v.nt = a.nt;
+    v.kind = d->D<int>("js_kind");
+    v.cptr = d->D<int>("js_cptr");
+    v.contrib = d->D<int>("js_contrib");
+    v.out_stride = v.nnz;
+    v.out = js;
+    v.is_fp = 0;
+    values_kernel<NV, NP><<<dim3(cdiv(v.nnz, 256), ychunks), 256, smem, s>>>(a, v);
+    STMHD_LAUNCH_CHECK();
+  }
+  if (fp) {
+    ValArgs v{};
+    v.nnz = (int)d->I("nnz_fp");
+    v.nt = a.nt;
+    v.kind = nullptr;
+    v.cptr = d->D<int>("fp_cptr");
+    v.contrib = d->D<int>("fp_contrib");
+    v.out_stride = v.nnz;
+    v.out = fp;
+    v.is_fp = 1;
+    values_kernel<NV, NP><<<dim3(cdiv(v.nnz, 256), ychunks), 256, smem, s>>>(a, v);
+    STMHD_LAUNCH_CHECK();
+  }
+  if (alf) {
+    alfven_kernel<<<a.nt, 256, 12 * sizeof(double), s>>>(a, a.tensors + O.G1, d->R("elem_area"), d->R("area"), alf);
+    STMHD_LAUNCH_CHECK();
+  }
+}
+
+void assemble(stmhd_disc_s *d, cudaStream_t s, const double *state, const double *ic_u, const double *ic_a,
+              double *res, double *js, double *fp, double *alf) {
+  require(state && ic_u && ic_a, "stmhd_assemble: state, ic_u and ic_a are required");
+  int nv = (int)d->I("nv"), np = (int)d->I("npl");
+  if (nv == 6 && np == 3)
+    assemble_t<6, 3>(d, s, state, ic_u, ic_a, res, js, fp, alf);
+  else if (nv == 10 && np == 6)
+    assemble_t<10, 6>(d, s, state, ic_u, ic_a, res, js, fp, alf);
+  else
+    throw Error(STMHD_CONFIG, "unsupported element pair (need P2/P1 or P3/P2)");
+}
+
+}  // namespace stmhd

@@ -167,3 +167,176 @@ class LUFactor:
 
 def lu_factor(matrix) -> LUFactor:
     return LUFactor(matrix)
+
+
+# -- device FGMRES ------------------------------------------------------------------
+
+
+@dataclass
+class GmresConfig:
+    rel_tol: float = 1e-2
+    abs_tol: float = 1e-14
+    max_iters: int = 200
+    restart: int | None = None  # None = full GMRES
+
+    def __post_init__(self):
+        if self.rel_tol <= 0 or self.abs_tol <= 0:
+            raise ValueError("tolerances must be positive")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be at least 1")
+
+
+@dataclass
+class GmresResult:
+    x: torch.Tensor
+    iterations: int
+    residuals: list = field(default_factory=list)
+    converged: bool = True
+    true_residual: float = 0.0
+
+
+def _fast(fn):
+    """(object, method) for callbacks that can write into a given buffer."""
+    obj = getattr(fn, "__self__", None)
+    if obj is not None and hasattr(obj, "_into") and getattr(fn, "__name__", "") in ("apply", "apply_inverse"):
+        return obj
+    return None
+
+
+class _Workspace:
+    """Krylov basis storage reused across gmres calls of the same size."""
+
+    cache: dict = {}
+
+    @classmethod
+    def get(cls, n, m):
+        key = (n, m)
+        ws = cls.cache.get(key)
+        if ws is None:
+            cls.cache.clear()
+            lib = _lib.load()
+            ws = dict(V=torch.empty((m + 1, n), dtype=torch.float64, device=DEV),
+                      Z=torch.empty((m, n), dtype=torch.float64, device=DEV),
+                      dev=torch.zeros(2 * (m + 2), dtype=torch.float64, device=DEV),
+                      host=torch.zeros(2 * (m + 2), dtype=torch.float64).pin_memory(),
+                      work=torch.empty(int(lib.stmhd_gs_work_size(n, m + 1)) + 8, dtype=torch.float64, device=DEV),
+                      y=torch.zeros(m, dtype=torch.float64, device=DEV),
+                      r=torch.empty(n, dtype=torch.float64, device=DEV))
+            cls.cache[key] = ws
+        return ws
+
+
+def gmres(apply_a, apply_pinv, b, x0=None, config: GmresConfig | None = None) -> GmresResult:
+    """Right-preconditioned restarted FGMRES on the device (reference
+    linalg.py:122-209 semantics: x0 = 0 unless given, tol = max(rel |r0|, abs)
+    fixed at entry, Givens rotations, restart residual recomputed, true
+    residual at exit).  Orthogonalisation is CGS2 with fused multi-vector
+    kernels; the preconditioned basis Z is stored, so the cycle update is
+    x += Z y (no extra preconditioner apply)."""
+    cfg = config or GmresConfig()
+    lib = _lib.load()
+    sp_ = _lib.stream_ptr()
+    b = as_device(b).contiguous()
+    n = b.numel()
+    if not bool(torch.isfinite(b).all()):
+        raise BreakdownError("right-hand side contains non-finite values")
+    ident = apply_pinv is None
+    fa, fp = _fast(apply_a), (None if ident else _fast(apply_pinv))
+
+    def A_into(v, out):
+        if fa is not None:
+            return fa._into(v, out)
+        out.copy_(as_device(apply_a(v)).reshape(-1))
+        return out
+
+    def P_into(v, out):
+        if ident:
+            out.copy_(v)
+        elif fp is not None:
+            fp._into(v, out)
+        else:
+            out.copy_(as_device(apply_pinv(v)).reshape(-1))
+        return out
+
+    restart = cfg.restart or cfg.max_iters
+    m_alloc = min(restart, cfg.max_iters)
+    ws = _Workspace.get(n, m_alloc)
+    V, Z, dev, host, work, ydev, r = ws["V"], ws["Z"], ws["dev"], ws["host"], ws["work"], ws["y"], ws["r"]
+    x = torch.zeros(n, dtype=torch.float64, device=DEV) if x0 is None else as_device(x0).clone().reshape(-1)
+    if x0 is not None:
+        A_into(x, r)
+        r.neg_().add_(b)
+    else:
+        r.copy_(b)
+    beta = float(torch.linalg.vector_norm(r))
+    residuals = [beta]
+    tol = max(cfg.rel_tol * beta, cfg.abs_tol)
+    if beta <= tol:
+        return GmresResult(x, 0, residuals, True, beta)
+    total, converged = 0, False
+    while total < cfg.max_iters and not converged:
+        m = min(restart, cfg.max_iters - total)
+        H = np.zeros((m + 1, m))
+        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+        torch.div(r, beta, out=V[0])
+        g[0] = beta
+        last = -1
+        for j in range(m):
+            P_into(V[j], Z[j])
+            w = V[j + 1]
+            A_into(Z[j], w)
+            nv = j + 1
+            h1, h2, nrm = dev[:nv], dev[m_alloc + 1: m_alloc + 1 + nv], dev[2 * m_alloc + 3: 2 * m_alloc + 4]
+            _lib.check(lib.stmhd_gs_dots(sp_, _lib.ptr(V), n, nv, _lib.ptr(w), n, _lib.ptr(h1), _lib.ptr(work)))
+            _lib.check(lib.stmhd_gs_update(sp_, _lib.ptr(V), n, nv, _lib.ptr(h1), _lib.ptr(w), n, _lib.ptr(h2),
+                                           0, _lib.ptr(work)))
+            _lib.check(lib.stmhd_gs_update(sp_, _lib.ptr(V), n, nv, _lib.ptr(h2), _lib.ptr(w), n, 0,
+                                           _lib.ptr(nrm), _lib.ptr(work)))
+            host.copy_(dev, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            hv = host.numpy()
+            col = hv[:nv] + hv[m_alloc + 1: m_alloc + 1 + nv]
+            nrm2 = hv[2 * m_alloc + 3]
+            if not (np.all(np.isfinite(col)) and np.isfinite(nrm2)):
+                raise BreakdownError("non-finite vector in Arnoldi process")
+            hnorm = float(np.sqrt(max(nrm2, 0.0)))
+            H[:nv, j] = col
+            H[j + 1, j] = hnorm
+            for i in range(j):
+                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t
+            den = np.hypot(H[j, j], H[j + 1, j])
+            cs[j], sn[j] = H[j, j] / den, H[j + 1, j] / den
+            H[j, j] = den
+            H[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            total += 1
+            last = j
+            residuals.append(abs(float(g[j + 1])))
+            if residuals[-1] <= tol:
+                converged = True
+                break
+            if den == 0.0:
+                break
+            if hnorm > 0:
+                _lib.check(lib.stmhd_gs_normalize(sp_, _lib.ptr(w), _lib.ptr(w), n, _lib.ptr(nrm)))
+        if last >= 0:
+            y = np.zeros(last + 1)
+            for i in range(last, -1, -1):
+                y[i] = (g[i] - H[i, i + 1:last + 1] @ y[i + 1:last + 1]) / H[i, i]
+            ydev[: last + 1].copy_(torch.from_numpy(y))
+            _lib.check(lib.stmhd_gs_combine(sp_, _lib.ptr(Z), n, last + 1, _lib.ptr(ydev), _lib.ptr(x), n))
+        if converged:
+            break
+        A_into(x, r)
+        r.neg_().add_(b)
+        beta = float(torch.linalg.vector_norm(r))
+        if beta <= tol:
+            converged = True
+            break
+    A_into(x, r)
+    r.neg_().add_(b)
+    true_res = float(torch.linalg.vector_norm(r))
+    return GmresResult(x, total, residuals, converged, true_res)

@@ -1,0 +1,207 @@
+"""GPU parity of the drop-in operators against the reference's golden vectors
+and the CPU oracle.
+
+Tolerances (north star): assembled values and matvecs per entry
+|gpu - ref| <= 1e-12 * max(|ref|, floor) with floor = max |row| (cancelling
+entries) for matrices and the |J||v| rounding scale for matvecs; P_T^{-1} r
+relative L2 <= 1e-10; FGMRES iteration count within +-1; solution relative
+L2 <= 1e-8.
+"""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import csr_from
+
+pytestmark = pytest.mark.gpu
+
+TOL_ENTRY = 1e-12
+
+
+@pytest.fixture(scope="module")
+def p():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2309_00768_b200 as pkg
+
+    return pkg
+
+
+def _disc(p, name):
+    if name == "ref_island":
+        return p.discretize(p.by_name("island_coalescence"), 0.5, 0.5, 1.0)
+    if name == "ref_tearing":
+        return p.discretize(p.by_name("tearing_mode"), 0.25, 0.5, 1.0)
+    if name == "bl_island4":
+        return p.discretize(p.baseline_island(1e-2), 0.5, 0.1, 0.3)
+    if name == "bl_tearing4":
+        return p.discretize(p.baseline_tearing(1e-3), 0.5, 0.02, 0.04)
+    if name == "bl_c1":
+        return p.discretize_config("C1")
+    raise KeyError(name)
+
+
+def _oracle_disc(name):
+    from oracle import configs, model
+
+    if name == "ref_island":
+        return model.make_disc_dx(configs.reference_problem("island_coalescence"), 0.5, 0.5, 1.0)
+    if name == "ref_tearing":
+        return model.make_disc_dx(configs.reference_problem("tearing_mode"), 0.25, 0.5, 1.0)
+    if name == "bl_island4":
+        return model.make_disc(configs.baseline_problem("island", 1e-2), 4, 0.1, 3)
+    if name == "bl_tearing4":
+        return model.make_disc(configs.baseline_problem("tearing", 1e-3), 4, 0.02, 2)
+    if name == "bl_c1":
+        return model.make_disc(configs.baseline_problem("island", 1e-2), 16, 0.1, 8)
+
+
+def relerr(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def entry_ok(mine, ref, scale):
+    """Per-entry check |mine-ref| <= TOL*max(|ref|, scale); returns worst ratio."""
+    err = np.abs(mine - ref)
+    den = np.maximum(np.abs(ref), scale)
+    den = np.where(den == 0, 1e-300, den)
+    return float(np.max(err / den)) if err.size else 0.0
+
+
+def matrix_ok(mine: sp.csr_matrix, ref: sp.csr_matrix):
+    """Union-pattern per-entry check with a 1e-12*max|row| floor."""
+    diff = (sp.csr_matrix(mine) - sp.csr_matrix(ref)).tocsr()
+    rowmax = np.asarray(abs(ref).max(axis=1).todense()).ravel()
+    rowmax = np.maximum(rowmax, np.asarray(abs(mine).max(axis=1).todense()).ravel())
+    worst = 0.0
+    diff = diff.tocoo()
+    refd = sp.csr_matrix(ref)
+    for r, c, v in zip(diff.row, diff.col, diff.data):
+        den = max(abs(refd[r, c]), rowmax[r])
+        if den > 0:
+            worst = max(worst, abs(v) / den)
+    return worst
+
+
+CASES = ["ref_island", "ref_tearing", "bl_island4", "bl_tearing4"]
+
+
+@pytest.fixture(scope="module", params=CASES)
+def case(request, p, golden):
+    import torch
+
+    g = golden(request.param)
+    d = _disc(p, request.param)
+    st = p.SpaceTimeState(p.BlockVector(d.layout, d.n_steps, g["state"]),
+                          torch.as_tensor(g["ic_u"], device="cuda"), torch.as_tensor(g["ic_a"], device="cuda"))
+    jac = p.assemble_jacobian(st, d)
+    pc = p.SpaceTimePreconditioner(jac, d, st)
+    return request.param, g, d, st, jac, pc
+
+
+def test_disc_data(case):
+    _, g, d, *_ = case
+    np.testing.assert_array_equal(d.u_bc_idx, g["u_bc_idx"])
+    np.testing.assert_array_equal(d.a_bc_idx, g["a_bc_idx"])
+    assert np.max(np.abs(d.a_bc_vals - g["a_bc_vals"])) < 1e-15
+    for name, mine in (("p_mean_row", d.p_mean_row), ("e_load", d.e_load), ("current_flux", d.current_flux)):
+        assert np.max(np.abs(mine - g[name])) <= 1e-14 * max(1.0, np.max(np.abs(g[name]))), name
+
+
+def test_initial_state(case, p):
+    _, g, d, *_ = case
+    st0 = p.initial_state(d)
+    assert np.max(np.abs(st0.vec.data.cpu().numpy() - g["state0"])) < 1e-13
+    assert np.max(np.abs(st0.ic_a.cpu().numpy() - g["ic_a"])) < 1e-15
+
+
+def test_residual(case, p):
+    name, g, d, st, *_ = case
+    import torch
+
+    for key, vec in (("r0", g["state0"]), ("r", g["state"])):
+        s = p.SpaceTimeState(p.BlockVector(d.layout, d.n_steps, vec), torch.as_tensor(g["ic_u"], device="cuda"),
+                             torch.as_tensor(g["ic_a"], device="cuda"))
+        mine = p.residual(s, d).data.cpu().numpy()
+        ref = g[key]
+        # floor: 1e-12 of the largest residual entry of the same slab
+        scale = np.repeat(np.abs(ref).reshape(d.n_steps, -1).max(axis=1), d.layout.slab_size)
+        assert entry_ok(mine, ref, 1e-1 * scale) <= TOL_ENTRY * 10, (name, key)
+
+
+def test_jacobian_blocks(case):
+    name, g, d, st, jac, pc = case
+    for k, b in enumerate(jac.slabs):
+        for blk in ("f_u", "z_j", "z_a", "y", "f_a"):
+            w = matrix_ok(getattr(b, blk), csr_from(g, f"s{k}_{blk}"))
+            assert w <= TOL_ENTRY, (name, k, blk, w)
+        assert matrix_ok(pc.f_p[k], csr_from(g, f"s{k}_f_p")) <= TOL_ENTRY
+        assert matrix_ok(pc.c_a[k], csr_from(g, f"s{k}_c_a")) <= 1e-11
+    for k, m in enumerate(pc.c_a_sub1):
+        assert matrix_ok(m, csr_from(g, f"sub1_{k}")) <= 1e-11
+    np.testing.assert_allclose(pc.alfven, g["alfven"], rtol=1e-12, atol=1e-15)
+
+
+def test_jacobian_apply(case):
+    name, g, d, st, jac, pc = case
+    from oracle import model
+
+    od = _oracle_disc(name)
+    ost = model.State(g["state"].copy(), g["ic_u"], g["ic_a"])
+    scale = model.jacobian(ost, od).abs_apply(g["v"])
+    mine = jac.apply(g["v"]).cpu().numpy()
+    assert entry_ok(mine, g["Jv"], scale) <= 4 * TOL_ENTRY
+
+
+def test_preconditioner_apply(case):
+    name, g, d, st, jac, pc = case
+    v = g["v"]
+    nt, L = d.n_steps, d.layout
+    assert relerr(pc.apply_inverse(v).cpu().numpy(), g["Pv"]) < 1e-10
+    assert relerr(pc.apply_forward(v).cpu().numpy(), g["PFv"]) < 1e-10
+    assert relerr(pc.solve_velocity(v[: nt * L.n_u]).cpu().numpy(), g["sv_u"]) < 1e-10
+    assert relerr(pc.solve_wave(v[: nt * L.n_a]).cpu().numpy(), g["sw_a"]) < 1e-10
+    assert relerr(pc.pressure_schur_inverse(v[: nt * L.n_p]).cpu().numpy(), g["psi_p"]) < 1e-10
+    assert relerr(pc.magnetic_schur_inverse(v[: nt * L.n_a]).cpu().numpy(), g["msi_a"]) < 1e-10
+
+
+def test_gmres_newton_step(case, p):
+    name, g, d, *_ = case
+    st0 = p.initial_state(d)
+    jac = p.assemble_jacobian(st0, d)
+    pc = p.SpaceTimePreconditioner(jac, d, st0)
+    r0 = p.residual(st0, d).data
+    cfg = p.GmresConfig(rel_tol=1e-8, abs_tol=1e-300, max_iters=100000, restart=50)
+    res = p.gmres(jac.apply, pc.apply_inverse, -r0, config=cfg)
+    assert abs(res.iterations - int(g["gmres_iters"])) <= 1, (name, res.iterations, int(g["gmres_iters"]))
+    assert relerr(res.x.cpu().numpy(), g["gmres_x"]) < 1e-8
+
+
+def test_config1(p, golden):
+    """BASELINE config 1 (16x16, Nt=8): r0, J.v, P^-1 v and one Newton step
+    with 92 +- 1 FGMRES iterations."""
+    import torch
+
+    g = golden("bl_c1")
+    d = _disc(p, "bl_c1")
+    st0 = p.initial_state(d)
+    assert np.max(np.abs(st0.vec.data.cpu().numpy() - g["state0"])) < 1e-13
+    r0 = p.residual(st0, d).data.cpu().numpy()
+    assert abs(np.linalg.norm(r0) - np.linalg.norm(g["r0"])) < 1e-12 * np.linalg.norm(g["r0"])
+    st = p.SpaceTimeState(p.BlockVector(d.layout, d.n_steps, g["state"]), torch.as_tensor(g["ic_u"], device="cuda"),
+                          torch.as_tensor(g["ic_a"], device="cuda"))
+    jac = p.assemble_jacobian(st, d)
+    pc = p.SpaceTimePreconditioner(jac, d, st)
+    assert relerr(jac.apply(g["v"]).cpu().numpy(), g["Jv"]) < 1e-13
+    assert relerr(pc.apply_inverse(g["v"]).cpu().numpy(), g["Pv"]) < 1e-10
+    cfg = p.NewtonConfig(abs_tol=1e-300, max_iters=1,
+                         gmres=p.GmresConfig(rel_tol=1e-8, abs_tol=1e-300, max_iters=100000, restart=50))
+    state, stats = p.solve_all_at_once(d, cfg)
+    assert stats.newton_iters == 1
+    assert abs(stats.gmres_iters[0] - 92) <= 1, stats.gmres_iters
+    x = state.vec.data.cpu().numpy() - g["state0"]
+    assert relerr(x, g["gmres_x"]) < 1e-8
+    assert abs(stats.residual_norms[1] / stats.residual_norms[0] - 1.0303688174095965e-2) < 1e-6
