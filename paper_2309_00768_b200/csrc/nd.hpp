@@ -53,8 +53,8 @@ struct NDDevice {
   const NDPlan *plan = nullptr;
   DevBuf ns, nb, first, idx_off, idx, child_ptr, child_list, emap_off, emap, scat_ptr,
       scat_src, scat_dst, fl_off, fu_off, front_off, cbv_off, lvl_sn, lvl_ptr;
-  // solve work items: int4 {sn, row_begin, row_end, 0}; per level ranges
-  DevBuf fwd_items, bwd_items;
+  // solve work items: int4 {sn, row_begin, row_end, 0} (32-row chunks); per level ranges
+  DevBuf fwd_items, bwd_items, gather3;  // SolveItem lists + flat forward gather table (int4 per front position)
   std::vector<int> fwd_ptr, bwd_ptr;  // host copies of level ranges (nlevels+1)
   DevBuf fwd_ptr_d, bwd_ptr_d;
   int max_front = 0;
@@ -71,6 +71,16 @@ struct SweepCoupling {
   int64_t val_shift = 0;   // value block used for slab k is (k - val_shift)
   int lag = 0;             // 0 = unused
   double coef = 0.0;
+};
+
+// Flat descriptor of one solve work item: everything a warp needs in one load.
+struct alignas(16) SolveItem {
+  int s, r0, r1, kl;  // supernode, row range, lanes per row
+  int ns, f, pad0, pad1;
+  int64_t foff;   // factor offset (FL^T forward, FU^T backward)
+  int64_t goff;   // offset of the supernode's front lists (idx / gather3)
+  int64_t first;  // elimination position of the first column
+  int64_t cboff;  // update-vector offset
 };
 
 struct NDFactor {
