@@ -51,6 +51,8 @@ typedef struct stmhd_pc_s *stmhd_pc;
 typedef struct stmhd_lu_s *stmhd_lu;
 
 int stmhd_abi_version(void);
+/* number of kernels this library has launched so far (all handles) */
+int64_t stmhd_launch_count(void);
 const char *stmhd_last_error(void);
 /* block name of the last SINGULAR status inside the preconditioner ("F_u", "C_A", ...) */
 const char *stmhd_last_block(void);

@@ -208,19 +208,19 @@ def gmres_mgs(apply_a, apply_pinv, b, rel_tol=1e-2, abs_tol=1e-14, max_iters=200
     cap = max_iters if max_total is None else min(max_iters, max_total)
     while total < cap and not conv:
         m = min(m_restart, cap - total)
-        V = np.zeros((m + 1, n))   # row-major basis (rows are vectors)
+        V = np.zeros((n, m + 1))   # column basis, as the reference stores it
         H = np.zeros((m + 1, m))
         cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
-        V[0] = r / beta
+        V[:, 0] = r / beta
         g[0] = beta
         last = -1
         for j in range(m):
-            w = np.array(apply_a(apply_pinv(V[j])), dtype=float)
+            w = np.array(apply_a(apply_pinv(V[:, j])), dtype=float)
             if not np.all(np.isfinite(w)):
                 raise Breakdown("arnoldi")
             for i in range(j + 1):
-                H[i, j] = V[i] @ w
-                w -= H[i, j] * V[i]
+                H[i, j] = V[:, i] @ w
+                w -= H[i, j] * V[:, i]
             H[j + 1, j] = np.linalg.norm(w)
             for i in range(j):
                 t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
@@ -242,12 +242,12 @@ def gmres_mgs(apply_a, apply_pinv, b, rel_tol=1e-2, abs_tol=1e-14, max_iters=200
                 break
             nw = np.linalg.norm(w)
             if nw > 0:
-                V[j + 1] = w / nw
+                V[:, j + 1] = w / nw
         if last >= 0:
             y = np.zeros(last + 1)
             for i in range(last, -1, -1):
                 y[i] = (g[i] - H[i, i + 1:last + 1] @ y[i + 1:last + 1]) / H[i, i]
-            x = x + apply_pinv(V[:last + 1].T @ y)
+            x = x + apply_pinv(V[:, :last + 1] @ y)
         if conv or total >= cap:
             break
         r = b - apply_a(x)

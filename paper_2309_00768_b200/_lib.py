@@ -21,6 +21,7 @@ P = C.c_void_p  # device/host pointers are passed as integers
 
 _SIGS = {
     "stmhd_abi_version": (c_int, []),
+    "stmhd_launch_count": (c_i64, []),
     "stmhd_last_error": (C.c_char_p, []),
     "stmhd_last_block": (C.c_char_p, []),
     "stmhd_disc_create": (c_int, [C.POINTER(c_vp)]),

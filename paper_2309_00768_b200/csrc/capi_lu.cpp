@@ -4,7 +4,11 @@
 
 #include "nd.hpp"
 
+#include <atomic>
+
 namespace stmhd {
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 static thread_local std::string g_last_error;
 static thread_local std::string g_last_block;
 void set_last_error(const std::string &msg, const std::string &block) {
@@ -37,6 +41,7 @@ struct stmhd_lu_s {
 extern "C" {
 
 int stmhd_abi_version(void) { return 1; }
+int64_t stmhd_launch_count(void) { return stmhd::g_launches.load(); }
 const char *stmhd_last_error(void) { return g_last_error.c_str(); }
 const char *stmhd_last_block(void) { return g_last_block.c_str(); }
 

@@ -31,7 +31,14 @@ void set_last_error(const std::string &msg, const std::string &block = "");
       throw ::stmhd::Error(STMHD_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
   } while (0)
 
-#define STMHD_LAUNCH_CHECK() STMHD_CUDA_CHECK(cudaGetLastError())
+// every kernel launch of the library goes through this check: it also counts
+// launches (stmhd_launch_count) so benchmarks can report what ran natively
+void count_launch();
+#define STMHD_LAUNCH_CHECK()                    \
+  do {                                          \
+    ::stmhd::count_launch();                    \
+    STMHD_CUDA_CHECK(cudaGetLastError());       \
+  } while (0)
 
 inline void require(bool cond, const std::string &msg) {
   if (!cond) throw Error(STMHD_CONFIG, msg);

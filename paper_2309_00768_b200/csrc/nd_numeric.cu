@@ -751,6 +751,7 @@ static void launch_solve(SolveArgs &a, const NDDevice &dev, cudaStream_t s) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     STMHD_CUDA_CHECK(cudaLaunchKernelExC(&cfg, (const void *)nd_solve_kernel<true>, args));
+    count_launch();
   } else {
     static bool attr = false;
     if (!attr) {
@@ -762,6 +763,7 @@ static void launch_solve(SolveArgs &a, const NDDevice &dev, cudaStream_t s) {
     per_sm = std::max(1, std::min(per_sm, 1));
     int grid = per_sm * num_sms();
     STMHD_CUDA_CHECK(cudaLaunchCooperativeKernel((void *)nd_solve_kernel<false>, dim3(grid), dim3(threads), args, smem, s));
+    count_launch();
   }
   if (a.trace) {
     std::vector<unsigned long long> h(nsteps);
