@@ -47,9 +47,67 @@ __global__ void chase_kernel(const int *next, int steps, int nbar, unsigned long
   }
 }
 
+// one warp per CTA of a cluster chases pointers; optionally a cluster barrier
+// (release/acquire) between consecutive loads
+__global__ void chase2_kernel(const int *next, int steps, int with_bar, int64_t nelem, unsigned long long *out) {
+  long long c0 = clock64();
+  int p = (int)((threadIdx.x * 7919ll + blockIdx.x * 104729ll) % nelem);
+  for (int i = 0; i < steps; ++i) {
+    p = next[p];
+    if (with_bar) {
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    }
+  }
+  long long c1 = clock64();
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    out[0] = (unsigned long long)(c1 - c0);
+    out[1] = (unsigned long long)p;
+  }
+}
+
 }  // namespace stmhd
 
 using namespace stmhd;
+
+extern "C" int stmhd_bench_chase2(int64_t nelem, int steps, int cluster, int threads, int with_bar,
+                                  double *cycles_per_step) {
+  try {
+    std::vector<int> perm(nelem), h(nelem);
+    for (int64_t i = 0; i < nelem; ++i) perm[i] = (int)i;
+    uint64_t st = 88172645463325252ull;
+    for (int64_t i = nelem - 1; i > 0; --i) {
+      st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+      int64_t j = st % (i + 1);
+      std::swap(perm[i], perm[j]);
+    }
+    for (int64_t i = 0; i < nelem; ++i) h[perm[i]] = perm[(i + 1) % nelem];
+    DevBuf d = upload_vec(h, 0);
+    DevBuf out(2 * sizeof(unsigned long long));
+    STMHD_CUDA_CHECK(cudaFuncSetAttribute(chase2_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cluster);
+    cfg.blockDim = dim3(threads);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const int *dp = d.as<int>();
+    unsigned long long *op = out.as<unsigned long long>();
+    void *args[] = {&dp, &steps, &with_bar, &nelem, &op};
+    for (int rep = 0; rep < 2; ++rep) STMHD_CUDA_CHECK(cudaLaunchKernelExC(&cfg, (const void *)chase2_kernel, args));
+    unsigned long long r[2];
+    STMHD_CUDA_CHECK(cudaMemcpy(r, out.ptr, sizeof(r), cudaMemcpyDeviceToHost));
+    *cycles_per_step = (double)r[0] / steps;
+    return 0;
+  } catch (const Error &e) {
+    set_last_error(e.what());
+    return e.status;
+  }
+}
 
 extern "C" int stmhd_bench_chase(int64_t nelem, int steps, int cluster, int threads, int nbar, double *ns_per_load,
                                  double *ns_per_barrier) {

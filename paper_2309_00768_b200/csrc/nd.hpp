@@ -16,6 +16,8 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
+#include <memory>
 #include <vector>
 
 #include "common.cuh"
@@ -48,6 +50,32 @@ struct NDPlan {
 NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const int32_t *gx,
                   const int32_t *gy, int leaf_max, const int32_t *value_map);
 
+// Work list of the cluster-resident time sweep (nd_sweep.cu), built lazily for
+// a launch shape: per level and warp, contiguous chunk ranges of one supernode.
+struct alignas(16) SweepTask {
+  int s, c0, c1, kl;  // supernode, chunk range (chunks of 32/kl rows), lanes per row
+  int ns, f, rows, pad;
+  int64_t foff;   // factor offset (FL^T forward, FU^T backward)
+  int64_t goff;   // offset of the supernode's front tables
+  int64_t first;  // elimination position of the first column
+  int64_t cboff;  // update-vector offset
+};
+
+struct NDSweepPlan {
+  int ncta = 0, warps = 0;
+  DevBuf fwd_tasks, bwd_tasks, fwd_wptr, bwd_wptr;
+  DevBuf g3p;   // int4 per front position: {permuted rhs index or -1, cb1, cb2, 0}
+  DevBuf bpos;  // int per front position: permuted position of the front entry
+  DevBuf pos;   // n: elimination position of each original index
+  DevBuf iperm; // n: original index at each elimination position
+  DevBuf seprows;  // permuted rows owned by non-leaf supernodes
+  int64_t nsep = 0;
+  // permuted column indices of coupling matrices, keyed by their column array
+  // (owned by the same discretisation as this plan, so lifetimes match)
+  // {rowptr, colp, eidx} of a coupling matrix in elimination order
+  mutable std::map<const int *, std::unique_ptr<std::vector<DevBuf>>> colp_cache;
+};
+
 // Device-resident copy of a plan plus the solve schedules.
 struct NDDevice {
   const NDPlan *plan = nullptr;
@@ -59,6 +87,8 @@ struct NDDevice {
   DevBuf fwd_ptr_d, bwd_ptr_d;
   int max_front = 0;
   void build(const NDPlan &p, cudaStream_t s);
+  mutable std::unique_ptr<NDSweepPlan> sweep_plan;
+  const NDSweepPlan &get_sweep_plan(int ncta, int warps, cudaStream_t s) const;
 };
 
 // A coupling term of a sequential block sweep:
@@ -98,5 +128,9 @@ struct NDFactor {
              const SweepCoupling *cpl, int ncpl, cudaStream_t s) const;
   int check_status(cudaStream_t s) const;  // synchronises
 };
+
+// Cluster-resident sweep in nested-dissection order (nd_sweep.cu).
+void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,
+              const SweepCoupling *cpl, int ncpl, cudaStream_t s);
 
 }  // namespace stmhd

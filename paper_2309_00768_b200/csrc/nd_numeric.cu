@@ -846,6 +846,11 @@ void NDFactor::solve(const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x,
 
 void NDFactor::sweep(const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,
                      const SweepCoupling *cpl, int ncpl, cudaStream_t s) const {
+  static const int legacy = env_int("STMHD_SWEEP_LEGACY", 0);
+  if (!legacy) {
+    nd_sweep(*this, rhs, ld_rhs, x, ld_x, nrhs, cpl, ncpl, s);
+    return;
+  }
   const NDPlan &p = *dev->plan;
   SolveArgs a = base_args(*dev, factors.as<double>(), nbatch == 1 ? 0 : p.factor_size);
   require(ncpl <= 2, "sweep: at most two coupling terms");
