@@ -233,15 +233,9 @@ def run_ours(args, rank, world):
     clk = clocks.stop()
     launches = int(lib.stmhd_launch_count()) - launches0
     barrier()
-    total_s = sum(ms) / 1e3
-    if world > 1:
-        t = torch.tensor([total_s], dtype=torch.float64, device=dev)
-        n = torch.tensor([float(iters)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(n, op=dist.ReduceOp.SUM)
-        total_s, iters_all = float(t), float(n)
-    else:
-        iters_all = float(iters)
+    from paper_2309_00768_b200.replicas import aggregate
+
+    total_s, iters_all = aggregate(sum(ms) / 1e3, iters, dev)
     value = iters_all / total_s
 
     # ---- e2e through the public API with host buffers ----
@@ -264,13 +258,7 @@ def run_ours(args, rank, world):
         e1.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
         e2e_iters += stats.total_gmres
-    e2e_s = sum(e2e_ms) / 1e3
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        n = torch.tensor([float(e2e_iters)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(n, op=dist.ReduceOp.SUM)
-        e2e_s, e2e_iters = float(t), float(n)
+    e2e_s, e2e_iters = aggregate(sum(e2e_ms) / 1e3, e2e_iters, dev)
     e2e_value = e2e_iters / e2e_s
     h2d = (h_state.numel() + h_icu.numel() + h_ica.numel()) * 8
     d2h = h_out.numel() * 8
