@@ -335,7 +335,7 @@ def run_ours(args, rank, world):
         "phase_s_per_solve": {k: v / args.steps for k, v in breakdown.items()},
         "per_call_ms": per_iter,
         "e2e": {"value": e2e_value, "unit": "FGMRES it/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "roofline": {"kernel": "nd_solve_kernel (F_u time sweep, solve_velocity)", "bound": "hbm",
+        "roofline": {"kernel": "nd_sweep_kernel (F_u time sweep, solve_velocity)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "algorithmic_bytes_per_launch": sweep_bytes,
                      "launch_ms": sweep_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},

@@ -700,7 +700,7 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   a.seprows = sp.seprows.as<int>();
   a.nsep = sp.nsep;
   size_t smem = (size_t)warps * a.vstride * sizeof(double);
-  static const int dsm_env = env_int2("STMHD_SWEEP_DSMEM", 1);
+  static const int dsm_env = env_int2("STMHD_SWEEP_DSMEM", 0);
   const bool use_dsm = dsm_env && (cluster & (cluster - 1)) == 0 &&
                        smem + a.dsm_local * sizeof(double) + 1024 <= 226 * 1024;
   if (use_dsm) smem += a.dsm_local * sizeof(double);

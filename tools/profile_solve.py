@@ -24,9 +24,12 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--solve", type=int, default=1)
     ap.add_argument("--leaf", type=int, default=32)
+    ap.add_argument("--leaf-fu", type=int, default=None)
+    ap.add_argument("--leaf-ca", type=int, default=None)
     args = ap.parse_args()
     t0 = time.perf_counter()
-    d = p.discretize_config(args.config, leaf={"fu": args.leaf, "ca": args.leaf, "const": args.leaf})
+    d = p.discretize_config(args.config, leaf={"fu": args.leaf_fu or args.leaf, "ca": args.leaf_ca or args.leaf,
+                                               "const": args.leaf})
     torch.cuda.synchronize()
     print(f"discretize {time.perf_counter()-t0:.2f}s  device bytes {d.device_bytes()/1e9:.2f} GB  N={d.n_steps*d.layout.slab_size}")
     st = p.initial_state(d)
