@@ -38,8 +38,18 @@ struct NDPlan {
   std::vector<int64_t> scat_ptr;  // per supernode range in scat_src/scat_dst
   std::vector<int64_t> scat_src;  // index into the caller's value array
   std::vector<int64_t> scat_dst;  // position fi*f+fj inside the front
+  // Factor storage (per matrix): for each supernode the forward operator
+  // FL (f x ns) and the backward operator FU (ns x f) are cut into row chunks
+  // of R rows; chunk c is one contiguous block [K][R] (K = ns for FL, f for FU,
+  // rows past the end zero padded, block padded to an even number of doubles),
+  // so a chunk is a single 1D bulk copy.  chunk_f/chunk_b = R per direction.
+  std::vector<int> rf, rb;             // rows per chunk (forward / backward)
+  std::vector<int64_t> bsz_f, bsz_b;   // doubles per chunk block
   std::vector<int64_t> fl_off, fu_off, front_off, cbv_off;
   int64_t factor_size = 0, front_size = 0, cbv_size = 0;
+  // column-major staging layout written by the factorisation kernel
+  std::vector<int64_t> sfl_off, sfu_off;
+  int64_t stage_size = 0;
   int64_t sym_nnz = 0;  // nnz of L+U implied by the supernodal structure
   int max_front = 0;
   std::vector<std::vector<int>> level_sn;
@@ -53,9 +63,9 @@ NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const in
 // Work list of the cluster-resident time sweep (nd_sweep.cu), built lazily for
 // a launch shape: per level and warp, contiguous chunk ranges of one supernode.
 struct alignas(16) SweepTask {
-  int s, c0, c1, kl;  // supernode, chunk range (chunks of 32/kl rows), lanes per row
-  int ns, f, rows, pad;
-  int64_t foff;   // factor offset (FL^T forward, FU^T backward)
+  int s, c0, c1, R;   // supernode, chunk range, rows per chunk
+  int ns, f, rows, bsz;  // bsz: doubles per chunk block
+  int64_t foff;   // offset of chunk 0 (forward FL or backward FU blocks)
   int64_t goff;   // offset of the supernode's front tables
   int64_t first;  // elimination position of the first column
   int64_t cboff;  // update-vector offset
@@ -68,8 +78,6 @@ struct NDSweepPlan {
   DevBuf bpos;  // int per front position: permuted position of the front entry
   DevBuf pos;   // n: elimination position of each original index
   DevBuf iperm; // n: original index at each elimination position
-  DevBuf seprows;  // permuted rows owned by non-leaf supernodes
-  int64_t nsep = 0;
   // permuted column indices of coupling matrices, keyed by their column array
   // (owned by the same discretisation as this plan, so lifetimes match)
   // {rowptr, colp, eidx} of a coupling matrix in elimination order
@@ -80,7 +88,8 @@ struct NDSweepPlan {
 struct NDDevice {
   const NDPlan *plan = nullptr;
   DevBuf ns, nb, first, idx_off, idx, child_ptr, child_list, emap_off, emap, scat_ptr,
-      scat_src, scat_dst, fl_off, fu_off, front_off, cbv_off, lvl_sn, lvl_ptr;
+      scat_src, scat_dst, fl_off, fu_off, sfl_off, sfu_off, rf, rb, bsz_f, bsz_b, front_off, cbv_off, lvl_sn,
+      lvl_ptr;
   // solve work items: int4 {sn, row_begin, row_end, 0} (32-row chunks); per level ranges
   DevBuf fwd_items, bwd_items, gather3;  // SolveItem lists + flat forward gather table (int4 per front position)
   std::vector<int> fwd_ptr, bwd_ptr;  // host copies of level ranges (nlevels+1)
@@ -128,6 +137,37 @@ struct NDFactor {
              const SweepCoupling *cpl, int ncpl, cudaStream_t s) const;
   int check_status(cudaStream_t s) const;  // synchronises
 };
+
+#if defined(__CUDACC__)
+// One warp computes the R rows of a chunk block [K][R] against v[0..K):
+// lane = (kq, rl) with rl = lane % R, kq = lane / R; a warp load touches 32
+// consecutive doubles.  16 loads per lane are issued before the FMAs.  The
+// result is valid in every lane for row rl.
+template <bool GLOBAL>
+__device__ __forceinline__ double chunk_gemv(const double *__restrict__ blk, int R, int K, const double *v, int lane) {
+  const int kl = 32 / R, rl = lane & (R - 1), kq = lane / R;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (K > 0) {
+    for (int t = kq; t < K; t += 16 * kl) {
+      double m[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const double *ptr = blk + (int64_t)min(t + q * kl, K - 1) * R + rl;
+        m[q] = GLOBAL ? __ldg(ptr) : *ptr;
+      }
+      asm volatile("" ::: "memory");
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int tq = t + q * kl;
+        acc[q & 3] = fma(m[q], tq < K ? v[tq] : 0.0, acc[q & 3]);
+      }
+    }
+  }
+  double out = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  for (int o = R; o < 32; o <<= 1) out += __shfl_xor_sync(0xffffffffu, out, o);
+  return out;
+}
+#endif
 
 // Cluster-resident sweep in nested-dissection order (nd_sweep.cu).
 void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,

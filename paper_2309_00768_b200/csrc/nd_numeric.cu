@@ -104,14 +104,14 @@ struct FactorArgs {
   const int64_t *emap_off;
   const int *emap;
   const int64_t *scat_ptr, *scat_src, *scat_dst;
-  const int64_t *fl_off, *fu_off, *front_off;
+  const int64_t *sfl_off, *sfu_off, *front_off;
   const double *values;
   int64_t value_stride;
   int batch0;  // first matrix of this chunk
   double *fronts;
   int64_t front_size;
-  double *factors;
-  int64_t factor_size;
+  double *stage;  // column-major factors of this chunk of matrices (relaid out afterwards)
+  int64_t stage_size;
   int *status;
 };
 
@@ -218,12 +218,12 @@ __global__ void __launch_bounds__(256) nd_factor_level(FactorArgs a) {
     if (tid == 0) atomicCAS(a.status, 0, s + 1);
     return;
   }
-  // 4. inverse-based factors, stored column-major so the solve GEMVs read
-  //    coalesced columns with one thread per output row:
+  // 4. inverse-based factors, column-major in the staging buffer (relaid out
+  //    into row-chunk blocks by nd_relayout afterwards):
   //    FLT[t*f + r] = FL[r][t] (FL = [L11^-1 P ; L21 L11^-1 P], f x ns)
   //    FUT[t*ns + r] = FU[r][t] (FU = [U11^-1 | -U11^-1 U12], ns x f)
-  double *FLT = a.factors + (int64_t)b * a.factor_size + a.fl_off[s];
-  double *FUT = a.factors + (int64_t)b * a.factor_size + a.fu_off[s];
+  double *FLT = a.stage + (int64_t)bl * a.stage_size + a.sfl_off[s];
+  double *FUT = a.stage + (int64_t)bl * a.stage_size + a.sfu_off[s];
   // L11^{-1} P: column i of L^{-1} goes to column perm[i]
   for (int i = tid; i < ns; i += nt) {
     int ci = perm[i];
@@ -258,6 +258,46 @@ __global__ void __launch_bounds__(256) nd_factor_level(FactorArgs a) {
   cta_gemm(nb, ns, ns, -1.0, F + ns, f, FUT, ns, 0.0, FUT + (int64_t)ns * ns, ns, smem, true, false);
 }
 
+// Column-major staging -> row-chunk blocks [K][R] (zero padded).
+__global__ void nd_relayout(const int *lvl_sn_all, const int *ns_, const int *nb_, const int *rf_, const int *rb_,
+                            const int64_t *bszf, const int64_t *bszb, const int64_t *sfl, const int64_t *sfu,
+                            const int64_t *fl, const int64_t *fu, const double *stage, int64_t stage_size,
+                            double *factors, int64_t factor_size, int batch0) {
+  const int s = lvl_sn_all[blockIdx.x];
+  const int bl = blockIdx.y;
+  const int ns = ns_[s], f = ns + nb_[s];
+  const double *st = stage + (int64_t)bl * stage_size;
+  double *fa = factors + (int64_t)(batch0 + bl) * factor_size;
+  // forward FL: rows f, K = ns, staged as FLT[t*f + r]
+  {
+    const int R = rf_[s];
+    const int64_t B = bszf[s];
+    const int nc = (f + R - 1) / R;
+    const int64_t total = (int64_t)nc * B;
+    for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+      const int c = (int)(e / B);
+      const int64_t w = e % B;
+      const int t = (int)(w / R), rl = (int)(w % R);
+      const int r = c * R + rl;
+      fa[fl[s] + e] = (t < ns && r < f) ? st[sfl[s] + (int64_t)t * f + r] : 0.0;
+    }
+  }
+  // backward FU: rows ns, K = f, staged as FUT[t*ns + r]
+  {
+    const int R = rb_[s];
+    const int64_t B = bszb[s];
+    const int nc = (ns + R - 1) / R;
+    const int64_t total = (int64_t)nc * B;
+    for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+      const int c = (int)(e / B);
+      const int64_t w = e % B;
+      const int t = (int)(w / R), rl = (int)(w % R);
+      const int r = c * R + rl;
+      fa[fu[s] + e] = (t < f && r < ns) ? st[sfu[s] + (int64_t)t * ns + r] : 0.0;
+    }
+  }
+}
+
 void NDDevice::build(const NDPlan &p, cudaStream_t s) {
   plan = &p;
   max_front = p.max_front;
@@ -275,6 +315,12 @@ void NDDevice::build(const NDPlan &p, cudaStream_t s) {
   scat_dst = upload_vec(p.scat_dst, s);
   fl_off = upload_vec(p.fl_off, s);
   fu_off = upload_vec(p.fu_off, s);
+  sfl_off = upload_vec(p.sfl_off, s);
+  sfu_off = upload_vec(p.sfu_off, s);
+  rf = upload_vec(p.rf, s);
+  rb = upload_vec(p.rb, s);
+  bsz_f = upload_vec(p.bsz_f, s);
+  bsz_b = upload_vec(p.bsz_b, s);
   front_off = upload_vec(p.front_off, s);
   cbv_off = upload_vec(p.cbv_off, s);
   std::vector<int> lsn, lptr{0};
@@ -284,36 +330,34 @@ void NDDevice::build(const NDPlan &p, cudaStream_t s) {
   }
   lvl_sn = upload_vec(lsn, s);
   lvl_ptr = upload_vec(lptr, s);
-  // solve work items: a warp computes 32/kl rows, kl lanes share each row's K loop
-  auto klanes = [](int K) { return K > 96 ? 8 : (K > 8 ? 4 : 1); };
+  // batched-solve work items: one row chunk (a contiguous factor block) each
   std::vector<SolveItem> fw, bw;
   fwd_ptr.assign(1, 0);
   bwd_ptr.assign(1, 0);
-  auto item = [&](int sn, int r0, int r1, int kl, int64_t foff) {
+  auto item = [&](int sn, int c, int R, int rows, int64_t off) {
     SolveItem it{};
-    it.s = sn; it.r0 = r0; it.r1 = r1; it.kl = kl;
+    it.s = sn; it.r0 = c * R; it.r1 = std::min(rows, (c + 1) * R); it.kl = 32 / R;
     it.ns = p.ns[sn]; it.f = p.ns[sn] + p.nb[sn];
-    it.foff = foff; it.goff = p.idx_off[sn]; it.first = p.first[sn]; it.cboff = p.cbv_off[sn];
+    it.foff = off; it.goff = p.idx_off[sn]; it.first = p.first[sn]; it.cboff = p.cbv_off[sn];
     return it;
   };
   for (int l = 0; l < p.nlevels; ++l) {
     for (int sn : p.level_sn[l]) {
       int f = p.ns[sn] + p.nb[sn];
       if (f == 0) continue;
-      int kl = klanes(p.ns[sn]), rows = 32 / kl;
-      for (int r = 0; r < f; r += rows) fw.push_back(item(sn, r, std::min(f, r + rows), kl, p.fl_off[sn]));
+      int R = p.rf[sn], nc = (f + R - 1) / R;
+      for (int c = 0; c < nc; ++c) fw.push_back(item(sn, c, R, f, p.fl_off[sn] + c * p.bsz_f[sn]));
     }
     fwd_ptr.push_back((int)fw.size());
   }
   for (int l = 0; l < p.nlevels; ++l) {
     for (int sn : p.level_sn[l]) {
-      int n = p.ns[sn], f = p.ns[sn] + p.nb[sn];
-      int kl = klanes(f), rows = 32 / kl;
-      for (int r = 0; r < n; r += rows) bw.push_back(item(sn, r, std::min(n, r + rows), kl, p.fu_off[sn]));
+      int n = p.ns[sn];
+      int R = p.rb[sn], nc = (n + R - 1) / R;
+      for (int c = 0; c < nc; ++c) bw.push_back(item(sn, c, R, n, p.fu_off[sn] + c * p.bsz_b[sn]));
     }
     bwd_ptr.push_back((int)bw.size());
   }
-  // flat forward gather table
   std::vector<int4> g3(p.idx.size(), make_int4(-1, -1, -1, 0));
   for (int sn = 0; sn < p.nsn; ++sn) {
     int64_t o = p.idx_off[sn];
@@ -342,10 +386,11 @@ void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s
   factors.alloc((size_t)nbatch * p.factor_size * sizeof(double));
   if (!status.ptr) status.alloc(sizeof(int));
   STMHD_CUDA_CHECK(cudaMemsetAsync(status.ptr, 0, sizeof(int), s));
-  // chunk the batch so the front workspace stays below ~2 GiB
-  int64_t per = std::max<int64_t>(p.front_size, 1) * (int64_t)sizeof(double);
-  int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t(2) << 30) / per));
-  DevBuf fronts((size_t)chunk * per);
+  // chunk the batch so front workspace + staging stay below ~3 GiB
+  int64_t per = (std::max<int64_t>(p.front_size, 1) + p.stage_size) * (int64_t)sizeof(double);
+  int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t(3) << 30) / per));
+  DevBuf fronts((size_t)chunk * std::max<int64_t>(p.front_size, 1) * sizeof(double));
+  DevBuf stage((size_t)chunk * std::max<int64_t>(p.stage_size, 1) * sizeof(double));
   size_t smem = (2 * GT * GK) * sizeof(double) + (size_t)(p.max_front + 1) * sizeof(int);
   static bool attr_set = false;
   if (smem > 48 * 1024 || !attr_set) {
@@ -372,22 +417,28 @@ void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s
       a.scat_ptr = dev->scat_ptr.as<int64_t>();
       a.scat_src = dev->scat_src.as<int64_t>();
       a.scat_dst = dev->scat_dst.as<int64_t>();
-      a.fl_off = dev->fl_off.as<int64_t>();
-      a.fu_off = dev->fu_off.as<int64_t>();
+      a.sfl_off = dev->sfl_off.as<int64_t>();
+      a.sfu_off = dev->sfu_off.as<int64_t>();
       a.front_off = dev->front_off.as<int64_t>();
       a.values = values;
       a.value_stride = value_stride;
       a.batch0 = b0;
       a.fronts = fronts.as<double>();
       a.front_size = p.front_size;
-      a.factors = factors.as<double>();
-      a.factor_size = p.factor_size;
+      a.stage = stage.as<double>();
+      a.stage_size = p.stage_size;
       a.status = status.as<int>();
       nd_factor_level<<<dim3(cnt, nbch), 256, smem, s>>>(a);
       STMHD_LAUNCH_CHECK();
     }
+    nd_relayout<<<dim3(p.nsn, nbch), 256, 0, s>>>(
+        dev->lvl_sn.as<int>(), dev->ns.as<int>(), dev->nb.as<int>(), dev->rf.as<int>(), dev->rb.as<int>(),
+        dev->bsz_f.as<int64_t>(), dev->bsz_b.as<int64_t>(), dev->sfl_off.as<int64_t>(), dev->sfu_off.as<int64_t>(),
+        dev->fl_off.as<int64_t>(), dev->fu_off.as<int64_t>(), stage.as<double>(), p.stage_size, factors.as<double>(),
+        p.factor_size, b0);
+    STMHD_LAUNCH_CHECK();
   }
-  // keep `fronts` alive until the kernels finish
+  // keep the workspaces alive until the kernels finish
   STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
@@ -399,21 +450,15 @@ int NDFactor::check_status(cudaStream_t s) const {
 }
 
 // ---------------------------------------------------------------------------
-// Persistent solve kernel: warp-granular work items.
-//
-// A work item is (supernode, 32-row chunk); one warp gathers the front vector
-// into its own shared-memory slice and computes its rows with one lane per
-// row over the column-major factor (coalesced, unrolled loads).  Level steps
-// are separated by a barrier: the hardware cluster barrier when the whole
-// kernel is one thread-block cluster (time sweeps: latency bound), or a
-// software grid barrier for batched solves over many right-hand sides.
+// Batched solve (many right-hand sides, e.g. the constant mass/stiffness
+// factors applied to every slab): one cooperative launch over the whole GPU,
+// warp work items = (row chunk, right-hand side), a software grid barrier
+// between tree levels.
 // ---------------------------------------------------------------------------
 struct SolveArgs {
-  const int *ns, *nb;
-  const int64_t *first, *idx_off, *emap_off, *fl_off, *fu_off, *cbv_off;
-  const int *idx, *child_ptr, *child_list, *emap;
   const SolveItem *fwd_items, *bwd_items;
   const int4 *gather3;
+  const int *idx;
   const int *fwd_ptr, *bwd_ptr;
   int nlevels;
   const double *factors;
@@ -423,20 +468,12 @@ struct SolveArgs {
   double *x;
   int64_t ld_x;
   int nrhs;
-  int sweep;  // 1: sequential slabs with coupling
-  SweepCoupling cpl[2];
-  int ncpl;
-  double *ybuf;  // nrhs * n  (indexed by elimination position)
+  double *ybuf;  // nrhs * n (elimination order)
   int64_t n;
   double *cbv;  // nrhs * cbv_size
   int64_t cbv_size;
-  unsigned *bar;  // [0] count, [1] generation
-  int vstride;    // doubles of shared memory per warp
-  double *reff;   // sweep: effective right-hand side of the current slab (n)
-  unsigned long long *trace;  // optional: globaltimer after every level step
-  int prefetch;
-  unsigned long long *wtrace;  // optional: per (step, warp) {gather, gemv} cycles of slab 1
-  int wtrace_nw;
+  unsigned *bar;
+  int vstride;
 };
 
 __device__ __forceinline__ void grid_barrier(unsigned *bar) {
@@ -459,33 +496,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar) {
   __syncthreads();
 }
 
-__device__ __forceinline__ void cluster_barrier() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
-template <bool CLUSTER>
-__device__ __forceinline__ void level_barrier(unsigned *bar) {
-  if (CLUSTER)
-    cluster_barrier();
-  else
-    grid_barrier(bar);
-}
-
-__device__ __forceinline__ void trace_step(const SolveArgs &a, int &step) {
-  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[step] = t;
-  }
-  ++step;
-}
-
-// Gather the front vector of a work item's supernode for right-hand side b
-// into v[0..f): one round for the flat gather table, one for the values
-// (right-hand side + up to two child update vectors, fixed summation order).
-__device__ __forceinline__ void warp_gather(const SolveArgs &a, const double *rhs, const SolveItem &it,
-                                            const double *cb, double *v) {
+__device__ void warp_gather(const SolveArgs &a, const double *rhs, const SolveItem &it, const double *cb, double *v) {
   const int lane = threadIdx.x & 31;
   const int4 *g = a.gather3 + it.goff;
   for (int t0 = lane; t0 < it.f; t0 += 128) {
@@ -510,53 +521,17 @@ __device__ __forceinline__ void warp_gather(const SolveArgs &a, const double *rh
   __syncwarp();
 }
 
-// Rows r0.. of a column-major block: lane = (row sub-index, k-lane).  Loads
-// are issued 16 deep per lane so one item costs a couple of memory latencies.
-__device__ __forceinline__ double warp_gemv(const double *__restrict__ Mt, int64_t ld, int K, const double *v,
-                                            int r, int kl, int kq, bool active) {
-  constexpr int U = 16;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  if (K > 0) {
-    const double *col = Mt + (active ? r : 0);
-    for (int t = kq; t < K; t += U * kl) {
-      double m[U];
-      // unpredicated loads with clamped addresses: all U issue back to back
-#pragma unroll
-      for (int q = 0; q < U; ++q) m[q] = __ldg(col + (int64_t)min(t + q * kl, K - 1) * ld);
-      asm volatile("" ::: "memory");
-#pragma unroll
-      for (int q = 0; q < U; ++q) {
-        const int tq = t + q * kl;
-        acc[q & 3] = fma(m[q], tq < K ? v[tq] : 0.0, acc[q & 3]);
-      }
-    }
-  }
-  double out = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-  for (int o = 1; o < kl; o <<= 1) out += __shfl_xor_sync(0xffffffffu, out, o);
-  return out;
-}
-
-__device__ void warp_forward(const SolveArgs &a, const double *rhs, const SolveItem &it, int b, double *v,
-                             unsigned long long *wt = nullptr) {
+__device__ void warp_forward(const SolveArgs &a, const double *rhs, const SolveItem &it, int b, double *v) {
   double *cb = a.cbv + (int64_t)b * a.cbv_size;
-  long long c0 = clock64();
   warp_gather(a, rhs, it, cb, v);
-  long long c1 = clock64();
-  const int lane = threadIdx.x & 31, kl = it.kl, kq = lane % kl;
-  const int r = it.r0 + lane / kl;
-  const bool active = r < it.r1;
-  const double *FLT = a.factors + (int64_t)b * a.factor_stride + it.foff;
-  const double out = warp_gemv(FLT, it.f, it.ns, v, r, kl, kq, active);
-  if (active && kq == 0) {
+  const int lane = threadIdx.x & 31, R = 32 / it.kl;
+  const int r = it.r0 + (lane & (R - 1));
+  const double out = chunk_gemv<true>(a.factors + (int64_t)b * a.factor_stride + it.foff, R, it.ns, v, lane);
+  if (lane < R && r < it.r1) {
     if (r < it.ns) a.ybuf[(int64_t)b * a.n + it.first + r] = out;
     else cb[it.cboff + r - it.ns] = v[r] - out;
   }
   __syncwarp();
-  if (wt && (threadIdx.x & 31) == 0) {
-    long long c2 = clock64();
-    wt[0] += c1 - c0;
-    wt[1] += c2 - c1;
-  }
 }
 
 __device__ void warp_backward(const SolveArgs &a, const SolveItem &it, int b, double *w) {
@@ -565,10 +540,6 @@ __device__ void warp_backward(const SolveArgs &a, const SolveItem &it, int b, do
   const int *idx = a.idx + it.goff;
   const double *y = a.ybuf + (int64_t)b * a.n + it.first;
   double *x = a.x + (int64_t)b * a.ld_x;
-  const int kl = it.kl, kq = lane % kl;
-  const int r = it.r0 + lane / kl;
-  const bool active = r < it.r1;
-  const int xr = (active && kq == 0) ? idx[r] : 0;
   for (int t0 = lane; t0 < f; t0 += 128) {
     int ii[4];
     double vv[4];
@@ -587,246 +558,44 @@ __device__ void warp_backward(const SolveArgs &a, const SolveItem &it, int b, do
       if (t0 + 32 * q < f) w[t0 + 32 * q] = vv[q];
   }
   __syncwarp();
-  const double *FUT = a.factors + (int64_t)b * a.factor_stride + it.foff;
-  const double out = warp_gemv(FUT, ns, f, w, r, kl, kq, active);
-  if (active && kq == 0) x[xr] = out;
+  const int R = 32 / it.kl;
+  const int r = it.r0 + (lane & (R - 1));
+  const double out = chunk_gemv<true>(a.factors + (int64_t)b * a.factor_stride + it.foff, R, f, w, lane);
+  if (lane < R && r < it.r1) x[idx[r]] = out;
   __syncwarp();
 }
 
-// rhs_eff = rhs_k + sum_c coef_c C_c x_(k-lag_c)  over all rows (4 lanes per row)
-__device__ void sweep_rhs(const SolveArgs &a, int k, double *out, int gw, int nw) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, gl = lane & 3;
-  const double *rhs = a.rhs + (int64_t)k * a.ld_rhs;
-  for (int64_t i0 = (int64_t)gw * 8; i0 < a.n; i0 += (int64_t)nw * 8) {
-    const int64_t i = i0 + g;
-    double acc = 0.0;
-    if (i < a.n) {
-      for (int c = 0; c < a.ncpl; ++c) {
-        const SweepCoupling &cp = a.cpl[c];
-        const int kp = k - cp.lag;
-        if (kp < 0) continue;
-        const double *xv = a.x + (int64_t)kp * a.ld_x;
-        const double *cv = cp.val + (int64_t)(k - cp.val_shift) * cp.val_stride;
-        double part = 0.0;
-        const int e0 = cp.rowptr[i], e1 = cp.rowptr[i + 1];
-#pragma unroll 4
-        for (int e = e0 + gl; e < e1; e += 4) part += cv[e] * xv[cp.col[e]];
-        acc += cp.coef * part;
-      }
-    }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (i < a.n && gl == 0) out[i] = rhs[i] + acc;
-  }
-}
-
-// Pull a byte range into L2 with bulk prefetches (fire and forget).
-__device__ __forceinline__ void l2_prefetch(const void *base, int64_t bytes, int gw, int nw) {
-  const int64_t chunk = 64 * 1024;
-  const char *p = static_cast<const char *>(base);
-  if ((threadIdx.x & 31) != 0) return;
-  for (int64_t off = (int64_t)gw * chunk; off < bytes; off += (int64_t)nw * chunk) {
-    int64_t len = bytes - off < chunk ? bytes - off : chunk;
-    len &= ~int64_t(15);
-    if (len > 0)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p + off), "r"((unsigned)len) : "memory");
-  }
-}
-
-template <bool CLUSTER>
 __global__ void __launch_bounds__(512, 1) nd_solve_kernel(SolveArgs a) {
   extern __shared__ double vbuf[];
-  const int warps_per_cta = blockDim.x >> 5;
-  // interleave warps across CTAs so small levels spread over every SM
   const int gw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
-  const int nw = gridDim.x * warps_per_cta;
+  const int nw = gridDim.x * (blockDim.x >> 5);
   double *v = vbuf + (threadIdx.x >> 5) * a.vstride;
-  const int nslab = a.sweep ? a.nrhs : 1;
-  const int nb_per = a.sweep ? 1 : a.nrhs;
-  const int64_t fbytes = a.factor_stride * (int64_t)sizeof(double);
-  int step = 0;
-  trace_step(a, step);
-  if (a.sweep && a.factor_stride && a.prefetch) l2_prefetch(a.factors, fbytes, gw, nw);
-  for (int k = 0; k < nslab; ++k) {
-    const double *rhs = a.rhs;
-    if (a.sweep) {
-      if (a.prefetch && a.factor_stride && k + 1 < nslab) l2_prefetch(a.factors + (int64_t)(k + 1) * a.factor_stride, fbytes, gw, nw);
-      rhs = a.rhs + (int64_t)k * a.ld_rhs;
-      if (a.ncpl && k > 0) {
-        sweep_rhs(a, k, a.reff, gw, nw);
-        level_barrier<CLUSTER>(a.bar);
-        trace_step(a, step);
-        rhs = a.reff;
-      }
+  for (int l = 0; l < a.nlevels; ++l) {
+    const int i0 = a.fwd_ptr[l], i1 = a.fwd_ptr[l + 1];
+    const int64_t total = (int64_t)(i1 - i0) * a.nrhs;
+    for (int64_t w = gw; w < total; w += nw) {
+      const SolveItem it = a.fwd_items[i0 + (int)(w / a.nrhs)];
+      const int b = (int)(w % a.nrhs);
+      warp_forward(a, a.rhs + (int64_t)b * a.ld_rhs, it, b, v);
     }
-    for (int l = 0; l < a.nlevels; ++l) {
-      const int i0 = a.fwd_ptr[l], i1 = a.fwd_ptr[l + 1];
-      const int64_t total = (int64_t)(i1 - i0) * nb_per;
-      for (int64_t w = gw; w < total; w += nw) {
-        const int item = i0 + (int)(w / nb_per);
-        const int b = a.sweep ? k : (int)(w % nb_per);
-        const SolveItem it = a.fwd_items[item];
-        unsigned long long *wt = (a.wtrace && k == 1) ? a.wtrace + ((int64_t)step * a.wtrace_nw + gw) * 2 : nullptr;
-        warp_forward(a, a.sweep ? rhs : a.rhs + (int64_t)b * a.ld_rhs, it, b, v, wt);
-      }
-      level_barrier<CLUSTER>(a.bar);
-      trace_step(a, step);
+    grid_barrier(a.bar);
+  }
+  for (int l = a.nlevels - 1; l >= 0; --l) {
+    const int i0 = a.bwd_ptr[l], i1 = a.bwd_ptr[l + 1];
+    const int64_t total = (int64_t)(i1 - i0) * a.nrhs;
+    for (int64_t w = gw; w < total; w += nw) {
+      const SolveItem it = a.bwd_items[i0 + (int)(w / a.nrhs)];
+      warp_backward(a, it, (int)(w % a.nrhs), v);
     }
-    for (int l = a.nlevels - 1; l >= 0; --l) {
-      const int i0 = a.bwd_ptr[l], i1 = a.bwd_ptr[l + 1];
-      const int64_t total = (int64_t)(i1 - i0) * nb_per;
-      for (int64_t w = gw; w < total; w += nw) {
-        const int item = i0 + (int)(w / nb_per);
-        const int b = a.sweep ? k : (int)(w % nb_per);
-        const SolveItem it = a.bwd_items[item];
-        warp_backward(a, it, b, v);
-      }
-      if (l > 0 || k + 1 < nslab) level_barrier<CLUSTER>(a.bar);
-      trace_step(a, step);
-    }
+    if (l > 0) grid_barrier(a.bar);
   }
 }
 
-static int env_int(const char *name, int dflt) {
-  const char *e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
-
-static void launch_solve(SolveArgs &a, const NDDevice &dev, cudaStream_t s) {
-  static DevBuf bar;
-  if (!bar.ptr) {
-    bar.alloc(2 * sizeof(unsigned));
-    STMHD_CUDA_CHECK(cudaMemset(bar.ptr, 0, 2 * sizeof(unsigned)));
-  }
-  a.bar = bar.as<unsigned>();
-  a.vstride = std::max(dev.max_front, 1);
-  // sweeps: one cluster (hardware barrier); batched solves: whole GPU
-  static const int cluster = std::max(1, std::min(16, env_int("STMHD_SWEEP_CLUSTER", 16)));
-  const bool use_cluster = a.sweep && cluster > 1;
-  int threads = 512;
-  size_t smem = (size_t)(threads / 32) * a.vstride * sizeof(double);
-  while (smem > 200 * 1024 && threads > 128) {
-    threads /= 2;
-    smem = (size_t)(threads / 32) * a.vstride * sizeof(double);
-  }
-  require(smem <= 227 * 1024, "nd solve: front too large for shared memory");
-  static const int trace_on = env_int("STMHD_SWEEP_TRACE", 0);
-  static const int prefetch_on = env_int("STMHD_SWEEP_PREFETCH", 1);
-  a.prefetch = prefetch_on;
-  static const int same_factor = env_int("STMHD_SWEEP_SAMEFACTOR", 0);  // diagnostics only
-  if (same_factor) a.factor_stride = 0;
-  DevBuf tr;
-  int nsteps = 0;
-  DevBuf wtr;
-  int wnw = 0;
-  if (trace_on && a.sweep) {
-    nsteps = 2 + a.nrhs * (2 * a.nlevels + 1);
-    tr.alloc(nsteps * sizeof(unsigned long long));
-    STMHD_CUDA_CHECK(cudaMemsetAsync(tr.ptr, 0, nsteps * sizeof(unsigned long long), s));
-    a.trace = tr.as<unsigned long long>();
-    wnw = (use_cluster ? cluster : num_sms()) * (threads / 32);
-    wtr.alloc((size_t)nsteps * wnw * 2 * sizeof(unsigned long long));
-    STMHD_CUDA_CHECK(cudaMemsetAsync(wtr.ptr, 0, wtr.bytes, s));
-    a.wtrace = wtr.as<unsigned long long>();
-    a.wtrace_nw = wnw;
-  }
-  void *args[] = {&a};
-  if (use_cluster) {
-    static bool attr = false;
-    if (!attr) {
-      STMHD_CUDA_CHECK(cudaFuncSetAttribute(nd_solve_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      STMHD_CUDA_CHECK(cudaFuncSetAttribute(nd_solve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      attr = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cluster);
-    cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cluster;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    STMHD_CUDA_CHECK(cudaLaunchKernelExC(&cfg, (const void *)nd_solve_kernel<true>, args));
-    count_launch();
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      STMHD_CUDA_CHECK(cudaFuncSetAttribute(nd_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      attr = true;
-    }
-    int per_sm = 0;
-    STMHD_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nd_solve_kernel<false>, threads, smem));
-    per_sm = std::max(1, std::min(per_sm, 1));
-    int grid = per_sm * num_sms();
-    STMHD_CUDA_CHECK(cudaLaunchCooperativeKernel((void *)nd_solve_kernel<false>, dim3(grid), dim3(threads), args, smem, s));
-    count_launch();
-  }
-  if (a.trace) {
-    std::vector<unsigned long long> h(nsteps);
-    STMHD_CUDA_CHECK(cudaMemcpyAsync(h.data(), tr.ptr, nsteps * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-    // per-step durations of slab 1 (steady state): coupling, forward levels, backward levels
-    int per = 2 * a.nlevels + 1;
-    int base = 1 + per;  // after slab 0 (slab 0 has no coupling step)
-    fprintf(stderr, "[trace] n=%lld levels=%d total=%.1f us | slab1 steps (us):", (long long)a.n, a.nlevels,
-            (*std::max_element(h.begin(), h.end()) - h[0]) / 1e3);
-    for (int i = 0; i < per && base + i < nsteps; ++i)
-      fprintf(stderr, " %.2f", (h[base + i] - h[base + i - 1]) / 1e3);
-    fprintf(stderr, "\n");
-    std::vector<unsigned long long> w((size_t)nsteps * wnw * 2);
-    STMHD_CUDA_CHECK(cudaMemcpy(w.data(), wtr.ptr, w.size() * 8, cudaMemcpyDeviceToHost));
-    fprintf(stderr, "[trace] forward steps of slab 1: max-warp gather/gemv cycles (busy warps):");
-    for (int i = 0; i < per && base + i < nsteps; ++i) {
-      unsigned long long mg = 0, mm = 0;
-      int busy = 0;
-      for (int q = 0; q < wnw; ++q) {
-        unsigned long long g = w[((size_t)(base + i - 1) * wnw + q) * 2], m = w[((size_t)(base + i - 1) * wnw + q) * 2 + 1];
-        if (g + m) ++busy;
-        if (g + m > mg + mm) { mg = g; mm = m; }
-      }
-      if (busy) fprintf(stderr, " [%llu/%llu x%d]", mg, mm, busy);
-    }
-    fprintf(stderr, "\n");
-  }
-}
-
-static SolveArgs base_args(const NDDevice &dev, const double *factors, int64_t fstride) {
-  const NDPlan &p = *dev.plan;
-  SolveArgs a{};
-  a.ns = dev.ns.as<int>();
-  a.nb = dev.nb.as<int>();
-  a.first = dev.first.as<int64_t>();
-  a.idx_off = dev.idx_off.as<int64_t>();
-  a.emap_off = dev.emap_off.as<int64_t>();
-  a.fl_off = dev.fl_off.as<int64_t>();
-  a.fu_off = dev.fu_off.as<int64_t>();
-  a.cbv_off = dev.cbv_off.as<int64_t>();
-  a.idx = dev.idx.as<int>();
-  a.child_ptr = dev.child_ptr.as<int>();
-  a.child_list = dev.child_list.as<int>();
-  a.emap = dev.emap.as<int>();
-  a.fwd_items = dev.fwd_items.as<SolveItem>();
-  a.bwd_items = dev.bwd_items.as<SolveItem>();
-  a.gather3 = dev.gather3.as<int4>();
-  a.fwd_ptr = dev.fwd_ptr_d.as<int>();
-  a.bwd_ptr = dev.bwd_ptr_d.as<int>();
-  a.nlevels = p.nlevels;
-  a.factors = factors;
-  a.factor_stride = fstride;
-  a.n = p.n;
-  a.cbv_size = p.cbv_size;
-  return a;
-}
-
-// Scratch for solves, grown on demand (per process; one stream at a time).
+// Scratch for batched solves, grown on demand (per process; one stream at a time).
 static double *solve_scratch(size_t doubles) {
   static DevBuf buf;
   if (buf.bytes < doubles * sizeof(double)) {
-    cudaDeviceSynchronize();
+    STMHD_CUDA_CHECK(cudaDeviceSynchronize());
     buf.alloc(doubles * sizeof(double) * 5 / 4 + 1024);
   }
   return buf.as<double>();
@@ -835,34 +604,50 @@ static double *solve_scratch(size_t doubles) {
 void NDFactor::solve(const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,
                      cudaStream_t s) const {
   const NDPlan &p = *dev->plan;
-  SolveArgs a = base_args(*dev, factors.as<double>(), nbatch == 1 ? 0 : p.factor_size);
   require(nbatch == 1 || nrhs <= nbatch, "lu solve: more right-hand sides than factors");
+  static DevBuf bar;
+  if (!bar.ptr) {
+    bar.alloc(2 * sizeof(unsigned));
+    STMHD_CUDA_CHECK(cudaMemset(bar.ptr, 0, 2 * sizeof(unsigned)));
+  }
+  SolveArgs a{};
+  a.fwd_items = dev->fwd_items.as<SolveItem>();
+  a.bwd_items = dev->bwd_items.as<SolveItem>();
+  a.gather3 = dev->gather3.as<int4>();
+  a.idx = dev->idx.as<int>();
+  a.fwd_ptr = dev->fwd_ptr_d.as<int>();
+  a.bwd_ptr = dev->bwd_ptr_d.as<int>();
+  a.nlevels = p.nlevels;
+  a.factors = factors.as<double>();
+  a.factor_stride = nbatch == 1 ? 0 : p.factor_size;
+  a.rhs = rhs;
+  a.ld_rhs = ld_rhs;
+  a.x = x;
+  a.ld_x = ld_x;
+  a.nrhs = nrhs;
   double *scr = solve_scratch((size_t)nrhs * (p.n + p.cbv_size));
-  a.rhs = rhs; a.ld_rhs = ld_rhs; a.x = x; a.ld_x = ld_x; a.nrhs = nrhs; a.sweep = 0; a.ncpl = 0;
   a.ybuf = scr;
+  a.n = p.n;
   a.cbv = scr + (int64_t)nrhs * p.n;
-  launch_solve(a, *dev, s);
+  a.cbv_size = p.cbv_size;
+  a.bar = bar.as<unsigned>();
+  a.vstride = std::max(dev->max_front, 1) + 8;
+  const int threads = 512;
+  const size_t smem = (size_t)(threads / 32) * a.vstride * sizeof(double);
+  require(smem <= 220 * 1024, "nd solve: front too large for shared memory");
+  static bool attr = false;
+  if (!attr) {
+    STMHD_CUDA_CHECK(cudaFuncSetAttribute(nd_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr = true;
+  }
+  void *args[] = {&a};
+  STMHD_CUDA_CHECK(cudaLaunchCooperativeKernel((void *)nd_solve_kernel, dim3(num_sms()), dim3(threads), args, smem, s));
+  count_launch();
 }
 
 void NDFactor::sweep(const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,
                      const SweepCoupling *cpl, int ncpl, cudaStream_t s) const {
-  static const int legacy = env_int("STMHD_SWEEP_LEGACY", 0);
-  if (!legacy) {
-    nd_sweep(*this, rhs, ld_rhs, x, ld_x, nrhs, cpl, ncpl, s);
-    return;
-  }
-  const NDPlan &p = *dev->plan;
-  SolveArgs a = base_args(*dev, factors.as<double>(), nbatch == 1 ? 0 : p.factor_size);
-  require(ncpl <= 2, "sweep: at most two coupling terms");
-  require(nbatch == 1 || nrhs <= nbatch, "sweep: more slabs than factors");
-  double *scr = solve_scratch((size_t)nrhs * (p.n + p.cbv_size) + p.n);
-  a.rhs = rhs; a.ld_rhs = ld_rhs; a.x = x; a.ld_x = ld_x; a.nrhs = nrhs; a.sweep = 1;
-  a.reff = scr + (int64_t)nrhs * (p.n + p.cbv_size);
-  a.ncpl = ncpl;
-  for (int i = 0; i < ncpl; ++i) a.cpl[i] = cpl[i];
-  a.ybuf = scr;
-  a.cbv = scr + (int64_t)nrhs * p.n;
-  launch_solve(a, *dev, s);
+  nd_sweep(*this, rhs, ld_rhs, x, ld_x, nrhs, cpl, ncpl, s);
 }
 
 }  // namespace stmhd

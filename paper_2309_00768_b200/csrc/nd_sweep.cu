@@ -4,17 +4,20 @@
 //
 //   x_k = A_k^{-1} ( rhs_k + sum_c coef_c C_c x_{k-lag_c} ),  k = 0..nt-1.
 //
-// The slabs are strictly sequential, so the sweep is latency bound: one
-// thread-block cluster (hardware barrier between tree levels) runs the whole
-// sweep in a single launch.  Everything inside runs in the nested-dissection
-// ordering: a supernode's own unknowns are a contiguous range, so front
-// gathers and result stores are coalesced.  The right-hand sides are permuted
-// in and the solutions permuted out by two bandwidth-bound kernels around the
-// sweep.  Each warp owns a contiguous range of row chunks of one supernode
-// per task, so a front is gathered once per warp; factor columns are read
-// with 16 loads in flight per lane.
-#include <cooperative_groups.h>
-
+// The slabs are strictly sequential, so the sweep is latency bound.  One
+// thread-block cluster runs the whole sweep in a single launch (hardware
+// cluster barrier between tree levels; a software grid barrier costs 2.3 us,
+// tools/bench_barrier.py).  Inside:
+//  * everything runs in the nested-dissection ordering, so a supernode's own
+//    unknowns are contiguous; rhs / solutions are permuted in and out by two
+//    bandwidth-bound kernels around the sweep;
+//  * each warp owns a contiguous range of row chunks of one supernode per
+//    level (LPT balanced); a chunk's factor block [K][R] is one contiguous
+//    range that the TMA engine copies into the warp's shared-memory slot
+//    (cp.async.bulk + mbarrier, double buffered), overlapped with the front
+//    gather; the GEMV then reads shared memory;
+//  * the next slab's factors are bulk-prefetched into L2 while a slab runs;
+//  * couplings are ELL tables in elimination order.
 #include <algorithm>
 #include <cstdlib>
 #include <map>
@@ -22,6 +25,11 @@
 #include "nd.hpp"
 
 namespace stmhd {
+
+static int env_int2(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
 
 const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, cudaStream_t s) const {
   if (sweep_plan && sweep_plan->ncta == ncta && sweep_plan->warps == warps) return *sweep_plan;
@@ -61,39 +69,22 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, cudaStream_t s)
     std::vector<int> wptr;
     for (int l = 0; l < p.nlevels; ++l) {
       struct SN {
-        int s, rows, K, kl, R, m;
-        double cost_gather, cost_chunk;
+        int s, rows, K, R, m;
+        double cg, cc;
       };
       std::vector<SN> sns;
-      // lanes per row: if the level's finest chunking still leaves warps idle, use
-      // 8 lanes per row (most parallel chunks, fewest rounds per chunk); otherwise
-      // minimise the total number of serial load rounds
-      int64_t chunks8 = 0;
-      for (int sn : p.level_sn[l]) {
-        int rows = fwd ? p.ns[sn] + p.nb[sn] : p.ns[sn];
-        chunks8 += (rows + 3) / 4;
-      }
-      const bool rich = chunks8 <= W;
       for (int sn : p.level_sn[l]) {
         int f = p.ns[sn] + p.nb[sn];
         int rows = fwd ? f : p.ns[sn];
         if (rows == 0) continue;
         int K = fwd ? p.ns[sn] : f;
-        int kl = 8;
-        if (!rich) {
-          int best = INT32_MAX;
-          for (int c : {1, 2, 4, 8}) {
-            int Rc = 32 / c, mc = (rows + Rc - 1) / Rc, rounds = mc * std::max(1, (K + 16 * c - 1) / (16 * c));
-            if (rounds <= best) { best = rounds; kl = c; }
-          }
-        }
-        int R = 32 / kl;
+        int R = fwd ? p.rf[sn] : p.rb[sn];
         int m = (rows + R - 1) / R;
-        sns.push_back({sn, rows, K, kl, R, m, 2.0 * ((f + 255) / 256), 1.0 + (double)((K + 16 * kl - 1) / (16 * kl))});
+        // cost model in memory rounds: gather ~2, one chunk ~1 + K/(16 kl)
+        sns.push_back({sn, rows, K, R, m, 2.0, 1.0 + (double)((K + 16 * (32 / R) - 1) / (16 * (32 / R)))});
       }
-      // pieces: split big supernodes so every warp gets work, then LPT onto warps
       double total = 0;
-      for (auto &x : sns) total += x.cost_gather + x.m * x.cost_chunk;
+      for (auto &x : sns) total += x.cg + x.m * x.cc;
       struct Piece {
         int idx, c0, c1;
         double cost;
@@ -101,12 +92,12 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, cudaStream_t s)
       std::vector<Piece> pieces;
       for (int i = 0; i < (int)sns.size(); ++i) {
         auto &x = sns[i];
-        double c = x.cost_gather + x.m * x.cost_chunk;
+        double c = x.cg + x.m * x.cc;
         int np = 1;
         if ((int)sns.size() < W) np = std::max(1, std::min(x.m, (int)(W * c / total)));
         for (int q = 0; q < np; ++q) {
           int c0 = (int)((int64_t)x.m * q / np), c1 = (int)((int64_t)x.m * (q + 1) / np);
-          if (c1 > c0) pieces.push_back({i, c0, c1, x.cost_gather + (c1 - c0) * x.cost_chunk});
+          if (c1 > c0) pieces.push_back({i, c0, c1, x.cg + (c1 - c0) * x.cc});
         }
       }
       std::sort(pieces.begin(), pieces.end(), [](const Piece &a, const Piece &b) { return a.cost > b.cost; });
@@ -122,8 +113,9 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, cudaStream_t s)
         for (auto &pc : per[w]) {
           auto &x = sns[pc.idx];
           SweepTask t{};
-          t.s = x.s; t.c0 = pc.c0; t.c1 = pc.c1; t.kl = x.kl;
+          t.s = x.s; t.c0 = pc.c0; t.c1 = pc.c1; t.R = x.R;
           t.ns = p.ns[x.s]; t.f = p.ns[x.s] + p.nb[x.s]; t.rows = x.rows;
+          t.bsz = (int)(fwd ? p.bsz_f[x.s] : p.bsz_b[x.s]);
           t.foff = fwd ? p.fl_off[x.s] : p.fu_off[x.s];
           t.goff = p.idx_off[x.s]; t.first = p.first[x.s]; t.cboff = p.cbv_off[x.s];
           tasks.push_back(t);
@@ -140,22 +132,15 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, cudaStream_t s)
   sp->bpos = upload_vec(bpos, s);
   sp->pos = upload_vec(pos, s);
   sp->iperm = upload_vec(iperm, s);
-  std::vector<int> sep;
-  for (int sn = 0; sn < p.nsn; ++sn)
-    if (p.level[sn] > 0)
-      for (int t = 0; t < p.ns[sn]; ++t) sep.push_back((int)(p.first[sn] + t));
-  sp->nsep = (int64_t)sep.size();
-  if (sep.empty()) sep.push_back(0);
-  sp->seprows = upload_vec(sep, s);
   STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
   sweep_plan = std::move(sp);
   return *sweep_plan;
 }
 
 struct SweepCpl {
-  int width;                 // ELL width (max entries per row)
-  const int *colp;           // [j*n + q]: permuted column of slot j of permuted row q (-1: pad)
-  const int *eidx;           // original entry index of that slot (value lookup)
+  int width;        // ELL width (max entries per row)
+  const int *colp;  // [j*n + q]: permuted column of slot j of permuted row q (-1: pad)
+  const int *eidx;  // original entry index of that slot (value lookup)
   const double *val;
   int64_t val_stride, val_shift;
   int lag;
@@ -166,7 +151,7 @@ struct SweepArgs {
   const SweepTask *ftask, *btask;
   const int *fwptr, *bwptr;  // per level W entries (+ one final sentinel)
   const int4 *g3p;
-  const int *bpos, *iperm;
+  const int *bpos;
   int nlevels, nw;
   int64_t n;
   const double *factors;
@@ -177,16 +162,10 @@ struct SweepArgs {
   int nslab;
   SweepCpl cpl[2];
   int ncpl;
-  int vstride;
+  int vstride;  // doubles per warp: gather buffer + 2 TMA slots
+  int slot;     // doubles per TMA slot (largest chunk block)
   int prefetch;
   unsigned long long *trace;
-  unsigned long long *wtrace;  // per (step, warp): {task-load, gather, gemv} cycles (slab 1 only)
-  // distributed-shared-memory layout (nd_sweep_dsm_kernel)
-  int ncta, lc;        // cluster size and log2
-  int64_t dsm_local;   // doubles of the distributed vectors held by each CTA
-  const int *seprows;  // permuted rows of non-leaf supernodes
-  int64_t nsep;
-  const double *rhs_g; // unused placeholder
 };
 
 __device__ __forceinline__ void sweep_barrier() {
@@ -194,48 +173,61 @@ __device__ __forceinline__ void sweep_barrier() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-__device__ __forceinline__ double sweep_gemv(const double *__restrict__ Mt, int64_t ld, int K, const double *v,
-                                             int r, int kl, int kq, bool active) {
-  constexpr int U = 16;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  const double *col = Mt + (active ? r : 0);
-  for (int t = kq; t < K; t += U * kl) {
-    double m[U];
-#pragma unroll
-    for (int q = 0; q < U; ++q) m[q] = __ldg(col + (int64_t)min(t + q * kl, K - 1) * ld);
-    asm volatile("" ::: "memory");
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      const int tq = t + q * kl;
-      acc[q & 3] = fma(m[q], tq < K ? v[tq] : 0.0, acc[q & 3]);
-    }
-  }
-  double out = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-  for (int o = 1; o < kl; o <<= 1) out += __shfl_xor_sync(0xffffffffu, out, o);
-  return out;
-}
-
 __device__ __forceinline__ void sweep_trace(const SweepArgs &a, int &step) {
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[step] = t;
-    if (a.wtrace) a.wtrace[step] = (unsigned long long)clock64();  // SM cycles beside the wall clock
   }
   ++step;
 }
 
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// one lane: stream `dbl` doubles from global `src` into shared `dst`, completing on `bar`
+__device__ __forceinline__ void tma_load(double *dst, const double *src, int dbl, unsigned long long *bar) {
+  const unsigned bytes = (unsigned)dbl * 8u;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
 __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
-  extern __shared__ double vbuf[];
-  const int lane = threadIdx.x & 31;
-  const int gw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;  // interleaved across CTAs
-  double *v = vbuf + (threadIdx.x >> 5) * a.vstride;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) unsigned long long mbar[16][2];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int gw = wl * gridDim.x + blockIdx.x;  // interleaved across CTAs
+  double *v = sm + wl * a.vstride;
+  double *slot[2] = {v + (a.vstride - 2 * a.slot), v + (a.vstride - a.slot)};
+  unsigned phase[2] = {0u, 0u};
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[wl][0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[wl][1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
   const int64_t n = a.n;
   int step = 0;
   sweep_trace(a, step);
   for (int k = 0; k < a.nslab; ++k) {
     if (a.prefetch && a.fstride && k + 1 < a.nslab && lane == 0) {
-      // pull the next slab's factors into L2 while this slab runs
       const char *base = reinterpret_cast<const char *>(a.factors + (int64_t)(k + 1) * a.fstride);
       const int64_t bytes = a.fstride * 8, chunk = 32 * 1024;
       for (int64_t off = (int64_t)gw * chunk; off < bytes; off += (int64_t)a.nw * chunk) {
@@ -248,8 +240,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
     const double *rhs = a.rhsp + (int64_t)k * n;
     double *x = a.xp + (int64_t)k * n;
     if (k > 0 && a.ncpl) {
-      // rhs_eff = rhs_k + sum_c coef_c C_c x_{k-lag}: one permuted row per thread,
-      // ELL slots loaded 8 at a time (coalesced across threads)
+      // rhs_eff = rhs_k + sum_c coef_c C_c x_{k-lag}: one permuted row per thread
       const int64_t nth = (int64_t)a.nw * 32;
       for (int64_t pr = (int64_t)gw * 32 + lane; pr < n; pr += nth) {
         double acc = 0.0;
@@ -285,13 +276,16 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
     const double *F = a.factors + (int64_t)k * a.fstride;
     // ---- forward (L) levels, bottom-up ----
     for (int l = 0; l < a.nlevels; ++l) {
-      const int *wp = a.fwptr + (int64_t)l * a.nw;  // nw entries per level + final sentinel
+      const int *wp = a.fwptr + (int64_t)l * a.nw;
       const int t0 = wp[gw], t1 = wp[gw + 1];
       for (int ti = t0; ti < t1; ++ti) {
-        long long c0 = clock64();
         const SweepTask tk = a.ftask[ti];
+        // start streaming the first two factor chunks, then gather the front
+        if (lane == 0) {
+          tma_load(slot[0], F + tk.foff + (int64_t)tk.c0 * tk.bsz, tk.bsz, &mbar[wl][0]);
+          if (tk.c0 + 1 < tk.c1) tma_load(slot[1], F + tk.foff + (int64_t)(tk.c0 + 1) * tk.bsz, tk.bsz, &mbar[wl][1]);
+        }
         const int4 *g = a.g3p + tk.goff;
-        long long c1 = clock64() + (tk.f & 0);
         for (int b0 = lane; b0 < tk.f; b0 += 256) {
           int4 gg[8];
 #pragma unroll
@@ -306,26 +300,21 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
             if (b0 + 32 * q < tk.f) v[b0 + 32 * q] = vv[q];
         }
         __syncwarp();
-        long long c2 = clock64();
-        const int kl = tk.kl, kq = lane % kl, R = 32 / kl;
-        const double *FLT = F + tk.foff;
+        const int R = tk.R;
         for (int c = tk.c0; c < tk.c1; ++c) {
-          const int r = c * R + lane / kl;
-          const bool act = r < tk.rows;
-          const double out = sweep_gemv(FLT, tk.f, tk.ns, v, r, kl, kq, act);
-          if (act && kq == 0) {
+          const int sl = (c - tk.c0) & 1;
+          mbar_wait(&mbar[wl][sl], phase[sl]);
+          phase[sl] ^= 1u;
+          const double out = chunk_gemv<false>(slot[sl], R, tk.ns, v, lane);
+          const int r = c * R + (lane & (R - 1));
+          if (lane < R && r < tk.rows) {
             if (r < tk.ns) a.ybuf[tk.first + r] = out;
             else a.cbv[tk.cboff + r - tk.ns] = v[r] - out;
           }
+          __syncwarp();
+          if (lane == 0 && c + 2 < tk.c1) tma_load(slot[sl], F + tk.foff + (int64_t)(c + 2) * tk.bsz, tk.bsz, &mbar[wl][sl]);
         }
         __syncwarp();
-        if (a.wtrace && k == 1 && lane == 0) {
-          long long c3 = clock64();
-          unsigned long long *w = a.wtrace + ((int64_t)step * a.nw + gw) * 3;
-          w[0] += c1 - c0;
-          w[1] += c2 - c1;
-          w[2] += c3 - c2;
-        }
       }
       sweep_barrier();
       sweep_trace(a, step);
@@ -336,6 +325,10 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
       const int t0 = wp[gw], t1 = wp[gw + 1];
       for (int ti = t0; ti < t1; ++ti) {
         const SweepTask tk = a.btask[ti];
+        if (lane == 0) {
+          tma_load(slot[0], F + tk.foff + (int64_t)tk.c0 * tk.bsz, tk.bsz, &mbar[wl][0]);
+          if (tk.c0 + 1 < tk.c1) tma_load(slot[1], F + tk.foff + (int64_t)(tk.c0 + 1) * tk.bsz, tk.bsz, &mbar[wl][1]);
+        }
         const int *bp = a.bpos + tk.goff;
         const double *y = a.ybuf + tk.first;
         for (int b0 = lane; b0 < tk.f; b0 += 256) {
@@ -356,13 +349,16 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
             if (b0 + 32 * q < tk.f) v[b0 + 32 * q] = vv[q];
         }
         __syncwarp();
-        const int kl = tk.kl, kq = lane % kl, R = 32 / kl;
-        const double *FUT = F + tk.foff;
+        const int R = tk.R;
         for (int c = tk.c0; c < tk.c1; ++c) {
-          const int r = c * R + lane / kl;
-          const bool act = r < tk.rows;
-          const double out = sweep_gemv(FUT, tk.ns, tk.f, v, r, kl, kq, act);
-          if (act && kq == 0) x[tk.first + r] = out;
+          const int sl = (c - tk.c0) & 1;
+          mbar_wait(&mbar[wl][sl], phase[sl]);
+          phase[sl] ^= 1u;
+          const double out = chunk_gemv<false>(slot[sl], R, tk.f, v, lane);
+          const int r = c * R + (lane & (R - 1));
+          if (lane < R && r < tk.rows) x[tk.first + r] = out;
+          __syncwarp();
+          if (lane == 0 && c + 2 < tk.c1) tma_load(slot[sl], F + tk.foff + (int64_t)(c + 2) * tk.bsz, tk.bsz, &mbar[wl][sl]);
         }
         __syncwarp();
       }
@@ -370,195 +366,6 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
       sweep_trace(a, step);
     }
   }
-}
-
-
-// ---------------------------------------------------------------------------
-// Distributed-shared-memory variant.  All vectors exchanged between tree
-// levels inside a slab (x ring for the lag-1/2 couplings, y, effective rhs,
-// update vectors) live in the cluster's shared memory, interleaved across the
-// CTAs in 32-element blocks; only read-only data (factors, rhs, coupling
-// matrices) is read from global memory, and each slab's solution is written
-// back once.  The level barrier then never waits on global stores.
-// ---------------------------------------------------------------------------
-namespace cg = cooperative_groups;
-
-struct Dsm {
-  double *rb[16];
-  int cmask, shift;
-  __device__ __forceinline__ double *at(int64_t e) const {
-    return rb[(e >> 5) & cmask] + (((e >> shift) << 5) | (e & 31));
-  }
-};
-
-// sum_c coef_c (C_c x_{k-lag_c})[pr] with the x ring in distributed shared memory
-__device__ __forceinline__ double coupling_row(const SweepArgs &a, const Dsm &dm, int k, int64_t pr) {
-  const int64_t n = a.n;
-  double acc = 0.0;
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    if (c >= a.ncpl) break;
-    const SweepCpl &cp = a.cpl[c];
-    const int kp = k - cp.lag;
-    if (kp < 0) continue;
-    const int64_t xl = (int64_t)(kp % 3) * n;
-    const double *cv = cp.val + (k - cp.val_shift) * cp.val_stride;
-    double part = 0.0;
-    for (int j0 = 0; j0 < cp.width; j0 += 8) {
-      int ci[8], ei[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const bool ok = j0 + q < cp.width;
-        ci[q] = ok ? cp.colp[(int64_t)(j0 + q) * n + pr] : -1;
-        ei[q] = ok ? cp.eidx[(int64_t)(j0 + q) * n + pr] : 0;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (ci[q] >= 0) part += cv[ei[q]] * *dm.at(xl + ci[q]);
-    }
-    acc += cp.coef * part;
-  }
-  return acc;
-}
-
-__global__ void __launch_bounds__(512, 1) nd_sweep_dsm_kernel(SweepArgs a) {
-  extern __shared__ double sm[];
-  __shared__ Dsm D;
-  cg::cluster_group cl = cg::this_cluster();
-  double *local = sm;
-  if (threadIdx.x < a.ncta) D.rb[threadIdx.x] = cl.map_shared_rank(local, (int)threadIdx.x);
-  if (threadIdx.x == 0) {
-    D.cmask = a.ncta - 1;
-    D.shift = 5 + a.lc;
-  }
-  const int lane = threadIdx.x & 31;
-  const int gw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
-  double *v = sm + a.dsm_local + (threadIdx.x >> 5) * a.vstride;
-  const int64_t n = a.n;
-  const int64_t XR = 0, Y = 3 * n, RF = 4 * n, CB = 5 * n;
-  cl.sync();
-  const Dsm &dm = D;  // remote bases stay in shared memory (no local-memory copy)
-  int step = 0;
-  sweep_trace(a, step);
-  const int64_t nth = (int64_t)a.nw * 32;
-  const int64_t tid = (int64_t)gw * 32 + lane;
-  for (int k = 0; k < a.nslab; ++k) {
-    if (a.prefetch && a.fstride && k + 1 < a.nslab && lane == 0) {
-      const char *base = reinterpret_cast<const char *>(a.factors + (int64_t)(k + 1) * a.fstride);
-      const int64_t bytes = a.fstride * 8, chunk = 32 * 1024;
-      for (int64_t off = (int64_t)gw * chunk; off < bytes; off += (int64_t)a.nw * chunk) {
-        int64_t len = min(chunk, bytes - off) & ~int64_t(15);
-        if (len > 0)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base + off), "r"((unsigned)len)
-                       : "memory");
-      }
-    }
-    const double *rhs = a.rhsp + (int64_t)k * n;
-    const int64_t xs = XR + (int64_t)(k % 3) * n;
-    const bool coupled = k > 0 && a.ncpl;
-    const double *F = a.factors + (int64_t)k * a.fstride;
-    for (int l = 0; l < a.nlevels; ++l) {
-      if (l == 0 && k > 0) {
-        // previous slab's solution to global memory; coupling rows of the
-        // separators (leaves compute their own rows' coupling in their gather)
-        const int64_t xprev = XR + (int64_t)((k - 1) % 3) * n;
-        double *xout = a.xp + (int64_t)(k - 1) * n;
-        for (int64_t pr = tid; pr < n; pr += nth) xout[pr] = *dm.at(xprev + pr);
-        if (coupled)
-          for (int64_t q = tid; q < a.nsep; q += nth) {
-            const int64_t pr = a.seprows[q];
-            *dm.at(RF + pr) = rhs[pr] + coupling_row(a, dm, k, pr);
-          }
-      }
-      const int *wp = a.fwptr + (int64_t)l * a.nw;
-      const int t0 = wp[gw], t1 = wp[gw + 1];
-      for (int ti = t0; ti < t1; ++ti) {
-        const SweepTask tk = a.ftask[ti];
-        const int4 *g = a.g3p + tk.goff;
-        for (int b0 = lane; b0 < tk.f; b0 += 256) {
-          int4 gg[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) gg[q] = (b0 + 32 * q < tk.f) ? g[b0 + 32 * q] : make_int4(-1, -1, -1, 0);
-          double vv[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            double r = 0.0;
-            if (gg[q].x >= 0) {
-              if (!coupled) r = rhs[gg[q].x];
-              else if (l == 0) r = rhs[gg[q].x] + coupling_row(a, dm, k, gg[q].x);
-              else r = *dm.at(RF + gg[q].x);
-            }
-            const double c1 = gg[q].y >= 0 ? *dm.at(CB + gg[q].y) : 0.0;
-            const double c2 = gg[q].z >= 0 ? *dm.at(CB + gg[q].z) : 0.0;
-            vv[q] = (r + c1) + c2;
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (b0 + 32 * q < tk.f) v[b0 + 32 * q] = vv[q];
-        }
-        __syncwarp();
-        const int kl = tk.kl, kq = lane % kl, R = 32 / kl;
-        const double *FLT = F + tk.foff;
-        for (int c = tk.c0; c < tk.c1; ++c) {
-          const int r = c * R + lane / kl;
-          const bool act = r < tk.rows;
-          const double out = sweep_gemv(FLT, tk.f, tk.ns, v, r, kl, kq, act);
-          if (act && kq == 0) {
-            if (r < tk.ns) *dm.at(Y + tk.first + r) = out;
-            else *dm.at(CB + tk.cboff + r - tk.ns) = v[r] - out;
-          }
-        }
-        __syncwarp();
-      }
-      cl.sync();
-      sweep_trace(a, step);
-    }
-    for (int l = a.nlevels - 1; l >= 0; --l) {
-      const int *wp = a.bwptr + (int64_t)l * a.nw;
-      const int t0 = wp[gw], t1 = wp[gw + 1];
-      for (int ti = t0; ti < t1; ++ti) {
-        const SweepTask tk = a.btask[ti];
-        const int *bp = a.bpos + tk.goff;
-        for (int b0 = lane; b0 < tk.f; b0 += 256) {
-          int ii[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int t = b0 + 32 * q;
-            ii[q] = (t >= tk.ns && t < tk.f) ? bp[t] : -1;
-          }
-          double vv[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int t = b0 + 32 * q;
-            vv[q] = t < tk.ns ? *dm.at(Y + tk.first + t) : (ii[q] >= 0 ? *dm.at(xs + ii[q]) : 0.0);
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (b0 + 32 * q < tk.f) v[b0 + 32 * q] = vv[q];
-        }
-        __syncwarp();
-        const int kl = tk.kl, kq = lane % kl, R = 32 / kl;
-        const double *FUT = F + tk.foff;
-        for (int c = tk.c0; c < tk.c1; ++c) {
-          const int r = c * R + lane / kl;
-          const bool act = r < tk.rows;
-          const double out = sweep_gemv(FUT, tk.ns, tk.f, v, r, kl, kq, act);
-          if (act && kq == 0) *dm.at(xs + tk.first + r) = out;
-        }
-        __syncwarp();
-      }
-      cl.sync();
-      sweep_trace(a, step);
-    }
-  }
-  // last slab's solution
-  {
-    const int k = a.nslab - 1;
-    const int64_t xs = XR + (int64_t)(k % 3) * n;
-    double *xout = a.xp + (int64_t)k * n;
-    for (int64_t pr = tid; pr < n; pr += nth) xout[pr] = *dm.at(xs + pr);
-  }
-  cl.sync();  // keep every CTA's shared memory alive until all remote reads are done
 }
 
 __global__ void permute_in_kernel(const double *rhs, int64_t ld, const int *pos, int64_t n, int nslab,
@@ -574,18 +381,7 @@ __global__ void permute_out_kernel(const double *xp, const int *pos, int64_t n, 
     x[(int64_t)k * ld + i] = xp[(int64_t)k * n + pos[i]];
 }
 
-__global__ void perm_cols_kernel(const int *col, int64_t nnz, const int *pos, int *colp) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
-    colp[e] = pos[col[e]];
-}
-
-static int env_int2(const char *name, int dflt) {
-  const char *e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
-
-// Coupling matrix re-indexed to the elimination order (rows and columns),
-// cached in the sweep plan: {rowptr_p (n+1), colp (nnz), eidx (nnz)}.
+// Coupling matrix as an ELL table in elimination order, cached in the sweep plan.
 static const std::vector<DevBuf> &permuted_ell(const NDSweepPlan &sp, const NDPlan &p, const int *rowptr,
                                                const int *col, cudaStream_t s, int *width) {
   auto &cache = sp.colp_cache;
@@ -610,7 +406,6 @@ static const std::vector<DevBuf> &permuted_ell(const NDSweepPlan &sp, const NDPl
     }
   int w = 1;
   for (int64_t i = 0; i < n; ++i) w = std::max(w, rp[i + 1] - rp[i]);
-  // ELL in elimination order, entry slot j of row q at [j*n + q]; padding: col -1
   std::vector<int> colp((size_t)w * n, -1), eidx((size_t)w * n, 0);
   for (int64_t q = 0; q < n; ++q) {
     int io = iperm[q], j = 0;
@@ -637,7 +432,6 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   const int warps = 16;
   const NDSweepPlan &sp = dev.get_sweep_plan(cluster, warps, s);
   const int64_t n = p.n;
-  // scratch: rhs_p, x_p (nrhs*n), reff, ybuf (n), cbv (cbv_size)
   static DevBuf scratch;
   const size_t need = ((size_t)2 * nrhs * n + 2 * n + p.cbv_size + 16) * sizeof(double);
   if (scratch.bytes < need) {
@@ -659,13 +453,11 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   a.bwptr = sp.bwd_wptr.as<int>();
   a.g3p = sp.g3p.as<int4>();
   a.bpos = sp.bpos.as<int>();
-  a.iperm = sp.iperm.as<int>();
   a.nlevels = p.nlevels;
   a.nw = cluster * warps;
   a.n = n;
   a.factors = fac.factors.as<double>();
   a.fstride = fac.nbatch == 1 ? 0 : p.factor_size;
-  if (env_int2("STMHD_SWEEP_SAMEFACTOR", 0)) a.fstride = 0;  // diagnostics only
   a.rhsp = rhsp;
   a.xp = xp;
   a.reff = reff;
@@ -686,35 +478,23 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
     a.cpl[c].lag = cpl[c].lag;
     a.cpl[c].coef = cpl[c].coef;
   }
-  a.vstride = std::max(dev.max_front, 1) + 8;
+  // per warp: gather buffer (max front, rounded to 16 doubles) + two TMA slots
+  int64_t maxb = 2;
+  for (int sn = 0; sn < p.nsn; ++sn) maxb = std::max({maxb, p.bsz_f[sn], p.bsz_b[sn]});
+  a.slot = (int)((maxb + 15) / 16 * 16);
+  a.vstride = (int)(((std::max(dev.max_front, 1) + 15) / 16) * 16 + 2 * a.slot);
   static const int prefetch = env_int2("STMHD_SWEEP_PREFETCH", 1);
   a.prefetch = prefetch;
   const int threads = warps * 32;
-  // distributed vectors: x ring (3n) + y (n) + rhs_eff (n) + update vectors
-  a.ncta = cluster;
-  a.lc = 0;
-  while ((1 << a.lc) < cluster) ++a.lc;
-  const int64_t V = 5 * n + p.cbv_size;
-  const int64_t blocks = (V + 32 * cluster - 1) / (32 * cluster);
-  a.dsm_local = blocks * 32;
-  a.seprows = sp.seprows.as<int>();
-  a.nsep = sp.nsep;
-  size_t smem = (size_t)warps * a.vstride * sizeof(double);
-  static const int dsm_env = env_int2("STMHD_SWEEP_DSMEM", 0);
-  const bool use_dsm = dsm_env && (cluster & (cluster - 1)) == 0 &&
-                       smem + a.dsm_local * sizeof(double) + 1024 <= 226 * 1024;
-  if (use_dsm) smem += a.dsm_local * sizeof(double);
-  require(smem <= 227 * 1024, "nd sweep: front too large for shared memory");
-  const void *kern = use_dsm ? (const void *)nd_sweep_dsm_kernel : (const void *)nd_sweep_kernel;
+  const size_t smem = (size_t)warps * a.vstride * sizeof(double);
+  require(smem <= 224 * 1024, "nd sweep: front too large for shared memory");
   static bool attr = false;
   if (!attr) {
-    for (const void *kf : {(const void *)nd_sweep_kernel, (const void *)nd_sweep_dsm_kernel}) {
-      cudaFuncAttributes fa{};
-      STMHD_CUDA_CHECK(cudaFuncGetAttributes(&fa, kf));
-      STMHD_CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      STMHD_CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)(227 * 1024 - fa.sharedSizeBytes)));
-    }
+    cudaFuncAttributes fa{};
+    STMHD_CUDA_CHECK(cudaFuncGetAttributes(&fa, (const void *)nd_sweep_kernel));
+    STMHD_CUDA_CHECK(cudaFuncSetAttribute(nd_sweep_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    STMHD_CUDA_CHECK(cudaFuncSetAttribute(nd_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(227 * 1024 - fa.sharedSizeBytes)));
     attr = true;
   }
   static const int trace_on = env_int2("STMHD_SWEEP_TRACE", 0);
@@ -725,12 +505,6 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
     tr.alloc(nsteps * sizeof(unsigned long long));
     STMHD_CUDA_CHECK(cudaMemsetAsync(tr.ptr, 0, tr.bytes, s));
     a.trace = tr.as<unsigned long long>();
-  }
-  DevBuf wtr;
-  if (trace_on) {
-    wtr.alloc((size_t)nsteps * a.nw * 3 * 8);
-    STMHD_CUDA_CHECK(cudaMemsetAsync(wtr.ptr, 0, wtr.bytes, s));
-    a.wtrace = wtr.as<unsigned long long>();
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cluster);
@@ -745,7 +519,7 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   cfg.attrs = at;
   cfg.numAttrs = 1;
   void *args[] = {&a};
-  STMHD_CUDA_CHECK(cudaLaunchKernelExC(&cfg, kern, args));
+  STMHD_CUDA_CHECK(cudaLaunchKernelExC(&cfg, (const void *)nd_sweep_kernel, args));
   count_launch();
   permute_out_kernel<<<dim3(std::min<int64_t>(cdiv(n, 256), 256), nrhs), 256, 0, s>>>(xp, sp.pos.as<int>(), n, nrhs, x,
                                                                                      ld_x);
@@ -758,27 +532,6 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
     fprintf(stderr, "[sweep] n=%lld levels=%d total=%.1f us | slab1 (us):", (long long)n, p.nlevels,
             (*std::max_element(h.begin(), h.end()) - h[0]) / 1e3);
     for (int i = 0; i < per && base + i < nsteps; ++i) fprintf(stderr, " %.2f", (h[base + i] - h[base + i - 1]) / 1e3);
-    fprintf(stderr, "\n");
-    std::vector<unsigned long long> w((size_t)nsteps * a.nw * 3);
-    STMHD_CUDA_CHECK(cudaMemcpy(w.data(), wtr.ptr, w.size() * 8, cudaMemcpyDeviceToHost));
-    {
-      int last = 0;
-      for (int i = 0; i < nsteps; ++i)
-        if (h[i]) last = i;
-      fprintf(stderr, "[sweep] SM clock during sweep: %.0f MHz\n", 1e3 * (double)(w[last] - w[0]) / (double)(h[last] - h[0]));
-    }
-    fprintf(stderr, "[sweep] fwd levels slab1, slowest warp cycles {task,gather,gemv} (busy):");
-    for (int l = 0; l < p.nlevels; ++l) {
-      int st = base - 1 + l;  // forward level l of slab 1 ran with step index base-1+l
-      unsigned long long best[3] = {0, 0, 0};
-      int busy = 0;
-      for (int q = 0; q < a.nw; ++q) {
-        const unsigned long long *x = &w[((size_t)st * a.nw + q) * 3];
-        if (x[0] + x[1] + x[2]) ++busy;
-        if (x[0] + x[1] + x[2] > best[0] + best[1] + best[2]) { best[0] = x[0]; best[1] = x[1]; best[2] = x[2]; }
-      }
-      fprintf(stderr, " [%llu,%llu,%llu x%d]", best[0], best[1], best[2], busy);
-    }
     fprintf(stderr, "\n");
   }
 }

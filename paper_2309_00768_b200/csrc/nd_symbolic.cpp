@@ -256,15 +256,38 @@ NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const in
   p.idx_off.assign(S + 1, 0);
   p.fl_off.assign(S, 0);
   p.fu_off.assign(S, 0);
+  p.sfl_off.assign(S, 0);
+  p.sfu_off.assign(S, 0);
+  p.rf.assign(S, 1);
+  p.rb.assign(S, 1);
+  p.bsz_f.assign(S, 0);
+  p.bsz_b.assign(S, 0);
+  // rows per chunk: the largest power of two <= 32 whose block fits kChunkMax doubles
+  const int64_t kChunkMax = 640;
+  auto rows_per_chunk = [&](int64_t K) {
+    int R = 32;
+    while (R > 1 && (int64_t)R * K > kChunkMax) R >>= 1;
+    return R;
+  };
   p.front_off.assign(S, 0);
   p.cbv_off.assign(S, 0);
   for (int s = 0; s < S; ++s) {
     int64_t f = p.ns[s] + p.nb[s];
     p.idx_off[s + 1] = p.idx_off[s] + f;
+    const int64_t ns64 = p.ns[s];
+    p.sfl_off[s] = p.stage_size;
+    p.stage_size += f * ns64;
+    p.sfu_off[s] = p.stage_size;
+    p.stage_size += f * ns64;
+    p.rf[s] = rows_per_chunk(ns64);
+    p.rb[s] = rows_per_chunk(f);
+    p.bsz_f[s] = ((int64_t)p.rf[s] * ns64 + 1) & ~int64_t(1);
+    p.bsz_b[s] = ((int64_t)p.rb[s] * f + 1) & ~int64_t(1);
+    const int64_t ncf = (f + p.rf[s] - 1) / p.rf[s], ncb = (ns64 + p.rb[s] - 1) / p.rb[s];
     p.fl_off[s] = p.factor_size;
-    p.factor_size += f * p.ns[s];
+    p.factor_size += ncf * p.bsz_f[s];
     p.fu_off[s] = p.factor_size;
-    p.factor_size += f * p.ns[s];
+    p.factor_size += ncb * p.bsz_b[s];
     p.front_off[s] = p.front_size;
     p.front_size += f * f;
     p.cbv_off[s] = p.cbv_size;
