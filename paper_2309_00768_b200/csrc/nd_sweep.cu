@@ -165,6 +165,7 @@ struct SweepArgs {
   int vstride;  // doubles per warp: gather buffer + 2 TMA slots
   int slot;     // doubles per TMA slot (largest chunk block)
   int prefetch;
+  int null_work;  // diagnostics: skip all task work (barrier/loop floor)
   unsigned long long *trace;
 };
 
@@ -209,6 +210,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
   } while (!done);
 }
 
+// Issue the first (up to) two factor-chunk loads of a task.
+__device__ __forceinline__ void task_begin(const SweepTask &tk, const double *F, double *const *slot,
+                                           unsigned long long (*bar)[2], int wl) {
+  tma_load(slot[0], F + tk.foff + (int64_t)tk.c0 * tk.bsz, tk.bsz, &bar[wl][0]);
+  if (tk.c0 + 1 < tk.c1) tma_load(slot[1], F + tk.foff + (int64_t)(tk.c0 + 1) * tk.bsz, tk.bsz, &bar[wl][1]);
+}
+
 __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long mbar[16][2];
@@ -224,8 +232,26 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
   }
   __syncwarp();
   const int64_t n = a.n;
+  const int L = a.nlevels;
   int step = 0;
   sweep_trace(a, step);
+  // The first task of the next level step is static (descriptor and factor
+  // chunks do not depend on the barrier), so it is fetched and its first TMA
+  // loads are issued before the warp waits at the barrier.
+  SweepTask next{};
+  bool have_next = false;
+  auto preload = [&](int kk, bool fwd, int l) {
+    have_next = false;
+    if (kk >= a.nslab) return;
+    const int *wp = (fwd ? a.fwptr : a.bwptr) + (int64_t)l * a.nw;
+    const int t0 = wp[gw], t1 = wp[gw + 1];
+    if (t0 < t1 && !a.null_work) {
+      next = (fwd ? a.ftask : a.btask)[t0];
+      have_next = true;
+      if (lane == 0) task_begin(next, a.factors + (int64_t)kk * a.fstride, slot, mbar, wl);
+    }
+  };
+  preload(0, true, 0);
   for (int k = 0; k < a.nslab; ++k) {
     if (a.prefetch && a.fstride && k + 1 < a.nslab && lane == 0) {
       const char *base = reinterpret_cast<const char *>(a.factors + (int64_t)(k + 1) * a.fstride);
@@ -239,11 +265,13 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
     }
     const double *rhs = a.rhsp + (int64_t)k * n;
     double *x = a.xp + (int64_t)k * n;
-    if (k > 0 && a.ncpl) {
-      // rhs_eff = rhs_k + sum_c coef_c C_c x_{k-lag}: one permuted row per thread
+    if (k > 0 && a.ncpl && !a.null_work) {
+      // rhs_eff = rhs_k + sum_c coef_c C_c x_{k-lag}: permuted rows, up to two rows
+      // per thread processed together (one pass), ELL slots 8 at a time
       const int64_t nth = (int64_t)a.nw * 32;
-      for (int64_t pr = (int64_t)gw * 32 + lane; pr < n; pr += nth) {
-        double acc = 0.0;
+      for (int64_t p0 = (int64_t)gw * 32 + lane; p0 < n; p0 += 2 * nth) {
+        const int64_t prr[2] = {p0, p0 + nth};
+        double acc[2] = {0.0, 0.0};
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           if (c >= a.ncpl) break;
@@ -252,22 +280,29 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
           if (kp < 0) continue;
           const double *xv = a.xp + (int64_t)kp * n;
           const double *cv = cp.val + (k - cp.val_shift) * cp.val_stride;
-          double part = 0.0;
+          double part[2] = {0.0, 0.0};
           for (int j0 = 0; j0 < cp.width; j0 += 8) {
-            int ci[8], ei[8];
+            int ci[2][8], ei[2][8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const bool ok = j0 + q < cp.width;
-              ci[q] = ok ? cp.colp[(int64_t)(j0 + q) * n + pr] : -1;
-              ei[q] = ok ? cp.eidx[(int64_t)(j0 + q) * n + pr] : 0;
-            }
+            for (int r = 0; r < 2; ++r)
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (ci[q] >= 0) part += cv[ei[q]] * xv[ci[q]];
+              for (int q = 0; q < 8; ++q) {
+                const bool ok = j0 + q < cp.width && prr[r] < n;
+                ci[r][q] = ok ? __ldg(cp.colp + (int64_t)(j0 + q) * n + prr[r]) : -1;
+                ei[r][q] = ok ? __ldg(cp.eidx + (int64_t)(j0 + q) * n + prr[r]) : 0;
+              }
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                if (ci[r][q] >= 0) part[r] += cv[ei[r][q]] * xv[ci[r][q]];
           }
-          acc += cp.coef * part;
+          acc[0] += cp.coef * part[0];
+          acc[1] += cp.coef * part[1];
         }
-        a.reff[pr] = rhs[pr] + acc;
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+          if (prr[r] < n) a.reff[prr[r]] = rhs[prr[r]] + acc[r];
       }
       sweep_barrier();
       sweep_trace(a, step);
@@ -275,21 +310,22 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
     }
     const double *F = a.factors + (int64_t)k * a.fstride;
     // ---- forward (L) levels, bottom-up ----
-    for (int l = 0; l < a.nlevels; ++l) {
+    for (int l = 0; l < L; ++l) {
       const int *wp = a.fwptr + (int64_t)l * a.nw;
-      const int t0 = wp[gw], t1 = wp[gw + 1];
+      const int t0 = wp[gw], t1 = a.null_work ? t0 : wp[gw + 1];
       for (int ti = t0; ti < t1; ++ti) {
-        const SweepTask tk = a.ftask[ti];
-        // start streaming the first two factor chunks, then gather the front
-        if (lane == 0) {
-          tma_load(slot[0], F + tk.foff + (int64_t)tk.c0 * tk.bsz, tk.bsz, &mbar[wl][0]);
-          if (tk.c0 + 1 < tk.c1) tma_load(slot[1], F + tk.foff + (int64_t)(tk.c0 + 1) * tk.bsz, tk.bsz, &mbar[wl][1]);
+        SweepTask tk;
+        if (ti == t0 && have_next) {
+          tk = next;
+        } else {
+          tk = a.ftask[ti];
+          if (lane == 0) task_begin(tk, F, slot, mbar, wl);
         }
         const int4 *g = a.g3p + tk.goff;
         for (int b0 = lane; b0 < tk.f; b0 += 256) {
           int4 gg[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) gg[q] = (b0 + 32 * q < tk.f) ? g[b0 + 32 * q] : make_int4(-1, -1, -1, 0);
+          for (int q = 0; q < 8; ++q) gg[q] = (b0 + 32 * q < tk.f) ? __ldg(g + b0 + 32 * q) : make_int4(-1, -1, -1, 0);
           double vv[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q)
@@ -316,18 +352,22 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
         }
         __syncwarp();
       }
+      if (l + 1 < L) preload(k, true, l + 1);
+      else preload(k, false, L - 1);
       sweep_barrier();
       sweep_trace(a, step);
     }
     // ---- backward (U) levels, top-down ----
-    for (int l = a.nlevels - 1; l >= 0; --l) {
+    for (int l = L - 1; l >= 0; --l) {
       const int *wp = a.bwptr + (int64_t)l * a.nw;
-      const int t0 = wp[gw], t1 = wp[gw + 1];
+      const int t0 = wp[gw], t1 = a.null_work ? t0 : wp[gw + 1];
       for (int ti = t0; ti < t1; ++ti) {
-        const SweepTask tk = a.btask[ti];
-        if (lane == 0) {
-          tma_load(slot[0], F + tk.foff + (int64_t)tk.c0 * tk.bsz, tk.bsz, &mbar[wl][0]);
-          if (tk.c0 + 1 < tk.c1) tma_load(slot[1], F + tk.foff + (int64_t)(tk.c0 + 1) * tk.bsz, tk.bsz, &mbar[wl][1]);
+        SweepTask tk;
+        if (ti == t0 && have_next) {
+          tk = next;
+        } else {
+          tk = a.btask[ti];
+          if (lane == 0) task_begin(tk, F, slot, mbar, wl);
         }
         const int *bp = a.bpos + tk.goff;
         const double *y = a.ybuf + tk.first;
@@ -336,7 +376,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const int t = b0 + 32 * q;
-            ii[q] = (t >= tk.ns && t < tk.f) ? bp[t] : -1;
+            ii[q] = (t >= tk.ns && t < tk.f) ? __ldg(bp + t) : -1;
           }
           double vv[8];
 #pragma unroll
@@ -362,6 +402,8 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
         }
         __syncwarp();
       }
+      if (l > 0) preload(k, false, l - 1);
+      else preload(k + 1, true, 0);
       if (l > 0 || k + 1 < a.nslab) sweep_barrier();
       sweep_trace(a, step);
     }
@@ -483,8 +525,9 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   for (int sn = 0; sn < p.nsn; ++sn) maxb = std::max({maxb, p.bsz_f[sn], p.bsz_b[sn]});
   a.slot = (int)((maxb + 15) / 16 * 16);
   a.vstride = (int)(((std::max(dev.max_front, 1) + 15) / 16) * 16 + 2 * a.slot);
-  static const int prefetch = env_int2("STMHD_SWEEP_PREFETCH", 1);
+  static const int prefetch = env_int2("STMHD_SWEEP_PREFETCH", 0);  // TMA streaming makes it redundant
   a.prefetch = prefetch;
+  a.null_work = env_int2("STMHD_SWEEP_NULL", 0);
   const int threads = warps * 32;
   const size_t smem = (size_t)warps * a.vstride * sizeof(double);
   require(smem <= 224 * 1024, "nd sweep: front too large for shared memory");
