@@ -63,7 +63,7 @@ NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const in
 // Work list of the cluster-resident time sweep (nd_sweep.cu), built lazily for
 // a launch shape: per level and warp, contiguous chunk ranges of one supernode.
 struct alignas(16) SweepTask {
-  int s, c0, c1, R;   // supernode, chunk range, rows per chunk
+  int flags, c0, c1, R;  // flags: 1 = write the update vector to global memory; chunk range; rows per chunk
   int ns, f, rows, bsz;  // bsz: doubles per chunk block
   int64_t foff;   // offset of chunk 0 (forward FL or backward FU blocks)
   int64_t goff;   // offset of the supernode's front tables
@@ -71,9 +71,30 @@ struct alignas(16) SweepTask {
   int64_t cboff;  // update-vector offset
 };
 
+// Slab-coupling "program" of a sweep with subtrees: per CTA, the output items it
+// computes at the start of every slab (its subtree rows into shared memory and a
+// share of the top rows into global memory).
+struct CplProgram {
+  bool ok = false;
+  int64_t nent = 0;      // entries (all CTAs)
+  DevBuf hdr;            // int4 per CTA {item_off, nitems, ent_off, width}
+  DevBuf items;          // int2 per item {dst (kind << 29 | index), rhs row or -1}
+  DevBuf ecol;           // int per entry, [slot][item] per CTA: col | 1<<28 smem | 1<<29 lag 2; -1 pad
+  DevBuf esrc;           // int2 per entry {coupling, value index} ({-1, 0} pad)
+};
+
 struct NDSweepPlan {
   int ncta = 0, warps = 0;
+  // top of the tree (cluster-wide level steps): task ranges per [top level][global warp]
+  int ntop = 0;
   DevBuf fwd_tasks, bwd_tasks, fwd_wptr, bwd_wptr;
+  // bottom subtrees, one per CTA (CTA-local level steps, data in shared memory):
+  // task ranges per [cta][local level][warp]
+  int nsub = 0;                  // local levels (0 = no subtree phase)
+  int64_t sub_len = 0, sub_cb = 0;  // max subtree columns / internal update-vector doubles per CTA
+  DevBuf sf_tasks, sb_tasks, sf_wptr, sb_wptr;
+  DevBuf sub_info;               // per CTA int64 {first col, ncols, first cb, ncb}
+  DevBuf pf_ptr, pf_items;       // per physical warp: its factor-chunk stream for one slab
   DevBuf g3p;   // int4 per front position: {permuted rhs index or -1, cb1, cb2, 0}
   DevBuf bpos;  // int per front position: permuted position of the front entry
   DevBuf pos;   // n: elimination position of each original index
@@ -82,6 +103,10 @@ struct NDSweepPlan {
   // (owned by the same discretisation as this plan, so lifetimes match)
   // {rowptr, colp, eidx} of a coupling matrix in elimination order
   mutable std::map<const int *, std::unique_ptr<std::vector<DevBuf>>> colp_cache;
+  std::vector<int64_t> sub_info_h;  // host copy of sub_info
+  std::vector<int> pos_h, iperm_h;  // host copies of pos / iperm
+  // fused slab-coupling programs (nd_sweep.cu), keyed by the coupling column arrays
+  mutable std::map<std::pair<const int *, const int *>, std::unique_ptr<struct CplProgram>> prog_cache;
 };
 
 // Device-resident copy of a plan plus the solve schedules.
@@ -97,7 +122,7 @@ struct NDDevice {
   int max_front = 0;
   void build(const NDPlan &p, cudaStream_t s);
   mutable std::unique_ptr<NDSweepPlan> sweep_plan;
-  const NDSweepPlan &get_sweep_plan(int ncta, int warps, cudaStream_t s) const;
+  const NDSweepPlan &get_sweep_plan(int ncta, int warps, int64_t sub_budget, cudaStream_t s) const;
 };
 
 // A coupling term of a sequential block sweep:

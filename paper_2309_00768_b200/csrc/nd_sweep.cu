@@ -31,7 +31,7 @@ static int env_int2(const char *name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, cudaStream_t s) const {
+const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_budget, cudaStream_t s) const {
   if (sweep_plan && sweep_plan->ncta == ncta && sweep_plan->warps == warps) return *sweep_plan;
   const NDPlan &p = *plan;
   auto sp = std::make_unique<NDSweepPlan>();
@@ -64,70 +64,223 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, cudaStream_t s)
       }
     }
   }
-  auto build_dir = [&](bool fwd, DevBuf &tasks_d, DevBuf &wptr_d) {
-    std::vector<SweepTask> tasks;
-    std::vector<int> wptr;
-    for (int l = 0; l < p.nlevels; ++l) {
-      struct SN {
-        int s, rows, K, R, m;
-        double cg, cc;
-      };
-      std::vector<SN> sns;
-      for (int sn : p.level_sn[l]) {
-        int f = p.ns[sn] + p.nb[sn];
-        int rows = fwd ? f : p.ns[sn];
-        if (rows == 0) continue;
-        int K = fwd ? p.ns[sn] : f;
-        int R = fwd ? p.rf[sn] : p.rb[sn];
-        int m = (rows + R - 1) / R;
-        // cost model in memory rounds: gather ~2, one chunk ~1 + K/(16 kl)
-        sns.push_back({sn, rows, K, R, m, 2.0, 1.0 + (double)((K + 16 * (32 / R) - 1) / (16 * (32 / R)))});
+
+  // ---- split the tree: subtrees rooted at depth D (one per CTA) + the top ----
+  std::vector<int> depth(p.nsn, 0);
+  for (int sn = p.nsn - 1; sn >= 0; --sn)  // postorder reversed: parents first
+    if (p.parent[sn] >= 0) depth[sn] = depth[p.parent[sn]] + 1;
+  int maxd = 0;
+  for (int sn = 0; sn < p.nsn; ++sn) maxd = std::max(maxd, depth[sn]);
+  int D = 0;
+  for (int d = 1; d <= maxd; ++d) {
+    int cnt = 0;
+    for (int sn = 0; sn < p.nsn; ++sn) cnt += depth[sn] == d;
+    if (cnt <= ncta) D = d;
+  }
+  static const int sub_env = [] {
+    const char *e = getenv("STMHD_SWEEP_SUBTREES");
+    return e ? atoi(e) : 1;
+  }();
+  if (!sub_env) D = 0;
+  // subtree membership: owner CTA of every supernode at depth >= D (D > 0); falls
+  // back to an all-top schedule when the subtree vectors exceed shared memory
+  std::vector<int> owner, roots;
+  std::vector<int64_t> info;
+  int64_t maxlen = 0, maxcb = 0;
+  for (;;) {
+    owner.assign(p.nsn, -1);
+    roots.clear();
+    info.assign(4 * (size_t)ncta, 0);
+    maxlen = maxcb = 0;
+    if (D > 0) {
+      for (int sn = 0; sn < p.nsn; ++sn)
+        if (depth[sn] == D) roots.push_back(sn);
+      for (int r = 0; r < (int)roots.size(); ++r) owner[roots[r]] = r;
+      for (int sn = p.nsn - 1; sn >= 0; --sn)
+        if (depth[sn] > D) owner[sn] = owner[p.parent[sn]];
+    }
+    // per-CTA subtree ranges (a subtree is contiguous in postorder/elimination order)
+    std::vector<int64_t> lo(roots.size(), INT64_MAX), hi(roots.size(), 0), cblo(roots.size(), INT64_MAX),
+        cbhi(roots.size(), 0);
+    for (int sn = 0; sn < p.nsn; ++sn) {
+      int o = owner[sn];
+      if (o < 0) continue;
+      lo[o] = std::min(lo[o], p.first[sn]);
+      hi[o] = std::max(hi[o], p.first[sn] + p.ns[sn]);
+      if (sn != roots[o] && p.nb[sn] > 0) {
+        cblo[o] = std::min(cblo[o], p.cbv_off[sn]);
+        cbhi[o] = std::max(cbhi[o], p.cbv_off[sn] + p.nb[sn]);
       }
-      double total = 0;
-      for (auto &x : sns) total += x.cg + x.m * x.cc;
-      struct Piece {
-        int idx, c0, c1;
-        double cost;
-      };
-      std::vector<Piece> pieces;
-      for (int i = 0; i < (int)sns.size(); ++i) {
-        auto &x = sns[i];
-        double c = x.cg + x.m * x.cc;
-        int np = 1;
-        if ((int)sns.size() < W) np = std::max(1, std::min(x.m, (int)(W * c / total)));
-        for (int q = 0; q < np; ++q) {
-          int c0 = (int)((int64_t)x.m * q / np), c1 = (int)((int64_t)x.m * (q + 1) / np);
-          if (c1 > c0) pieces.push_back({i, c0, c1, x.cg + (c1 - c0) * x.cc});
+    }
+    for (int r = 0; r < (int)roots.size(); ++r) {
+      if (cblo[r] == INT64_MAX) cblo[r] = cbhi[r] = 0;
+      info[4 * r + 0] = lo[r];
+      info[4 * r + 1] = hi[r] - lo[r];
+      info[4 * r + 2] = cblo[r];
+      info[4 * r + 3] = cbhi[r] - cblo[r];
+      maxlen = std::max(maxlen, hi[r] - lo[r]);
+      maxcb = std::max(maxcb, cbhi[r] - cblo[r]);
+    }
+    if (D == 0 || 3 * maxlen + maxcb <= sub_budget) break;  // ys, xs, rhs_s + cbs
+    D = 0;
+  }
+  if (D == 0) maxlen = maxcb = 0;
+
+  struct SN {
+    int s, rows, K, R, m;
+    double cg, cc;
+  };
+  auto make_sn = [&](int sn, bool fwd, SN &x) {
+    int f = p.ns[sn] + p.nb[sn];
+    int rows = fwd ? f : p.ns[sn];
+    if (rows == 0) return false;
+    int K = fwd ? p.ns[sn] : f;
+    int R = fwd ? p.rf[sn] : p.rb[sn];
+    x = {sn, rows, K, R, (rows + R - 1) / R, 2.0, 1.0 + (double)((K + 16 * (32 / R) - 1) / (16 * (32 / R)))};
+    return true;
+  };
+  auto make_task = [&](const SN &x, int c0, int c1, bool fwd, bool cb_global) {
+    SweepTask t{};
+    t.flags = cb_global ? 1 : 0;
+    t.c0 = c0; t.c1 = c1; t.R = x.R;
+    t.ns = p.ns[x.s]; t.f = p.ns[x.s] + p.nb[x.s]; t.rows = x.rows;
+    t.bsz = (int)(fwd ? p.bsz_f[x.s] : p.bsz_b[x.s]);
+    t.foff = fwd ? p.fl_off[x.s] : p.fu_off[x.s];
+    t.goff = p.idx_off[x.s]; t.first = p.first[x.s]; t.cboff = p.cbv_off[x.s];
+    return t;
+  };
+  // LPT of a set of supernodes onto `nw` warps; pieces split big supernodes
+  auto schedule = [&](const std::vector<SN> &sns, int nw, bool fwd, std::vector<std::vector<SweepTask>> &per,
+                      const std::vector<char> &cbg) {
+    per.assign(nw, {});
+    double total = 0;
+    for (auto &x : sns) total += x.cg + x.m * x.cc;
+    struct Piece {
+      int idx, c0, c1;
+      double cost;
+    };
+    std::vector<Piece> pieces;
+    for (int i = 0; i < (int)sns.size(); ++i) {
+      auto &x = sns[i];
+      double c = x.cg + x.m * x.cc;
+      int np = 1;
+      if ((int)sns.size() < nw) np = std::max(1, std::min(x.m, (int)(nw * c / total)));
+      for (int q = 0; q < np; ++q) {
+        int c0 = (int)((int64_t)x.m * q / np), c1 = (int)((int64_t)x.m * (q + 1) / np);
+        if (c1 > c0) pieces.push_back({i, c0, c1, x.cg + (c1 - c0) * x.cc});
+      }
+    }
+    std::sort(pieces.begin(), pieces.end(), [](const Piece &a, const Piece &b) { return a.cost > b.cost; });
+    std::vector<double> load(nw, 0.0);
+    for (auto &pc : pieces) {
+      int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+      per[w].push_back(make_task(sns[pc.idx], pc.c0, pc.c1, fwd, cbg[pc.idx]));
+      load[w] += pc.cost;
+    }
+  };
+  // top part: levels (heights) that contain top supernodes, ascending
+  std::vector<int> top_levels;
+  for (int l = 0; l < p.nlevels; ++l) {
+    bool any = false;
+    for (int sn : p.level_sn[l]) any |= owner[sn] < 0;
+    if (any) top_levels.push_back(l);
+  }
+  sp->ntop = (int)top_levels.size();
+  int nsub = 0;
+  for (int r = 0; r < (int)roots.size(); ++r) nsub = std::max(nsub, p.level[roots[r]] + 1);
+  sp->nsub = roots.empty() ? 0 : nsub;
+  sp->sub_len = maxlen;
+  sp->sub_cb = maxcb;
+  std::vector<SweepTask> h_tasks[2], h_stasks[2];
+  std::vector<int> h_wptr[2], h_swptr[2];
+  auto build_dir = [&](bool fwd, DevBuf &tasks_d, DevBuf &wptr_d, DevBuf &stasks_d, DevBuf &swptr_d) {
+    std::vector<SweepTask> &tasks = h_tasks[fwd], &stasks = h_stasks[fwd];
+    std::vector<int> &wptr = h_wptr[fwd], &swptr = h_swptr[fwd];
+    for (int l : top_levels) {
+      std::vector<SN> sns;
+      std::vector<char> cbg;
+      for (int sn : p.level_sn[l]) {
+        SN x;
+        if (owner[sn] < 0 && make_sn(sn, fwd, x)) {
+          sns.push_back(x);
+          cbg.push_back(1);
         }
       }
-      std::sort(pieces.begin(), pieces.end(), [](const Piece &a, const Piece &b) { return a.cost > b.cost; });
-      std::vector<std::vector<Piece>> per(W);
-      std::vector<double> load(W, 0.0);
-      for (auto &pc : pieces) {
-        int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-        per[w].push_back(pc);
-        load[w] += pc.cost;
-      }
+      std::vector<std::vector<SweepTask>> per;
+      schedule(sns, W, fwd, per, cbg);
       for (int w = 0; w < W; ++w) {
         wptr.push_back((int)tasks.size());
-        for (auto &pc : per[w]) {
-          auto &x = sns[pc.idx];
-          SweepTask t{};
-          t.s = x.s; t.c0 = pc.c0; t.c1 = pc.c1; t.R = x.R;
-          t.ns = p.ns[x.s]; t.f = p.ns[x.s] + p.nb[x.s]; t.rows = x.rows;
-          t.bsz = (int)(fwd ? p.bsz_f[x.s] : p.bsz_b[x.s]);
-          t.foff = fwd ? p.fl_off[x.s] : p.fu_off[x.s];
-          t.goff = p.idx_off[x.s]; t.first = p.first[x.s]; t.cboff = p.cbv_off[x.s];
-          tasks.push_back(t);
-        }
+        tasks.insert(tasks.end(), per[w].begin(), per[w].end());
       }
     }
     wptr.push_back((int)tasks.size());
+    for (int c = 0; c < ncta; ++c)
+      for (int h = 0; h < sp->nsub; ++h) {
+        std::vector<SN> sns;
+        std::vector<char> cbg;
+        if (c < (int)roots.size())
+          for (int sn : p.level_sn[h]) {
+            SN x;
+            if (owner[sn] == c && make_sn(sn, fwd, x)) {
+              sns.push_back(x);
+              cbg.push_back(sn == roots[c]);
+            }
+          }
+        std::vector<std::vector<SweepTask>> per;
+        schedule(sns, warps, fwd, per, cbg);
+        for (int w = 0; w < warps; ++w) {
+          swptr.push_back((int)stasks.size());
+          stasks.insert(stasks.end(), per[w].begin(), per[w].end());
+        }
+      }
+    swptr.push_back((int)stasks.size());
+    if (stasks.empty()) stasks.push_back(SweepTask{});
     tasks_d = upload_vec(tasks, s);
     wptr_d = upload_vec(wptr, s);
+    stasks_d = upload_vec(stasks, s);
+    swptr_d = upload_vec(swptr, s);
   };
-  build_dir(true, sp->fwd_tasks, sp->fwd_wptr);
-  build_dir(false, sp->bwd_tasks, sp->bwd_wptr);
+  build_dir(true, sp->fwd_tasks, sp->fwd_wptr, sp->sf_tasks, sp->sf_wptr);
+  build_dir(false, sp->bwd_tasks, sp->bwd_wptr, sp->sb_tasks, sp->sb_wptr);
+  // per physical warp (cta c, warp w): the factor chunks it consumes in one slab, in
+  // kernel order (subtree fwd, top fwd, top bwd, subtree bwd) -- the L2 prefetch stream
+  {
+    std::vector<int> pptr;
+    std::vector<longlong2> items;
+    auto add = [&](const std::vector<SweepTask> &ts, int b, int e) {
+      for (int i = b; i < e; ++i)
+        for (int c = ts[i].c0; c < ts[i].c1; ++c)
+          items.push_back(make_longlong2(ts[i].foff + (int64_t)c * ts[i].bsz, ts[i].bsz));
+    };
+    for (int c = 0; c < ncta; ++c)
+      for (int w = 0; w < warps; ++w) {
+        pptr.push_back((int)items.size());
+        for (int h = 0; h < sp->nsub; ++h) {
+          const int q = (c * sp->nsub + h) * warps + w;
+          add(h_stasks[1], h_swptr[1][q], h_swptr[1][q + 1]);
+        }
+        for (int t = 0; t < sp->ntop; ++t) {
+          const int q = t * W + w * ncta + c;
+          add(h_tasks[1], h_wptr[1][q], h_wptr[1][q + 1]);
+        }
+        for (int t = sp->ntop - 1; t >= 0; --t) {
+          const int q = t * W + w * ncta + c;
+          add(h_tasks[0], h_wptr[0][q], h_wptr[0][q + 1]);
+        }
+        for (int h = sp->nsub - 1; h >= 0; --h) {
+          const int q = (c * sp->nsub + h) * warps + w;
+          add(h_stasks[0], h_swptr[0][q], h_swptr[0][q + 1]);
+        }
+      }
+    pptr.push_back((int)items.size());
+    if (items.empty()) items.push_back(make_longlong2(0, 0));
+    sp->pf_ptr = upload_vec(pptr, s);
+    sp->pf_items = upload_vec(items, s);
+  }
+  sp->sub_info = upload_vec(info, s);
+  sp->sub_info_h = info;
+  sp->pos_h = pos;
+  sp->iperm_h = iperm;
   sp->g3p = upload_vec(g3, s);
   sp->bpos = upload_vec(bpos, s);
   sp->pos = upload_vec(pos, s);
@@ -149,7 +302,22 @@ struct SweepCpl {
 
 struct SweepArgs {
   const SweepTask *ftask, *btask;
-  const int *fwptr, *bwptr;  // per level W entries (+ one final sentinel)
+  const int *fwptr, *bwptr;  // per top level W entries (+ one final sentinel)
+  const SweepTask *sftask, *sbtask;
+  const int *sfwptr, *sbwptr;  // per [cta][local level] `warps` entries (+ sentinel)
+  const int64_t *sub_info;     // per CTA {first col, ncols, first cb, ncb}
+  int ntop, nsub, warps;
+  int64_t sub_len, sub_cb;     // shared-memory sizes of the subtree vectors
+  // fused slab coupling (CplProgram): per-CTA items computed at the start of a slab
+  const int4 *prog_hdr;
+  const int2 *prog_items;
+  const int *prog_ecol;
+  const double *prog_vals;     // [slab or 0][entry]: coef * coupling value
+  int64_t prog_nent;
+  int prog_per_slab;
+  double *tbuf;                // coupled right-hand side of the top rows
+  const int *pf_ptr;           // per physical warp: range of its chunk stream
+  const longlong2 *pf_items;   // {offset in a slab's factors, doubles}
   const int4 *g3p;
   const int *bpos;
   int nlevels, nw;
@@ -167,6 +335,7 @@ struct SweepArgs {
   int prefetch;
   int null_work;  // diagnostics: skip all task work (barrier/loop floor)
   unsigned long long *trace;
+  unsigned long long *prof;  // PROF instantiation: 6 counters per warp
 };
 
 __device__ __forceinline__ void sweep_barrier() {
@@ -211,20 +380,249 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
 }
 
 // Issue the first (up to) two factor-chunk loads of a task.
-__device__ __forceinline__ void task_begin(const SweepTask &tk, const double *F, double *const *slot,
+__device__ __forceinline__ void task_begin(const SweepTask &tk, const double *F, double *slot0, int slotsz,
                                            unsigned long long (*bar)[2], int wl) {
-  tma_load(slot[0], F + tk.foff + (int64_t)tk.c0 * tk.bsz, tk.bsz, &bar[wl][0]);
-  if (tk.c0 + 1 < tk.c1) tma_load(slot[1], F + tk.foff + (int64_t)(tk.c0 + 1) * tk.bsz, tk.bsz, &bar[wl][1]);
+  tma_load(slot0, F + tk.foff + (int64_t)tk.c0 * tk.bsz, tk.bsz, &bar[wl][0]);
+  if (tk.c0 + 1 < tk.c1) tma_load(slot0 + slotsz, F + tk.foff + (int64_t)(tk.c0 + 1) * tk.bsz, tk.bsz, &bar[wl][1]);
 }
 
+// Per-CTA view of the subtree vectors kept in shared memory.
+struct SubView {
+  double *ys, *xs, *cbs, *rhs_s;  // rhs_s: coupled right-hand side of the subtree rows (fused mode)
+  int64_t first, len, cbfirst;
+};
+
+struct WarpCtx {
+  int lane, wl;
+  double *v;
+  double *slot0;   // two TMA slots: slot0, slot0 + slotsz
+  int slotsz;
+  unsigned phase;  // bit sl = parity of slot sl
+  // L2 prefetch cursor along this warp's chunk stream (lane 0 only)
+  const longlong2 *pf;
+  int pfn, pidx, pslab;
+  // PROF instantiation: cycles in gather / TMA wait / GEMV+store / barriers, tasks, chunks
+  long long acc[8];
+};
+
+template <bool PROF>
+__device__ __forceinline__ long long pclock() {
+  if constexpr (PROF) return clock64();
+  else return 0;
+}
+
+__device__ __forceinline__ void l2_prefetch(const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// Advance the prefetch cursor by one chunk (it runs a.prefetch chunks ahead of the
+// consumer, across level, phase and slab boundaries).
+__device__ __forceinline__ void pf_advance(const SweepArgs &a, WarpCtx &w) {
+  if (w.pslab < (a.fstride ? a.nslab : 1) && w.pfn > 0) {
+    const longlong2 it = w.pf[w.pidx];
+    l2_prefetch(a.factors + (int64_t)w.pslab * a.fstride + it.x, (unsigned)it.y * 8u);
+    if (++w.pidx == w.pfn) {
+      w.pidx = 0;
+      ++w.pslab;
+    }
+  }
+}
+
+// GEMV of one shared-memory chunk block [K][R] (R a power of two, lane = kq*R + rl):
+// element (kq + q*kl, rl) sits at blk[lane + 32 q], so the block is walked with
+// immediate offsets and one predicate per step.  Returns row rl's dot product
+// (reduced over the kl lanes sharing rl).
+__device__ __forceinline__ double chunk_gemv_smem(const double *blk, int KR, int kl, int kq, int R,
+                                                  const double *v, int lane) {
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const double *b = blk + lane;
+  const double *vv = v + kq;
+  for (int base = 0; base < KR; base += 640) {
+    const int rem = KR - base - lane;
+#pragma unroll
+    for (int q = 0; q < 20; ++q)
+      if (32 * q < rem) acc[q & 3] = fma(b[32 * q], vv[q * kl], acc[q & 3]);
+    b += 640;
+    vv += 20 * kl;
+  }
+  double out = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  for (int o = R; o < 32; o <<= 1) out += __shfl_xor_sync(0xffffffffu, out, o);
+  return out;
+}
+
+// Forward (L) step of one task: gather the front, stream its factor chunks, GEMV.
+template <bool SUB, bool PROF>
+__device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask &tk, const double *F,
+                                             const double *rhs, const SubView &sv, WarpCtx &w,
+                                             unsigned long long (*mbar)[2]) {
+  const int lane = w.lane;
+  long long t0 = pclock<PROF>();
+  if (lane == 0) task_begin(tk, F, w.slot0, w.slotsz, mbar, w.wl);
+  const int4 *g = a.g3p + tk.goff;
+  const double *cbsrc = SUB ? sv.cbs - sv.cbfirst : a.cbv;
+  // fused coupling: subtree rows come from shared memory, top rows from tbuf
+  const bool fused = a.prog_hdr != nullptr;
+  const double *rsrc = (SUB && fused) ? sv.rhs_s - sv.first : (fused ? a.tbuf : rhs);
+  for (int b0 = lane; b0 < tk.f; b0 += 256) {
+    int4 gg[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) gg[q] = (b0 + 32 * q < tk.f) ? __ldg(g + b0 + 32 * q) : make_int4(-1, -1, -1, 0);
+    double vv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      vv[q] = ((gg[q].x >= 0 ? rsrc[gg[q].x] : 0.0) + (gg[q].y >= 0 ? cbsrc[gg[q].y] : 0.0)) +
+              (gg[q].z >= 0 ? cbsrc[gg[q].z] : 0.0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (b0 + 32 * q < tk.f) w.v[b0 + 32 * q] = vv[q];
+  }
+  __syncwarp();
+  if (PROF) {
+    const long long t1 = pclock<PROF>();
+    w.acc[0] += t1 - t0;
+    w.acc[4] += 1;
+    w.acc[5] += tk.c1 - tk.c0;
+    t0 = t1;
+  }
+  const int R = tk.R, lgR = __ffs(R) - 1, kl = 32 >> lgR, kq = lane >> lgR;
+  double *ydst = SUB ? sv.ys - sv.first : a.ybuf;
+  double *cbdst = (!SUB || (tk.flags & 1)) ? a.cbv : sv.cbs - sv.cbfirst;
+  for (int c = tk.c0; c < tk.c1; ++c) {
+    const int sl = (c - tk.c0) & 1;
+    if (lane == 0 && a.prefetch) pf_advance(a, w);
+    mbar_wait(&mbar[w.wl][sl], (w.phase >> sl) & 1u);
+    w.phase ^= 1u << sl;
+    const double *blk = w.slot0 + sl * w.slotsz;
+    if (PROF) {
+      const long long t1 = pclock<PROF>();
+      w.acc[1] += t1 - t0;
+      t0 = t1;
+    }
+    const double out = chunk_gemv_smem(blk, tk.ns * R, kl, kq, R, w.v, lane);
+    if (PROF) {
+      const long long t1 = pclock<PROF>();
+      w.acc[6] += t1 - t0;
+      t0 = t1;
+    }
+    const int r = c * R + (lane & (R - 1));
+    if (lane < R && r < tk.rows) {
+      if (r < tk.ns) ydst[tk.first + r] = out;
+      else cbdst[tk.cboff + r - tk.ns] = w.v[r] - out;
+    }
+    __syncwarp();
+    if (lane == 0 && c + 2 < tk.c1) tma_load(w.slot0 + sl * w.slotsz, F + tk.foff + (int64_t)(c + 2) * tk.bsz, tk.bsz, &mbar[w.wl][sl]);
+    if (PROF) {
+      const long long t1 = pclock<PROF>();
+      w.acc[2] += t1 - t0;
+      t0 = t1;
+    }
+  }
+  __syncwarp();
+}
+
+// Backward (U) step of one task.
+template <bool SUB, bool PROF>
+__device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTask &tk, const double *F, double *x,
+                                              const SubView &sv, WarpCtx &w, unsigned long long (*mbar)[2]) {
+  const int lane = w.lane;
+  long long t0 = pclock<PROF>();
+  if (lane == 0) task_begin(tk, F, w.slot0, w.slotsz, mbar, w.wl);
+  const int *bp = a.bpos + tk.goff;
+  const double *y = (SUB ? sv.ys - sv.first : a.ybuf) + tk.first;
+  for (int b0 = lane; b0 < tk.f; b0 += 256) {
+    int ii[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int t = b0 + 32 * q;
+      ii[q] = (t >= tk.ns && t < tk.f) ? __ldg(bp + t) : -1;
+    }
+    double vv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int t = b0 + 32 * q;
+      // one (generic) load per entry: own subtree from shared memory, else global
+      const int64_t off = ii[q] - sv.first;
+      const double *src = (SUB && (uint64_t)off < (uint64_t)sv.len) ? sv.xs + off : x + ii[q];
+      if (ii[q] < 0) src = y + (t < tk.ns ? t : 0);  // t >= f: any valid address (unused)
+      vv[q] = *src;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (b0 + 32 * q < tk.f) w.v[b0 + 32 * q] = vv[q];
+  }
+  __syncwarp();
+  if (PROF) {
+    const long long t1 = pclock<PROF>();
+    w.acc[0] += t1 - t0;
+    w.acc[4] += 1;
+    w.acc[5] += tk.c1 - tk.c0;
+    t0 = t1;
+  }
+  const int R = tk.R, lgR = __ffs(R) - 1, kl = 32 >> lgR, kq = lane >> lgR;
+  for (int c = tk.c0; c < tk.c1; ++c) {
+    const int sl = (c - tk.c0) & 1;
+    if (lane == 0 && a.prefetch) pf_advance(a, w);
+    mbar_wait(&mbar[w.wl][sl], (w.phase >> sl) & 1u);
+    w.phase ^= 1u << sl;
+    const double *blk = w.slot0 + sl * w.slotsz;
+    if (PROF) {
+      const long long t1 = pclock<PROF>();
+      w.acc[1] += t1 - t0;
+      t0 = t1;
+    }
+    const double out = chunk_gemv_smem(blk, tk.f * R, kl, kq, R, w.v, lane);
+    if (PROF) {
+      const long long t1 = pclock<PROF>();
+      w.acc[7] += t1 - t0;
+      t0 = t1;
+    }
+    const int r = c * R + (lane & (R - 1));
+    if (lane < R && r < tk.rows) {
+      x[tk.first + r] = out;
+      if (SUB) sv.xs[tk.first + r - sv.first] = out;
+    }
+    __syncwarp();
+    if (lane == 0 && c + 2 < tk.c1) tma_load(w.slot0 + sl * w.slotsz, F + tk.foff + (int64_t)(c + 2) * tk.bsz, tk.bsz, &mbar[w.wl][sl]);
+    if (PROF) {
+      const long long t1 = pclock<PROF>();
+      w.acc[2] += t1 - t0;
+      t0 = t1;
+    }
+  }
+  __syncwarp();
+}
+
+template <bool PROF>
 __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long mbar[16][2];
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int gw = wl * gridDim.x + blockIdx.x;  // interleaved across CTAs
-  double *v = sm + wl * a.vstride;
-  double *slot[2] = {v + (a.vstride - 2 * a.slot), v + (a.vstride - a.slot)};
-  unsigned phase[2] = {0u, 0u};
+  WarpCtx w;
+  w.lane = threadIdx.x & 31;
+  w.wl = threadIdx.x >> 5;
+  const int lane = w.lane, wl = w.wl;
+  const int gw = wl * gridDim.x + blockIdx.x;  // interleaved across CTAs (top phases)
+  w.v = sm + wl * a.vstride;
+  w.slot0 = w.v + (a.vstride - 2 * a.slot);
+  w.slotsz = a.slot;
+  w.phase = 0u;
+  for (int i = 0; i < 8; ++i) w.acc[i] = 0;
+  long long tb = 0;
+  {
+    const int gid = blockIdx.x * a.warps + wl;
+    w.pf = a.pf_items + a.pf_ptr[gid];
+    w.pfn = a.pf_ptr[gid + 1] - a.pf_ptr[gid];
+    w.pidx = w.pslab = 0;
+    if (lane == 0 && !a.null_work)
+      for (int i = 0; i < a.prefetch; ++i) pf_advance(a, w);
+  }
+  SubView sv;
+  sv.ys = sm + (int64_t)a.warps * a.vstride;
+  sv.xs = sv.ys + a.sub_len;
+  sv.cbs = sv.xs + a.sub_len;
+  sv.rhs_s = sv.cbs + a.sub_cb;
+  sv.first = a.sub_info[4 * blockIdx.x + 0];
+  sv.len = a.sub_info[4 * blockIdx.x + 1];
+  sv.cbfirst = a.sub_info[4 * blockIdx.x + 2];
   if (lane == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[wl][0])) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[wl][1])) : "memory");
@@ -232,40 +630,69 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
   }
   __syncwarp();
   const int64_t n = a.n;
-  const int L = a.nlevels;
   int step = 0;
   sweep_trace(a, step);
-  // The first task of the next level step is static (descriptor and factor
-  // chunks do not depend on the barrier), so it is fetched and its first TMA
-  // loads are issued before the warp waits at the barrier.
-  SweepTask next{};
-  bool have_next = false;
-  auto preload = [&](int kk, bool fwd, int l) {
-    have_next = false;
-    if (kk >= a.nslab) return;
-    const int *wp = (fwd ? a.fwptr : a.bwptr) + (int64_t)l * a.nw;
-    const int t0 = wp[gw], t1 = wp[gw + 1];
-    if (t0 < t1 && !a.null_work) {
-      next = (fwd ? a.ftask : a.btask)[t0];
-      have_next = true;
-      if (lane == 0) task_begin(next, a.factors + (int64_t)kk * a.fstride, slot, mbar, wl);
-    }
-  };
-  preload(0, true, 0);
   for (int k = 0; k < a.nslab; ++k) {
-    if (a.prefetch && a.fstride && k + 1 < a.nslab && lane == 0) {
-      const char *base = reinterpret_cast<const char *>(a.factors + (int64_t)(k + 1) * a.fstride);
-      const int64_t bytes = a.fstride * 8, chunk = 32 * 1024;
-      for (int64_t off = (int64_t)gw * chunk; off < bytes; off += (int64_t)a.nw * chunk) {
-        int64_t len = min(chunk, bytes - off) & ~int64_t(15);
-        if (len > 0)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base + off), "r"((unsigned)len)
-                       : "memory");
-      }
-    }
     const double *rhs = a.rhsp + (int64_t)k * n;
     double *x = a.xp + (int64_t)k * n;
-    if (k > 0 && a.ncpl && !a.null_work) {
+    if (a.prog_hdr && !a.null_work) {
+      // fused coupling (CTA-local): rhs_k + sum_c coef_c C_c x_{k-lag_c} for this CTA's
+      // items, two items per thread with all their loads in flight together; x_{k-1}
+      // of the CTA's own subtree is read from shared memory (xs)
+      const int4 hd = a.prog_hdr[blockIdx.x];
+      const double *vk = a.prog_vals + (a.prog_per_slab ? (int64_t)k * a.prog_nent : 0);
+      // x_{k-1} (lag-2 entries are offset by -n; at k = 1 they point into the
+      // permuted rhs, which precedes xp in scratch, and carry value 0)
+      const double *x1 = a.xp + (int64_t)(k - 1) * n;
+      const int nth = blockDim.x;
+      for (int i0 = threadIdx.x; i0 < hd.y; i0 += 2 * nth) {
+        const int it[2] = {i0, i0 + nth};
+        const bool live[2] = {true, i0 + nth < hd.y};
+        double acc[2];
+        int2 io[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          io[r] = live[r] ? a.prog_items[hd.x + it[r]] : make_int2(0, -1);
+          acc[r] = io[r].y >= 0 ? rhs[io[r].y] : 0.0;
+        }
+        if (k >= 1) {
+          for (int s0 = 0; s0 < hd.w; s0 += 8) {
+            int cc[2][8];
+            double vv[2][8];
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const int64_t id = hd.z + (int64_t)(s0 + q) * hd.y + it[r];
+                const bool ok = live[r] && s0 + q < hd.w;
+                cc[r][q] = ok ? __ldg(a.prog_ecol + id) : 0;
+                vv[r][q] = ok ? __ldg(vk + id) : 0.0;
+              }
+            double xv[2][8];  // all 16 loads in flight together
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const bool sm = cc[r][q] >= (1 << 30);
+                xv[r][q] = *((sm ? (const double *)sv.xs : x1) + (sm ? cc[r][q] - (1 << 30) : cc[r][q]));
+              }
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+              for (int q = 0; q < 8; ++q) acc[r] = fma(vv[r][q], xv[r][q], acc[r]);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          if (!live[r]) continue;
+          const int kind = io[r].x >> 29, di = io[r].x & ((1 << 29) - 1);
+          if (kind == 0) sv.rhs_s[di] = acc[r];
+          else a.tbuf[di] = acc[r];
+        }
+      }
+      tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+      sweep_trace(a, step);
+    } else if (k > 0 && a.ncpl && !a.null_work) {
       // rhs_eff = rhs_k + sum_c coef_c C_c x_{k-lag}: permuted rows, up to two rows
       // per thread processed together (one pass), ELL slots 8 at a time
       const int64_t nth = (int64_t)a.nw * 32;
@@ -291,11 +718,20 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
                 ci[r][q] = ok ? __ldg(cp.colp + (int64_t)(j0 + q) * n + prr[r]) : -1;
                 ei[r][q] = ok ? __ldg(cp.eidx + (int64_t)(j0 + q) * n + prr[r]) : 0;
               }
+            double cvv[2][8], xvv[2][8];  // unconditional (clamped) loads: all in flight
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const bool ok = ci[r][q] >= 0;
+                cvv[r][q] = cv[ok ? ei[r][q] : 0];
+                xvv[r][q] = xv[ok ? ci[r][q] : 0];
+              }
 #pragma unroll
             for (int r = 0; r < 2; ++r)
 #pragma unroll
               for (int q = 0; q < 8; ++q)
-                if (ci[r][q] >= 0) part[r] += cv[ei[r][q]] * xv[ci[r][q]];
+                if (ci[r][q] >= 0) part[r] += cvv[r][q] * xvv[r][q];
           }
           acc[0] += cp.coef * part[0];
           acc[1] += cp.coef * part[1];
@@ -304,110 +740,66 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
         for (int r = 0; r < 2; ++r)
           if (prr[r] < n) a.reff[prr[r]] = rhs[prr[r]] + acc[r];
       }
-      sweep_barrier();
+      tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step);
       rhs = a.reff;
     }
     const double *F = a.factors + (int64_t)k * a.fstride;
-    // ---- forward (L) levels, bottom-up ----
-    for (int l = 0; l < L; ++l) {
-      const int *wp = a.fwptr + (int64_t)l * a.nw;
-      const int t0 = wp[gw], t1 = a.null_work ? t0 : wp[gw + 1];
-      for (int ti = t0; ti < t1; ++ti) {
-        SweepTask tk;
-        if (ti == t0 && have_next) {
-          tk = next;
-        } else {
-          tk = a.ftask[ti];
-          if (lane == 0) task_begin(tk, F, slot, mbar, wl);
-        }
-        const int4 *g = a.g3p + tk.goff;
-        for (int b0 = lane; b0 < tk.f; b0 += 256) {
-          int4 gg[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) gg[q] = (b0 + 32 * q < tk.f) ? __ldg(g + b0 + 32 * q) : make_int4(-1, -1, -1, 0);
-          double vv[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            vv[q] = ((gg[q].x >= 0 ? rhs[gg[q].x] : 0.0) + (gg[q].y >= 0 ? a.cbv[gg[q].y] : 0.0)) +
-                    (gg[q].z >= 0 ? a.cbv[gg[q].z] : 0.0);
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (b0 + 32 * q < tk.f) v[b0 + 32 * q] = vv[q];
-        }
-        __syncwarp();
-        const int R = tk.R;
-        for (int c = tk.c0; c < tk.c1; ++c) {
-          const int sl = (c - tk.c0) & 1;
-          mbar_wait(&mbar[wl][sl], phase[sl]);
-          phase[sl] ^= 1u;
-          const double out = chunk_gemv<false>(slot[sl], R, tk.ns, v, lane);
-          const int r = c * R + (lane & (R - 1));
-          if (lane < R && r < tk.rows) {
-            if (r < tk.ns) a.ybuf[tk.first + r] = out;
-            else a.cbv[tk.cboff + r - tk.ns] = v[r] - out;
-          }
-          __syncwarp();
-          if (lane == 0 && c + 2 < tk.c1) tma_load(slot[sl], F + tk.foff + (int64_t)(c + 2) * tk.bsz, tk.bsz, &mbar[wl][sl]);
-        }
-        __syncwarp();
+    // ---- forward: bottom subtrees (CTA-local), then the top (cluster-wide) ----
+    for (int h = 0; h < a.nsub; ++h) {
+      const int *wp = a.sfwptr + ((int64_t)blockIdx.x * a.nsub + h) * a.warps + wl;
+      const int t1 = a.null_work ? wp[0] : wp[1];
+      for (int ti = wp[0]; ti < t1; ++ti) {
+        const SweepTask tk = a.sftask[ti];
+        forward_task<true, PROF>(a, tk, F, rhs, sv, w, mbar);
       }
-      if (l + 1 < L) preload(k, true, l + 1);
-      else preload(k, false, L - 1);
-      sweep_barrier();
+      tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+    }
+    if (a.nsub) {
+      tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step);
     }
-    // ---- backward (U) levels, top-down ----
-    for (int l = L - 1; l >= 0; --l) {
-      const int *wp = a.bwptr + (int64_t)l * a.nw;
-      const int t0 = wp[gw], t1 = a.null_work ? t0 : wp[gw + 1];
-      for (int ti = t0; ti < t1; ++ti) {
-        SweepTask tk;
-        if (ti == t0 && have_next) {
-          tk = next;
-        } else {
-          tk = a.btask[ti];
-          if (lane == 0) task_begin(tk, F, slot, mbar, wl);
-        }
-        const int *bp = a.bpos + tk.goff;
-        const double *y = a.ybuf + tk.first;
-        for (int b0 = lane; b0 < tk.f; b0 += 256) {
-          int ii[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int t = b0 + 32 * q;
-            ii[q] = (t >= tk.ns && t < tk.f) ? __ldg(bp + t) : -1;
-          }
-          double vv[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int t = b0 + 32 * q;
-            vv[q] = t < tk.ns ? y[t] : (ii[q] >= 0 ? x[ii[q]] : 0.0);
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (b0 + 32 * q < tk.f) v[b0 + 32 * q] = vv[q];
-        }
-        __syncwarp();
-        const int R = tk.R;
-        for (int c = tk.c0; c < tk.c1; ++c) {
-          const int sl = (c - tk.c0) & 1;
-          mbar_wait(&mbar[wl][sl], phase[sl]);
-          phase[sl] ^= 1u;
-          const double out = chunk_gemv<false>(slot[sl], R, tk.f, v, lane);
-          const int r = c * R + (lane & (R - 1));
-          if (lane < R && r < tk.rows) x[tk.first + r] = out;
-          __syncwarp();
-          if (lane == 0 && c + 2 < tk.c1) tma_load(slot[sl], F + tk.foff + (int64_t)(c + 2) * tk.bsz, tk.bsz, &mbar[wl][sl]);
-        }
-        __syncwarp();
+    for (int t = 0; t < a.ntop; ++t) {
+      const int *wp = a.fwptr + (int64_t)t * a.nw + gw;
+      const int t1 = a.null_work ? wp[0] : wp[1];
+      for (int ti = wp[0]; ti < t1; ++ti) {
+        const SweepTask tk = a.ftask[ti];
+        forward_task<false, PROF>(a, tk, F, rhs, sv, w, mbar);
       }
-      if (l > 0) preload(k, false, l - 1);
-      else preload(k + 1, true, 0);
-      if (l > 0 || k + 1 < a.nslab) sweep_barrier();
+      tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+      sweep_trace(a, step);
+    }
+    // ---- backward: the top, then the bottom subtrees ----
+    for (int t = a.ntop - 1; t >= 0; --t) {
+      const int *wp = a.bwptr + (int64_t)t * a.nw + gw;
+      const int t1 = a.null_work ? wp[0] : wp[1];
+      for (int ti = wp[0]; ti < t1; ++ti) {
+        const SweepTask tk = a.btask[ti];
+        backward_task<false, PROF>(a, tk, F, x, sv, w, mbar);
+      }
+      if (t > 0 || a.nsub || k + 1 < a.nslab) {
+        tb = pclock<PROF>();
+        sweep_barrier();
+        if (PROF) w.acc[3] += pclock<PROF>() - tb;
+      }
+      sweep_trace(a, step);
+    }
+    for (int h = a.nsub - 1; h >= 0; --h) {
+      const int *wp = a.sbwptr + ((int64_t)blockIdx.x * a.nsub + h) * a.warps + wl;
+      const int t1 = a.null_work ? wp[0] : wp[1];
+      for (int ti = wp[0]; ti < t1; ++ti) {
+        const SweepTask tk = a.sbtask[ti];
+        backward_task<true, PROF>(a, tk, F, x, sv, w, mbar);
+      }
+      tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+    }
+    if (a.nsub && k + 1 < a.nslab) {  // x_k visible to every CTA's next coupling
+      tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step);
     }
   }
+  if (PROF && lane == 0)
+    for (int i = 0; i < 8; ++i) a.prof[(blockIdx.x * a.warps + wl) * 8 + i] = (unsigned long long)w.acc[i];
 }
 
 __global__ void permute_in_kernel(const double *rhs, int64_t ld, const int *pos, int64_t n, int nslab,
@@ -466,16 +858,157 @@ static const std::vector<DevBuf> &permuted_ell(const NDSweepPlan &sp, const NDPl
   return r;
 }
 
+// Build (once per coupling set) the fused slab-coupling program: the coupling rows
+// are split by owner -- subtree rows to their CTA (x_{k-1} of the same subtree read
+// from shared memory, other columns from global memory), top rows balanced over the
+// CTAs (global x).  The end-of-slab cluster barrier makes x_{k-1} visible to all.
+static const CplProgram &get_program(const NDSweepPlan &sp, const NDPlan &p, const SweepCoupling *cpl, int ncpl,
+                                     cudaStream_t s) {
+  const auto key = std::make_pair(cpl[0].col, ncpl > 1 ? cpl[1].col : (const int *)nullptr);
+  auto it = sp.prog_cache.find(key);
+  if (it != sp.prog_cache.end()) return *it->second;
+  auto pg = std::make_unique<CplProgram>();
+  const int64_t n = p.n;
+  const int ncta = sp.ncta;
+  std::vector<int> owner(n, -1);
+  for (int c = 0; c < ncta; ++c)
+    for (int64_t q = sp.sub_info_h[4 * c]; q < sp.sub_info_h[4 * c] + sp.sub_info_h[4 * c + 1]; ++q) owner[q] = c;
+  struct Ent {
+    int col, cid, e;
+  };
+  struct Item {
+    int dst, rhs;
+    std::vector<Ent> ents;
+  };
+  std::vector<std::vector<Item>> items(ncta);
+  // coupling rows in permuted order: (j permuted, coupling id, value index)
+  std::vector<std::vector<int>> rp(ncpl), cl(ncpl);
+  for (int c = 0; c < ncpl; ++c) {
+    rp[c].resize(n + 1);
+    STMHD_CUDA_CHECK(cudaMemcpyAsync(rp[c].data(), cpl[c].rowptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
+    cl[c].resize(std::max(rp[c][n], 1));
+    if (rp[c][n])
+      STMHD_CUDA_CHECK(cudaMemcpy(cl[c].data(), cpl[c].col, rp[c][n] * sizeof(int), cudaMemcpyDeviceToHost));
+  }
+  bool ok = true;
+  std::vector<int64_t> top_rows;
+  for (int64_t q = 0; q < n; ++q)
+    if (owner[q] < 0) top_rows.push_back(q);
+  // entry = signed offset from x_{k-1} (lag 1 -> j, lag 2 -> j - n), or, for lag-1
+  // columns of the CTA's own subtree (still in its shared memory), 2^30 + (j - first)
+  auto entries_of = [&](int64_t q, Item &itm, int own) {
+    const int io = sp.iperm_h[q];
+    for (int c = 0; c < ncpl; ++c)
+      for (int e = rp[c][io]; e < rp[c][io + 1]; ++e) {
+        const int64_t j = sp.pos_h[cl[c][e]];
+        int enc = (int)(j - (int64_t)(cpl[c].lag - 1) * n);
+        if (cpl[c].lag == 1 && own >= 0 && owner[j] == own) enc = (1 << 30) + (int)(j - sp.sub_info_h[4 * own]);
+        itm.ents.push_back({enc, c, e});
+      }
+  };
+  // subtree rows -> their CTA (result into shared memory)
+  for (int64_t q = 0; q < n; ++q) {
+    const int o = owner[q];
+    if (o < 0) continue;
+    Item itm{(int)(q - sp.sub_info_h[4 * o]), (int)q, {}};
+    entries_of(q, itm, o);
+    items[o].push_back(std::move(itm));
+  }
+  // top rows -> balanced over the CTAs (result into global tbuf)
+  std::vector<int> load(ncta);
+  for (int c = 0; c < ncta; ++c) load[c] = (int)items[c].size();
+  for (int64_t q : top_rows) {
+    const int d = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    ++load[d];
+    Item itm{(1 << 29) | (int)q, (int)q, {}};
+    entries_of(q, itm, -1);
+    items[d].push_back(std::move(itm));
+  }
+  if (ok) {
+    require(n < (1 << 28), "sweep coupling program: index overflow");
+    std::vector<int4> hdr(ncta);
+    std::vector<int2> it2;
+    std::vector<int> ecol;
+    std::vector<int2> esrc;
+    for (int c = 0; c < ncta; ++c) {
+      int width = 0;
+      for (auto &x : items[c]) width = std::max(width, (int)x.ents.size());
+      const int ni = (int)items[c].size();
+      hdr[c] = make_int4((int)it2.size(), ni, (int)ecol.size(), width);
+      for (auto &x : items[c]) it2.push_back(make_int2(x.dst, x.rhs));
+      const size_t base = ecol.size();
+      ecol.resize(base + (size_t)width * ni, 0);  // pad: offset 0 with value 0
+      esrc.resize(base + (size_t)width * ni, make_int2(-1, 0));
+      for (int i = 0; i < ni; ++i)
+        for (int sl = 0; sl < (int)items[c][i].ents.size(); ++sl) {
+          const Ent &en = items[c][i].ents[sl];
+          ecol[base + (size_t)sl * ni + i] = en.col;
+          esrc[base + (size_t)sl * ni + i] = make_int2(en.cid, en.e);
+        }
+    }
+    if (ecol.empty()) {
+      ecol.push_back(0);
+      esrc.push_back(make_int2(-1, 0));
+    }
+    pg->nent = (int64_t)ecol.size();
+    pg->hdr = upload_vec(hdr, s);
+    pg->items = upload_vec(it2, s);
+    pg->ecol = upload_vec(ecol, s);
+    pg->esrc = upload_vec(esrc, s);
+    STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (getenv("STMHD_SWEEP_TRACE")) {
+      fprintf(stderr, "[sweep-prog] ncpl %d top rows %zu nent %lld | per CTA items/width:", ncpl,
+              top_rows.size(), (long long)pg->nent);
+      for (int c = 0; c < ncta; ++c) fprintf(stderr, " %d/%d", hdr[c].y, hdr[c].w);
+      fprintf(stderr, "\n");
+    }
+  }
+  pg->ok = ok;
+  const CplProgram &ref = *pg;
+  sp.prog_cache[key] = std::move(pg);
+  return ref;
+}
+
+struct CplVals {
+  const double *val[2];
+  int64_t stride[2], shift[2];
+  double coef[2];
+  int lag[2];
+};
+
+// vals[b][id] = coef * val_c[(b - shift_c) * stride_c + e] for the program entries
+// (b = slab when any coupling has per-slab values or a lag > 1, else a single
+// block); entries whose lag exceeds the slab are zero (their x is not defined)
+__global__ void cpl_vals_kernel(const int2 *esrc, int64_t nent, CplVals cv, int per_slab, double *vals) {
+  const int b = blockIdx.y;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < nent; id += (int64_t)gridDim.x * blockDim.x) {
+    const int2 sr = esrc[id];
+    double v = 0.0;
+    if (sr.x >= 0 && !(per_slab && b < cv.lag[sr.x])) {
+      const int64_t blk = per_slab && cv.stride[sr.x] ? (int64_t)b - cv.shift[sr.x] : 0;
+      if (blk >= 0) v = cv.coef[sr.x] * cv.val[sr.x][blk * cv.stride[sr.x] + sr.y];
+    }
+    vals[(int64_t)b * nent + id] = v;
+  }
+}
+
 void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,
               const SweepCoupling *cpl, int ncpl, cudaStream_t s) {
   const NDDevice &dev = *fac.dev;
   const NDPlan &p = *dev.plan;
   static const int cluster = std::max(2, std::min(16, env_int2("STMHD_SWEEP_CLUSTER", 16)));
   const int warps = 16;
-  const NDSweepPlan &sp = dev.get_sweep_plan(cluster, warps, s);
+  // per warp: gather buffer (max front, rounded to 16 doubles) + two TMA slots
+  int64_t maxb = 2;
+  for (int sn = 0; sn < p.nsn; ++sn) maxb = std::max({maxb, p.bsz_f[sn], p.bsz_b[sn]});
+  const int slot = (int)((maxb + 15) / 16 * 16);
+  const int vstride = (int)(((std::max(dev.max_front, 1) + 15) / 16) * 16 + 2 * slot);
+  const int64_t smem_doubles = 224 * 1024 / 8;
+  const NDSweepPlan &sp = dev.get_sweep_plan(cluster, warps, smem_doubles - (int64_t)warps * vstride, s);
   const int64_t n = p.n;
   static DevBuf scratch;
-  const size_t need = ((size_t)2 * nrhs * n + 2 * n + p.cbv_size + 16) * sizeof(double);
+  const size_t need = ((size_t)2 * nrhs * n + 3 * n + p.cbv_size + 16) * sizeof(double);
   if (scratch.bytes < need) {
     STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
     scratch.alloc(need * 5 / 4);
@@ -485,6 +1018,7 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   double *reff = xp + (int64_t)nrhs * n;
   double *ybuf = reff + n;
   double *cbv = ybuf + n;
+  double *tbuf = cbv + p.cbv_size;
   permute_in_kernel<<<dim3(std::min<int64_t>(cdiv(n, 256), 256), nrhs), 256, 0, s>>>(rhs, ld_rhs, sp.pos.as<int>(), n,
                                                                                     nrhs, rhsp);
   STMHD_LAUNCH_CHECK();
@@ -493,6 +1027,18 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   a.btask = sp.bwd_tasks.as<SweepTask>();
   a.fwptr = sp.fwd_wptr.as<int>();
   a.bwptr = sp.bwd_wptr.as<int>();
+  a.sftask = sp.sf_tasks.as<SweepTask>();
+  a.sbtask = sp.sb_tasks.as<SweepTask>();
+  a.sfwptr = sp.sf_wptr.as<int>();
+  a.sbwptr = sp.sb_wptr.as<int>();
+  a.sub_info = sp.sub_info.as<int64_t>();
+  a.ntop = sp.ntop;
+  a.nsub = sp.nsub;
+  a.warps = warps;
+  a.sub_len = sp.sub_len;
+  a.sub_cb = sp.sub_cb;
+  a.pf_ptr = sp.pf_ptr.as<int>();
+  a.pf_items = sp.pf_items.as<longlong2>();
   a.g3p = sp.g3p.as<int4>();
   a.bpos = sp.bpos.as<int>();
   a.nlevels = p.nlevels;
@@ -520,34 +1066,72 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
     a.cpl[c].lag = cpl[c].lag;
     a.cpl[c].coef = cpl[c].coef;
   }
-  // per warp: gather buffer (max front, rounded to 16 doubles) + two TMA slots
-  int64_t maxb = 2;
-  for (int sn = 0; sn < p.nsn; ++sn) maxb = std::max({maxb, p.bsz_f[sn], p.bsz_b[sn]});
-  a.slot = (int)((maxb + 15) / 16 * 16);
-  a.vstride = (int)(((std::max(dev.max_front, 1) + 15) / 16) * 16 + 2 * a.slot);
-  static const int prefetch = env_int2("STMHD_SWEEP_PREFETCH", 0);  // TMA streaming makes it redundant
+  static const int fused_env = env_int2("STMHD_SWEEP_FUSED", 1);
+  if (fused_env && ncpl > 0 && sp.nsub > 0) {
+    const CplProgram &pg = get_program(sp, p, cpl, ncpl, s);
+    if (pg.ok) {
+      int per_slab = 0;
+      CplVals cv{};
+      for (int c = 0; c < ncpl; ++c) {
+        per_slab |= cpl[c].val_stride != 0 || cpl[c].lag > 1;
+        cv.lag[c] = cpl[c].lag;
+        cv.val[c] = cpl[c].val;
+        cv.stride[c] = cpl[c].val_stride;
+        cv.shift[c] = cpl[c].val_shift;
+        cv.coef[c] = cpl[c].coef;
+      }
+      const int nblk = per_slab ? nrhs : 1;
+      static DevBuf pvals;
+      const size_t vneed = (size_t)nblk * pg.nent * sizeof(double);
+      if (pvals.bytes < vneed) {
+        STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
+        pvals.alloc(vneed * 5 / 4);
+      }
+      cpl_vals_kernel<<<dim3((unsigned)std::min<int64_t>(cdiv(pg.nent, 256), 1024), nblk), 256, 0, s>>>(
+          pg.esrc.as<int2>(), pg.nent, cv, per_slab, pvals.as<double>());
+      STMHD_LAUNCH_CHECK();
+      a.prog_hdr = pg.hdr.as<int4>();
+      a.prog_items = pg.items.as<int2>();
+      a.prog_ecol = pg.ecol.as<int>();
+      a.prog_vals = pvals.as<double>();
+      a.prog_nent = pg.nent;
+      a.prog_per_slab = per_slab;
+      a.tbuf = tbuf;
+    }
+  }
+  a.slot = slot;
+  a.vstride = vstride;
+  static const int prefetch = env_int2("STMHD_SWEEP_PREFETCH", 8);  // L2 prefetch distance (chunks)
   a.prefetch = prefetch;
   a.null_work = env_int2("STMHD_SWEEP_NULL", 0);
   const int threads = warps * 32;
-  const size_t smem = (size_t)warps * a.vstride * sizeof(double);
-  require(smem <= 224 * 1024, "nd sweep: front too large for shared memory");
+  const size_t smem = ((size_t)warps * a.vstride + 3 * a.sub_len + a.sub_cb) * sizeof(double);
+  require(smem <= 224 * 1024, "nd sweep: subtree vectors or fronts too large for shared memory");
   static bool attr = false;
   if (!attr) {
     cudaFuncAttributes fa{};
-    STMHD_CUDA_CHECK(cudaFuncGetAttributes(&fa, (const void *)nd_sweep_kernel));
-    STMHD_CUDA_CHECK(cudaFuncSetAttribute(nd_sweep_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    STMHD_CUDA_CHECK(cudaFuncSetAttribute(nd_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)(227 * 1024 - fa.sharedSizeBytes)));
+    for (const void *fn : {(const void *)nd_sweep_kernel<false>, (const void *)nd_sweep_kernel<true>}) {
+      STMHD_CUDA_CHECK(cudaFuncGetAttributes(&fa, fn));
+      STMHD_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      STMHD_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)(227 * 1024 - fa.sharedSizeBytes)));
+    }
     attr = true;
   }
   static const int trace_on = env_int2("STMHD_SWEEP_TRACE", 0);
   DevBuf tr;
   int nsteps = 0;
   if (trace_on) {
-    nsteps = 2 + nrhs * (2 * p.nlevels + 1);
+    nsteps = 4 + nrhs * (2 * p.nlevels + 4);
     tr.alloc(nsteps * sizeof(unsigned long long));
     STMHD_CUDA_CHECK(cudaMemsetAsync(tr.ptr, 0, tr.bytes, s));
     a.trace = tr.as<unsigned long long>();
+  }
+  static const int prof_on = env_int2("STMHD_SWEEP_PROF", 0);
+  DevBuf pr;
+  if (prof_on) {
+    pr.alloc((size_t)cluster * warps * 8 * sizeof(unsigned long long));
+    a.prof = pr.as<unsigned long long>();
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cluster);
@@ -562,7 +1146,8 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   cfg.attrs = at;
   cfg.numAttrs = 1;
   void *args[] = {&a};
-  STMHD_CUDA_CHECK(cudaLaunchKernelExC(&cfg, (const void *)nd_sweep_kernel, args));
+  STMHD_CUDA_CHECK(cudaLaunchKernelExC(
+      &cfg, prof_on ? (const void *)nd_sweep_kernel<true> : (const void *)nd_sweep_kernel<false>, args));
   count_launch();
   permute_out_kernel<<<dim3(std::min<int64_t>(cdiv(n, 256), 256), nrhs), 256, 0, s>>>(xp, sp.pos.as<int>(), n, nrhs, x,
                                                                                      ld_x);
@@ -571,11 +1156,34 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
     std::vector<unsigned long long> h(nsteps);
     STMHD_CUDA_CHECK(cudaMemcpyAsync(h.data(), tr.ptr, nsteps * 8, cudaMemcpyDeviceToHost, s));
     STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-    const int per = 2 * p.nlevels + 1, base = 1 + per;
-    fprintf(stderr, "[sweep] n=%lld levels=%d total=%.1f us | slab1 (us):", (long long)n, p.nlevels,
-            (*std::max_element(h.begin(), h.end()) - h[0]) / 1e3);
+    const bool fz = a.prog_hdr != nullptr;
+    auto entries = [&](int k) {
+      return (int)fz + (k > 0 && a.ncpl && !fz) + (a.nsub ? 1 : 0) + 2 * a.ntop + (a.nsub && k + 1 < a.nslab);
+    };
+    const int per = entries(1), base = 1 + entries(0);
+    fprintf(stderr, "[sweep] n=%lld levels=%d top=%d sub=%d fused=%d total=%.1f us | slab1 (us):", (long long)n,
+            p.nlevels, a.ntop, a.nsub, (int)fz, (*std::max_element(h.begin(), h.end()) - h[0]) / 1e3);
     for (int i = 0; i < per && base + i < nsteps; ++i) fprintf(stderr, " %.2f", (h[base + i] - h[base + i - 1]) / 1e3);
-    fprintf(stderr, "\n");
+    fprintf(stderr, "\n[sweep] factor/slab %.2f MB nslab %d (batch %d) smem %zu B vstride %d slot %d sub_len %lld sub_cb %lld\n",
+            p.factor_size * 8e-6, nrhs, fac.nbatch, smem, a.vstride, a.slot, (long long)a.sub_len, (long long)a.sub_cb);
+  }
+  if (prof_on) {
+    const int nwp = cluster * warps;
+    std::vector<unsigned long long> h((size_t)nwp * 8);
+    STMHD_CUDA_CHECK(cudaMemcpyAsync(h.data(), pr.ptr, h.size() * 8, cudaMemcpyDeviceToHost, s));
+    STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
+    double mean[8] = {0}, mx[8] = {0};
+    for (int w = 0; w < nwp; ++w)
+      for (int i = 0; i < 8; ++i) {
+        mean[i] += (double)h[w * 8 + i] / nwp;
+        mx[i] = std::max(mx[i], (double)h[w * 8 + i]);
+      }
+    const double us = 1.0 / 1963.0 / nrhs;  // cycles -> us per slab at the loaded SM clock
+    fprintf(stderr,
+            "[sweep-prof] per slab per warp (us) mean/max: gather %.2f/%.2f wait %.2f/%.2f gemv %.2f/%.2f "
+            "barrier %.2f/%.2f | tasks %.1f/%.0f chunks %.1f/%.0f | gemv-only fwd %.2f bwd %.2f\n",
+            mean[0] * us, mx[0] * us, mean[1] * us, mx[1] * us, mean[2] * us, mx[2] * us, mean[3] * us, mx[3] * us,
+            mean[4] / nrhs, mx[4] / nrhs, mean[5] / nrhs, mx[5] / nrhs, mean[6] * us, mean[7] * us);
   }
 }
 
