@@ -60,16 +60,21 @@ struct NDPlan {
 NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const int32_t *gx,
                   const int32_t *gy, int leaf_max, const int32_t *value_map);
 
-// Work list of the cluster-resident time sweep (nd_sweep.cu), built lazily for
-// a launch shape: per level and warp, contiguous chunk ranges of one supernode.
+// Work item of the cluster-resident time sweep (nd_sweep.cu), built lazily for a
+// launch shape: a contiguous chunk range of one supernode.  32 bytes, so a warp's
+// whole task list sits in shared memory.
 struct alignas(16) SweepTask {
-  int flags, c0, c1, R;  // flags: 1 = write the update vector to global memory; chunk range; rows per chunk
-  int ns, f, rows, bsz;  // bsz: doubles per chunk block
-  int64_t foff;   // offset of chunk 0 (forward FL or backward FU blocks)
-  int64_t goff;   // offset of the supernode's front tables
-  int64_t first;  // elimination position of the first column
-  int64_t cboff;  // update-vector offset
+  int foff;             // offset of chunk 0 in a slab's factors (forward FL or backward FU blocks)
+  int goff;             // offset of the supernode's front tables
+  int first;            // elimination position of the first column
+  int cboff;            // update-vector offset
+  short c0, c1;         // chunk range
+  short ns, f, rows;    // columns, front size, rows of the step (f forward, ns backward)
+  unsigned char R;      // rows per chunk (power of two <= 32)
+  unsigned char flags;  // 1 = write the update vector to global memory
+  int bsz;              // doubles per chunk block
 };
+static_assert(sizeof(SweepTask) == 32, "SweepTask must stay 32 bytes");
 
 // Slab-coupling "program" of a sweep with subtrees: per CTA, the output items it
 // computes at the start of every slab (its subtree rows into shared memory and a
@@ -85,16 +90,16 @@ struct CplProgram {
 
 struct NDSweepPlan {
   int ncta = 0, warps = 0;
-  // top of the tree (cluster-wide level steps): task ranges per [top level][global warp]
-  int ntop = 0;
-  DevBuf fwd_tasks, bwd_tasks, fwd_wptr, bwd_wptr;
-  // bottom subtrees, one per CTA (CTA-local level steps, data in shared memory):
-  // task ranges per [cta][local level][warp]
-  int nsub = 0;                  // local levels (0 = no subtree phase)
+  // top of the tree: cluster-wide level steps (ntop); bottom: one subtree per CTA,
+  // CTA-local level steps (nsub, 0 = none) with its vectors in shared memory
+  int ntop = 0, nsub = 0;
   int64_t sub_len = 0, sub_cb = 0;  // max subtree columns / internal update-vector doubles per CTA
-  DevBuf sf_tasks, sb_tasks, sf_wptr, sb_wptr;
-  DevBuf sub_info;               // per CTA int64 {first col, ncols, first cb, ncb}
-  DevBuf pf_ptr, pf_items;       // per physical warp: its factor-chunk stream for one slab
+  DevBuf sub_info;                  // per CTA int64 {first col, ncols, first cb, ncb}
+  // per physical warp (cta * warps + w): its task list for one slab in kernel order
+  // (subtree forward levels, top forward, top backward, subtree backward) and the
+  // start of every phase level in it (nl = 2 nsub + 2 ntop levels, nl + 1 bounds)
+  int nl = 0, max_wtasks = 0;
+  DevBuf wl_tasks, wl_off, wl_bnd;
   DevBuf g3p;   // int4 per front position: {permuted rhs index or -1, cb1, cb2, 0}
   DevBuf bpos;  // int per front position: permuted position of the front entry
   DevBuf pos;   // n: elimination position of each original index
@@ -122,7 +127,7 @@ struct NDDevice {
   int max_front = 0;
   void build(const NDPlan &p, cudaStream_t s);
   mutable std::unique_ptr<NDSweepPlan> sweep_plan;
-  const NDSweepPlan &get_sweep_plan(int ncta, int warps, int64_t sub_budget, cudaStream_t s) const;
+  const NDSweepPlan &get_sweep_plan(int ncta, int warps, int64_t sub_budget, cudaStream_t s, bool flat = false) const;
 };
 
 // A coupling term of a sequential block sweep:

@@ -31,7 +31,8 @@ static int env_int2(const char *name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_budget, cudaStream_t s) const {
+const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_budget, cudaStream_t s,
+                                            bool flat) const {
   if (sweep_plan && sweep_plan->ncta == ncta && sweep_plan->warps == warps) return *sweep_plan;
   const NDPlan &p = *plan;
   auto sp = std::make_unique<NDSweepPlan>();
@@ -81,7 +82,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
     const char *e = getenv("STMHD_SWEEP_SUBTREES");
     return e ? atoi(e) : 1;
   }();
-  if (!sub_env) D = 0;
+  if (!sub_env || flat) D = 0;
   // subtree membership: owner CTA of every supernode at depth >= D (D > 0); falls
   // back to an all-top schedule when the subtree vectors exceed shared memory
   std::vector<int> owner, roots;
@@ -140,13 +141,24 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
     return true;
   };
   auto make_task = [&](const SN &x, int c0, int c1, bool fwd, bool cb_global) {
+    const int64_t foff = fwd ? p.fl_off[x.s] : p.fu_off[x.s];
+    const int f = p.ns[x.s] + p.nb[x.s];
+    require(foff + (int64_t)x.m * (fwd ? p.bsz_f[x.s] : p.bsz_b[x.s]) < INT32_MAX && p.idx_off[x.s] < INT32_MAX &&
+                p.cbv_off[x.s] < INT32_MAX && f < 32768 && x.m < 32768,
+            "nd sweep: factor too large for the compact task layout");
     SweepTask t{};
+    t.foff = (int)foff;
+    t.goff = (int)p.idx_off[x.s];
+    t.first = (int)p.first[x.s];
+    t.cboff = (int)p.cbv_off[x.s];
+    t.c0 = (short)c0;
+    t.c1 = (short)c1;
+    t.ns = (short)p.ns[x.s];
+    t.f = (short)f;
+    t.rows = (short)x.rows;
+    t.R = (unsigned char)x.R;
     t.flags = cb_global ? 1 : 0;
-    t.c0 = c0; t.c1 = c1; t.R = x.R;
-    t.ns = p.ns[x.s]; t.f = p.ns[x.s] + p.nb[x.s]; t.rows = x.rows;
     t.bsz = (int)(fwd ? p.bsz_f[x.s] : p.bsz_b[x.s]);
-    t.foff = fwd ? p.fl_off[x.s] : p.fu_off[x.s];
-    t.goff = p.idx_off[x.s]; t.first = p.first[x.s]; t.cboff = p.cbv_off[x.s];
     return t;
   };
   // LPT of a set of supernodes onto `nw` warps; pieces split big supernodes
@@ -191,15 +203,18 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
   sp->nsub = roots.empty() ? 0 : nsub;
   sp->sub_len = maxlen;
   sp->sub_cb = maxcb;
-  std::vector<SweepTask> h_tasks[2], h_stasks[2];
-  std::vector<int> h_wptr[2], h_swptr[2];
-  auto build_dir = [&](bool fwd, DevBuf &tasks_d, DevBuf &wptr_d, DevBuf &stasks_d, DevBuf &swptr_d) {
-    std::vector<SweepTask> &tasks = h_tasks[fwd], &stasks = h_stasks[fwd];
-    std::vector<int> &wptr = h_wptr[fwd], &swptr = h_swptr[fwd];
-    for (int l : top_levels) {
+  // per direction: top tasks per [top level][global warp], subtree tasks per
+  // [cta][local level][warp]
+  std::vector<std::vector<SweepTask>> top_t[2], sub_t[2];
+  auto build_dir = [&](bool fwd) {
+    auto &tt = top_t[fwd];
+    auto &st = sub_t[fwd];
+    tt.assign((size_t)sp->ntop * W, {});
+    st.assign((size_t)ncta * sp->nsub * warps, {});
+    for (int t = 0; t < sp->ntop; ++t) {
       std::vector<SN> sns;
       std::vector<char> cbg;
-      for (int sn : p.level_sn[l]) {
+      for (int sn : p.level_sn[top_levels[t]]) {
         SN x;
         if (owner[sn] < 0 && make_sn(sn, fwd, x)) {
           sns.push_back(x);
@@ -208,12 +223,8 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
       }
       std::vector<std::vector<SweepTask>> per;
       schedule(sns, W, fwd, per, cbg);
-      for (int w = 0; w < W; ++w) {
-        wptr.push_back((int)tasks.size());
-        tasks.insert(tasks.end(), per[w].begin(), per[w].end());
-      }
+      for (int w = 0; w < W; ++w) tt[(size_t)t * W + w] = std::move(per[w]);
     }
-    wptr.push_back((int)tasks.size());
     for (int c = 0; c < ncta; ++c)
       for (int h = 0; h < sp->nsub; ++h) {
         std::vector<SN> sns;
@@ -228,54 +239,43 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
           }
         std::vector<std::vector<SweepTask>> per;
         schedule(sns, warps, fwd, per, cbg);
-        for (int w = 0; w < warps; ++w) {
-          swptr.push_back((int)stasks.size());
-          stasks.insert(stasks.end(), per[w].begin(), per[w].end());
-        }
+        for (int w = 0; w < warps; ++w) st[((size_t)c * sp->nsub + h) * warps + w] = std::move(per[w]);
       }
-    swptr.push_back((int)stasks.size());
-    if (stasks.empty()) stasks.push_back(SweepTask{});
-    tasks_d = upload_vec(tasks, s);
-    wptr_d = upload_vec(wptr, s);
-    stasks_d = upload_vec(stasks, s);
-    swptr_d = upload_vec(swptr, s);
   };
-  build_dir(true, sp->fwd_tasks, sp->fwd_wptr, sp->sf_tasks, sp->sf_wptr);
-  build_dir(false, sp->bwd_tasks, sp->bwd_wptr, sp->sb_tasks, sp->sb_wptr);
-  // per physical warp (cta c, warp w): the factor chunks it consumes in one slab, in
-  // kernel order (subtree fwd, top fwd, top bwd, subtree bwd) -- the L2 prefetch stream
+  build_dir(true);
+  build_dir(false);
+  // per physical warp (cta c, warp w; top-phase global warp id w * ncta + c): its
+  // list in kernel order and the bound of every phase level
+  sp->nl = 2 * sp->nsub + 2 * sp->ntop;
   {
-    std::vector<int> pptr;
-    std::vector<longlong2> items;
-    auto add = [&](const std::vector<SweepTask> &ts, int b, int e) {
-      for (int i = b; i < e; ++i)
-        for (int c = ts[i].c0; c < ts[i].c1; ++c)
-          items.push_back(make_longlong2(ts[i].foff + (int64_t)c * ts[i].bsz, ts[i].bsz));
-    };
+    std::vector<SweepTask> all;
+    std::vector<int> off, bnd;
+    int maxw = 0;
     for (int c = 0; c < ncta; ++c)
       for (int w = 0; w < warps; ++w) {
-        pptr.push_back((int)items.size());
-        for (int h = 0; h < sp->nsub; ++h) {
-          const int q = (c * sp->nsub + h) * warps + w;
-          add(h_stasks[1], h_swptr[1][q], h_swptr[1][q + 1]);
-        }
-        for (int t = 0; t < sp->ntop; ++t) {
-          const int q = t * W + w * ncta + c;
-          add(h_tasks[1], h_wptr[1][q], h_wptr[1][q + 1]);
-        }
-        for (int t = sp->ntop - 1; t >= 0; --t) {
-          const int q = t * W + w * ncta + c;
-          add(h_tasks[0], h_wptr[0][q], h_wptr[0][q + 1]);
-        }
-        for (int h = sp->nsub - 1; h >= 0; --h) {
-          const int q = (c * sp->nsub + h) * warps + w;
-          add(h_stasks[0], h_swptr[0][q], h_swptr[0][q + 1]);
-        }
+        off.push_back((int)all.size());
+        const size_t o = all.size();
+        auto add = [&](const std::vector<SweepTask> &v) {
+          bnd.push_back((int)(all.size() - o));
+          all.insert(all.end(), v.begin(), v.end());
+        };
+        for (int h = 0; h < sp->nsub; ++h) add(sub_t[1][((size_t)c * sp->nsub + h) * warps + w]);
+        for (int t = 0; t < sp->ntop; ++t) add(top_t[1][(size_t)t * W + w * ncta + c]);
+        for (int t = sp->ntop - 1; t >= 0; --t) add(top_t[0][(size_t)t * W + w * ncta + c]);
+        for (int h = sp->nsub - 1; h >= 0; --h) add(sub_t[0][((size_t)c * sp->nsub + h) * warps + w]);
+        bnd.push_back((int)(all.size() - o));
+        maxw = std::max(maxw, (int)(all.size() - o));
       }
-    pptr.push_back((int)items.size());
-    if (items.empty()) items.push_back(make_longlong2(0, 0));
-    sp->pf_ptr = upload_vec(pptr, s);
-    sp->pf_items = upload_vec(items, s);
+    off.push_back((int)all.size());
+    if (all.empty()) all.push_back(SweepTask{});
+    sp->max_wtasks = maxw;
+    // shared memory: subtree vectors + per-warp task lists must fit next to the
+    // per-warp gather buffers; otherwise fall back to an all-top schedule
+    const int64_t tdoubles = (int64_t)warps * (((sp->nl + 1 + 3) / 4) * 16 + (int64_t)maxw * 32) / 8;
+    if (!flat && D > 0 && 3 * maxlen + maxcb + tdoubles > sub_budget) return get_sweep_plan(ncta, warps, sub_budget, s, true);
+    sp->wl_tasks = upload_vec(all, s);
+    sp->wl_off = upload_vec(off, s);
+    sp->wl_bnd = upload_vec(bnd, s);
   }
   sp->sub_info = upload_vec(info, s);
   sp->sub_info_h = info;
@@ -301,10 +301,10 @@ struct SweepCpl {
 };
 
 struct SweepArgs {
-  const SweepTask *ftask, *btask;
-  const int *fwptr, *bwptr;  // per top level W entries (+ one final sentinel)
-  const SweepTask *sftask, *sbtask;
-  const int *sfwptr, *sbwptr;  // per [cta][local level] `warps` entries (+ sentinel)
+  // per physical warp task lists (NDSweepPlan::wl_*), copied to shared memory
+  const SweepTask *wl_tasks;
+  const int *wl_off, *wl_bnd;
+  int nl, tstride;             // phase levels; bytes of shared memory per warp list
   const int64_t *sub_info;     // per CTA {first col, ncols, first cb, ncb}
   int ntop, nsub, warps;
   int64_t sub_len, sub_cb;     // shared-memory sizes of the subtree vectors
@@ -316,8 +316,6 @@ struct SweepArgs {
   int64_t prog_nent;
   int prog_per_slab;
   double *tbuf;                // coupled right-hand side of the top rows
-  const int *pf_ptr;           // per physical warp: range of its chunk stream
-  const longlong2 *pf_items;   // {offset in a slab's factors, doubles}
   const int4 *g3p;
   const int *bpos;
   int nlevels, nw;
@@ -332,7 +330,6 @@ struct SweepArgs {
   int ncpl;
   int vstride;  // doubles per warp: gather buffer + 2 TMA slots
   int slot;     // doubles per TMA slot (largest chunk block)
-  int prefetch;
   int null_work;  // diagnostics: skip all task work (barrier/loop floor)
   unsigned long long *trace;
   unsigned long long *prof;  // PROF instantiation: 6 counters per warp
@@ -379,13 +376,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
   } while (!done);
 }
 
-// Issue the first (up to) two factor-chunk loads of a task.
-__device__ __forceinline__ void task_begin(const SweepTask &tk, const double *F, double *slot0, int slotsz,
-                                           unsigned long long (*bar)[2], int wl) {
-  tma_load(slot0, F + tk.foff + (int64_t)tk.c0 * tk.bsz, tk.bsz, &bar[wl][0]);
-  if (tk.c0 + 1 < tk.c1) tma_load(slot0 + slotsz, F + tk.foff + (int64_t)(tk.c0 + 1) * tk.bsz, tk.bsz, &bar[wl][1]);
-}
-
 // Per-CTA view of the subtree vectors kept in shared memory.
 struct SubView {
   double *ys, *xs, *cbs, *rhs_s;  // rhs_s: coupled right-hand side of the subtree rows (fused mode)
@@ -395,12 +385,14 @@ struct SubView {
 struct WarpCtx {
   int lane, wl;
   double *v;
-  double *slot0;   // two TMA slots: slot0, slot0 + slotsz
+  double *slot0;  // two TMA slots: slot0, slot0 + slotsz
   int slotsz;
-  unsigned phase;  // bit sl = parity of slot sl
-  // L2 prefetch cursor along this warp's chunk stream (lane 0 only)
-  const longlong2 *pf;
-  int pfn, pidx, pslab;
+  // this warp's task list for one slab (shared memory; repeated for every slab)
+  const SweepTask *tl;
+  const int *bnd;  // start of every phase level in tl (nl + 1 entries)
+  int nt;
+  int jc;                       // chunks consumed (slot jc & 1, mbarrier parity (jc >> 1) & 1)
+  int icount, rt, rc, rslab;    // TMA ring cursor (lane 0): two chunks ahead of jc
   // PROF instantiation: cycles in gather / TMA wait / GEMV+store / barriers, tasks, chunks
   long long acc[8];
 };
@@ -411,19 +403,22 @@ __device__ __forceinline__ long long pclock() {
   else return 0;
 }
 
-__device__ __forceinline__ void l2_prefetch(const void *src, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
-}
-
-// Advance the prefetch cursor by one chunk (it runs a.prefetch chunks ahead of the
-// consumer, across level, phase and slab boundaries).
-__device__ __forceinline__ void pf_advance(const SweepArgs &a, WarpCtx &w) {
-  if (w.pslab < (a.fstride ? a.nslab : 1) && w.pfn > 0) {
-    const longlong2 it = w.pf[w.pidx];
-    l2_prefetch(a.factors + (int64_t)w.pslab * a.fstride + it.x, (unsigned)it.y * 8u);
-    if (++w.pidx == w.pfn) {
-      w.pidx = 0;
-      ++w.pslab;
+// Issue the next chunk of the warp's chunk sequence into the free slot (lane 0).
+// The ring runs across task, level and slab boundaries (factors do not depend on
+// the data), so a warp's next chunks are in flight while it waits at a barrier.
+__device__ __forceinline__ void ring_issue(const SweepArgs &a, WarpCtx &w, unsigned long long (*mbar)[2]) {
+  if (w.rslab < a.nslab && w.nt > 0) {
+    const SweepTask &t = w.tl[w.rt];
+    const int sl = w.icount & 1;
+    tma_load(w.slot0 + sl * w.slotsz, a.factors + (int64_t)w.rslab * a.fstride + t.foff + (int64_t)w.rc * t.bsz,
+             t.bsz, &mbar[w.wl][sl]);
+    ++w.icount;
+    if (++w.rc == t.c1) {
+      if (++w.rt == w.nt) {
+        w.rt = 0;
+        ++w.rslab;
+      }
+      w.rc = w.tl[w.rt].c0;
     }
   }
 }
@@ -457,7 +452,6 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
                                              unsigned long long (*mbar)[2]) {
   const int lane = w.lane;
   long long t0 = pclock<PROF>();
-  if (lane == 0) task_begin(tk, F, w.slot0, w.slotsz, mbar, w.wl);
   const int4 *g = a.g3p + tk.goff;
   const double *cbsrc = SUB ? sv.cbs - sv.cbfirst : a.cbv;
   // fused coupling: subtree rows come from shared memory, top rows from tbuf
@@ -488,10 +482,8 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
   double *ydst = SUB ? sv.ys - sv.first : a.ybuf;
   double *cbdst = (!SUB || (tk.flags & 1)) ? a.cbv : sv.cbs - sv.cbfirst;
   for (int c = tk.c0; c < tk.c1; ++c) {
-    const int sl = (c - tk.c0) & 1;
-    if (lane == 0 && a.prefetch) pf_advance(a, w);
-    mbar_wait(&mbar[w.wl][sl], (w.phase >> sl) & 1u);
-    w.phase ^= 1u << sl;
+    const int sl = w.jc & 1;
+    mbar_wait(&mbar[w.wl][sl], (unsigned)(w.jc >> 1) & 1u);
     const double *blk = w.slot0 + sl * w.slotsz;
     if (PROF) {
       const long long t1 = pclock<PROF>();
@@ -510,7 +502,8 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
       else cbdst[tk.cboff + r - tk.ns] = w.v[r] - out;
     }
     __syncwarp();
-    if (lane == 0 && c + 2 < tk.c1) tma_load(w.slot0 + sl * w.slotsz, F + tk.foff + (int64_t)(c + 2) * tk.bsz, tk.bsz, &mbar[w.wl][sl]);
+    ++w.jc;
+    if (lane == 0) ring_issue(a, w, mbar);
     if (PROF) {
       const long long t1 = pclock<PROF>();
       w.acc[2] += t1 - t0;
@@ -526,7 +519,6 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
                                               const SubView &sv, WarpCtx &w, unsigned long long (*mbar)[2]) {
   const int lane = w.lane;
   long long t0 = pclock<PROF>();
-  if (lane == 0) task_begin(tk, F, w.slot0, w.slotsz, mbar, w.wl);
   const int *bp = a.bpos + tk.goff;
   const double *y = (SUB ? sv.ys - sv.first : a.ybuf) + tk.first;
   for (int b0 = lane; b0 < tk.f; b0 += 256) {
@@ -560,10 +552,8 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
   }
   const int R = tk.R, lgR = __ffs(R) - 1, kl = 32 >> lgR, kq = lane >> lgR;
   for (int c = tk.c0; c < tk.c1; ++c) {
-    const int sl = (c - tk.c0) & 1;
-    if (lane == 0 && a.prefetch) pf_advance(a, w);
-    mbar_wait(&mbar[w.wl][sl], (w.phase >> sl) & 1u);
-    w.phase ^= 1u << sl;
+    const int sl = w.jc & 1;
+    mbar_wait(&mbar[w.wl][sl], (unsigned)(w.jc >> 1) & 1u);
     const double *blk = w.slot0 + sl * w.slotsz;
     if (PROF) {
       const long long t1 = pclock<PROF>();
@@ -582,7 +572,8 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
       if (SUB) sv.xs[tk.first + r - sv.first] = out;
     }
     __syncwarp();
-    if (lane == 0 && c + 2 < tk.c1) tma_load(w.slot0 + sl * w.slotsz, F + tk.foff + (int64_t)(c + 2) * tk.bsz, tk.bsz, &mbar[w.wl][sl]);
+    ++w.jc;
+    if (lane == 0) ring_issue(a, w, mbar);
     if (PROF) {
       const long long t1 = pclock<PROF>();
       w.acc[2] += t1 - t0;
@@ -604,17 +595,9 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
   w.v = sm + wl * a.vstride;
   w.slot0 = w.v + (a.vstride - 2 * a.slot);
   w.slotsz = a.slot;
-  w.phase = 0u;
+  w.jc = w.icount = w.rt = w.rc = w.rslab = 0;
   for (int i = 0; i < 8; ++i) w.acc[i] = 0;
   long long tb = 0;
-  {
-    const int gid = blockIdx.x * a.warps + wl;
-    w.pf = a.pf_items + a.pf_ptr[gid];
-    w.pfn = a.pf_ptr[gid + 1] - a.pf_ptr[gid];
-    w.pidx = w.pslab = 0;
-    if (lane == 0 && !a.null_work)
-      for (int i = 0; i < a.prefetch; ++i) pf_advance(a, w);
-  }
   SubView sv;
   sv.ys = sm + (int64_t)a.warps * a.vstride;
   sv.xs = sv.ys + a.sub_len;
@@ -623,10 +606,34 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
   sv.first = a.sub_info[4 * blockIdx.x + 0];
   sv.len = a.sub_info[4 * blockIdx.x + 1];
   sv.cbfirst = a.sub_info[4 * blockIdx.x + 2];
+  {
+    // copy this warp's task list and level bounds into shared memory (static for
+    // the whole sweep: no global round trip per level or task afterwards)
+    const int gid = blockIdx.x * a.warps + wl;
+    const uintptr_t base = (reinterpret_cast<uintptr_t>(sv.rhs_s + a.sub_len) + 15) & ~(uintptr_t)15;
+    char *area = reinterpret_cast<char *>(base) + (size_t)wl * a.tstride;
+    int *bnd = reinterpret_cast<int *>(area);
+    SweepTask *tl = reinterpret_cast<SweepTask *>(area + ((a.nl + 1 + 3) / 4) * 16);
+    const int o = a.wl_off[gid];
+    const int nt = a.wl_off[gid + 1] - o;
+    for (int i = lane; i <= a.nl; i += 32) bnd[i] = a.wl_bnd[(size_t)gid * (a.nl + 1) + i];
+    const int4 *src = reinterpret_cast<const int4 *>(a.wl_tasks + o);
+    int4 *dst = reinterpret_cast<int4 *>(tl);
+    for (int i = lane; i < 2 * nt; i += 32) dst[i] = src[i];
+    __syncwarp();
+    w.tl = tl;
+    w.bnd = bnd;
+    w.nt = nt;
+    if (nt > 0) w.rc = tl[0].c0;
+  }
   if (lane == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[wl][0])) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[wl][1])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    if (!a.null_work) {  // fill the TMA ring
+      ring_issue(a, w, mbar);
+      ring_issue(a, w, mbar);
+    }
   }
   __syncwarp();
   const int64_t n = a.n;
@@ -745,38 +752,27 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
       rhs = a.reff;
     }
     const double *F = a.factors + (int64_t)k * a.fstride;
-    // ---- forward: bottom subtrees (CTA-local), then the top (cluster-wide) ----
-    for (int h = 0; h < a.nsub; ++h) {
-      const int *wp = a.sfwptr + ((int64_t)blockIdx.x * a.nsub + h) * a.warps + wl;
-      const int t1 = a.null_work ? wp[0] : wp[1];
-      for (int ti = wp[0]; ti < t1; ++ti) {
-        const SweepTask tk = a.sftask[ti];
-        forward_task<true, PROF>(a, tk, F, rhs, sv, w, mbar);
-      }
+    // phase levels of this warp's list: subtree forward (CTA-local), top forward,
+    // top backward (cluster-wide), subtree backward (CTA-local)
+    int L = 0;
+    for (int h = 0; h < a.nsub; ++h, ++L) {
+      const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
+      for (int ti = w.bnd[L]; ti < t1; ++ti) forward_task<true, PROF>(a, w.tl[ti], F, rhs, sv, w, mbar);
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
     }
     if (a.nsub) {
       tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step);
     }
-    for (int t = 0; t < a.ntop; ++t) {
-      const int *wp = a.fwptr + (int64_t)t * a.nw + gw;
-      const int t1 = a.null_work ? wp[0] : wp[1];
-      for (int ti = wp[0]; ti < t1; ++ti) {
-        const SweepTask tk = a.ftask[ti];
-        forward_task<false, PROF>(a, tk, F, rhs, sv, w, mbar);
-      }
+    for (int t = 0; t < a.ntop; ++t, ++L) {
+      const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
+      for (int ti = w.bnd[L]; ti < t1; ++ti) forward_task<false, PROF>(a, w.tl[ti], F, rhs, sv, w, mbar);
       tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step);
     }
-    // ---- backward: the top, then the bottom subtrees ----
-    for (int t = a.ntop - 1; t >= 0; --t) {
-      const int *wp = a.bwptr + (int64_t)t * a.nw + gw;
-      const int t1 = a.null_work ? wp[0] : wp[1];
-      for (int ti = wp[0]; ti < t1; ++ti) {
-        const SweepTask tk = a.btask[ti];
-        backward_task<false, PROF>(a, tk, F, x, sv, w, mbar);
-      }
+    for (int t = a.ntop - 1; t >= 0; --t, ++L) {
+      const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
+      for (int ti = w.bnd[L]; ti < t1; ++ti) backward_task<false, PROF>(a, w.tl[ti], F, x, sv, w, mbar);
       if (t > 0 || a.nsub || k + 1 < a.nslab) {
         tb = pclock<PROF>();
         sweep_barrier();
@@ -784,13 +780,9 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
       }
       sweep_trace(a, step);
     }
-    for (int h = a.nsub - 1; h >= 0; --h) {
-      const int *wp = a.sbwptr + ((int64_t)blockIdx.x * a.nsub + h) * a.warps + wl;
-      const int t1 = a.null_work ? wp[0] : wp[1];
-      for (int ti = wp[0]; ti < t1; ++ti) {
-        const SweepTask tk = a.sbtask[ti];
-        backward_task<true, PROF>(a, tk, F, x, sv, w, mbar);
-      }
+    for (int h = a.nsub - 1; h >= 0; --h, ++L) {
+      const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
+      for (int ti = w.bnd[L]; ti < t1; ++ti) backward_task<true, PROF>(a, w.tl[ti], F, x, sv, w, mbar);
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
     }
     if (a.nsub && k + 1 < a.nslab) {  // x_k visible to every CTA's next coupling
@@ -1023,22 +1015,17 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
                                                                                     nrhs, rhsp);
   STMHD_LAUNCH_CHECK();
   SweepArgs a{};
-  a.ftask = sp.fwd_tasks.as<SweepTask>();
-  a.btask = sp.bwd_tasks.as<SweepTask>();
-  a.fwptr = sp.fwd_wptr.as<int>();
-  a.bwptr = sp.bwd_wptr.as<int>();
-  a.sftask = sp.sf_tasks.as<SweepTask>();
-  a.sbtask = sp.sb_tasks.as<SweepTask>();
-  a.sfwptr = sp.sf_wptr.as<int>();
-  a.sbwptr = sp.sb_wptr.as<int>();
+  a.wl_tasks = sp.wl_tasks.as<SweepTask>();
+  a.wl_off = sp.wl_off.as<int>();
+  a.wl_bnd = sp.wl_bnd.as<int>();
+  a.nl = sp.nl;
+  a.tstride = ((sp.nl + 1 + 3) / 4) * 16 + sp.max_wtasks * (int)sizeof(SweepTask);
   a.sub_info = sp.sub_info.as<int64_t>();
   a.ntop = sp.ntop;
   a.nsub = sp.nsub;
   a.warps = warps;
   a.sub_len = sp.sub_len;
   a.sub_cb = sp.sub_cb;
-  a.pf_ptr = sp.pf_ptr.as<int>();
-  a.pf_items = sp.pf_items.as<longlong2>();
   a.g3p = sp.g3p.as<int4>();
   a.bpos = sp.bpos.as<int>();
   a.nlevels = p.nlevels;
@@ -1101,11 +1088,10 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   }
   a.slot = slot;
   a.vstride = vstride;
-  static const int prefetch = env_int2("STMHD_SWEEP_PREFETCH", 8);  // L2 prefetch distance (chunks)
-  a.prefetch = prefetch;
   a.null_work = env_int2("STMHD_SWEEP_NULL", 0);
   const int threads = warps * 32;
-  const size_t smem = ((size_t)warps * a.vstride + 3 * a.sub_len + a.sub_cb) * sizeof(double);
+  const size_t smem =
+      ((size_t)warps * a.vstride + 3 * a.sub_len + a.sub_cb + 1) * sizeof(double) + (size_t)warps * a.tstride;
   require(smem <= 224 * 1024, "nd sweep: subtree vectors or fronts too large for shared memory");
   static bool attr = false;
   if (!attr) {
