@@ -45,26 +45,69 @@ inline void require(bool cond, const std::string &msg) {
 }
 
 // Owning device allocation.
+// Device buffer.  alloc() uses cudaMalloc; alloc_async() takes the block from the
+// device's default stream-ordered pool (kept, not returned to the driver), which is
+// what the per-Newton-step preconditioner storage uses: a new preconditioner reuses
+// the blocks of the previous one without cudaMalloc/cudaFree round trips.
+inline void ensure_pool_retained() {
+  static bool done = false;
+  if (!done) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done = true;
+  }
+}
+
 struct DevBuf {
   void *ptr = nullptr;
   size_t bytes = 0;
+  cudaStream_t stream = nullptr;  // pooled buffers: freed in order on this stream
+  bool pooled = false;
   DevBuf() = default;
   explicit DevBuf(size_t b) { alloc(b); }
   DevBuf(const DevBuf &) = delete;
   DevBuf &operator=(const DevBuf &) = delete;
-  DevBuf(DevBuf &&o) noexcept : ptr(o.ptr), bytes(o.bytes) { o.ptr = nullptr; o.bytes = 0; }
+  DevBuf(DevBuf &&o) noexcept : ptr(o.ptr), bytes(o.bytes), stream(o.stream), pooled(o.pooled) {
+    o.ptr = nullptr;
+    o.bytes = 0;
+  }
   DevBuf &operator=(DevBuf &&o) noexcept {
-    if (this != &o) { release(); ptr = o.ptr; bytes = o.bytes; o.ptr = nullptr; o.bytes = 0; }
+    if (this != &o) {
+      release();
+      ptr = o.ptr;
+      bytes = o.bytes;
+      stream = o.stream;
+      pooled = o.pooled;
+      o.ptr = nullptr;
+      o.bytes = 0;
+    }
     return *this;
   }
   ~DevBuf() { release(); }
   void alloc(size_t b) {
     release();
     bytes = b;
+    pooled = false;
     if (b) STMHD_CUDA_CHECK(cudaMalloc(&ptr, b));
   }
+  void alloc_async(size_t b, cudaStream_t s) {
+    release();
+    ensure_pool_retained();
+    bytes = b;
+    stream = s;
+    pooled = true;
+    if (b) STMHD_CUDA_CHECK(cudaMallocAsync(&ptr, b, s));
+  }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr) {
+      if (pooled) cudaFreeAsync(ptr, stream);
+      else cudaFree(ptr);
+    }
     ptr = nullptr;
     bytes = 0;
   }

@@ -383,14 +383,16 @@ void NDDevice::build(const NDPlan &p, cudaStream_t s) {
 
 void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s) {
   const NDPlan &p = *dev->plan;
-  factors.alloc((size_t)nbatch * p.factor_size * sizeof(double));
+  if (factors.bytes != (size_t)nbatch * p.factor_size * sizeof(double))
+    factors.alloc_async((size_t)nbatch * p.factor_size * sizeof(double), s);
   if (!status.ptr) status.alloc(sizeof(int));
   STMHD_CUDA_CHECK(cudaMemsetAsync(status.ptr, 0, sizeof(int), s));
   // chunk the batch so front workspace + staging stay below ~3 GiB
   int64_t per = (std::max<int64_t>(p.front_size, 1) + p.stage_size) * (int64_t)sizeof(double);
   int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t(3) << 30) / per));
-  DevBuf fronts((size_t)chunk * std::max<int64_t>(p.front_size, 1) * sizeof(double));
-  DevBuf stage((size_t)chunk * std::max<int64_t>(p.stage_size, 1) * sizeof(double));
+  DevBuf fronts, stage;  // stream-ordered pool: reused by the next factorisation
+  fronts.alloc_async((size_t)chunk * std::max<int64_t>(p.front_size, 1) * sizeof(double), s);
+  stage.alloc_async((size_t)chunk * std::max<int64_t>(p.stage_size, 1) * sizeof(double), s);
   size_t smem = (2 * GT * GK) * sizeof(double) + (size_t)(p.max_front + 1) * sizeof(int);
   static bool attr_set = false;
   if (smem > 48 * 1024 || !attr_set) {

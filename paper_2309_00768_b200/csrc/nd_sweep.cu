@@ -66,25 +66,42 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
     }
   }
 
-  // ---- split the tree: subtrees rooted at depth D (one per CTA) + the top ----
-  std::vector<int> depth(p.nsn, 0);
-  for (int sn = p.nsn - 1; sn >= 0; --sn)  // postorder reversed: parents first
-    if (p.parent[sn] >= 0) depth[sn] = depth[p.parent[sn]] + 1;
-  int maxd = 0;
-  for (int sn = 0; sn < p.nsn; ++sn) maxd = std::max(maxd, depth[sn]);
-  int D = 0;
-  for (int d = 1; d <= maxd; ++d) {
-    int cnt = 0;
-    for (int sn = 0; sn < p.nsn; ++sn) cnt += depth[sn] == d;
-    if (cnt <= ncta) D = d;
+  // ---- split the tree: a frontier of <= ncta subtrees (one per CTA) + the top ----
+  // Greedy: start from the tree roots and keep splitting the frontier node with the
+  // most subtree work (factor doubles) while the frontier still fits the CTAs, so
+  // the subtrees are balanced even when the tree is not.
+  std::vector<double> swork(p.nsn, 0.0);
+  for (int sn = 0; sn < p.nsn; ++sn) {  // postorder: children first
+    swork[sn] += 2.0 * (double)(p.ns[sn] + p.nb[sn]) * p.ns[sn] + 64.0;
+    if (p.parent[sn] >= 0) swork[p.parent[sn]] += swork[sn];
   }
   static const int sub_env = [] {
     const char *e = getenv("STMHD_SWEEP_SUBTREES");
     return e ? atoi(e) : 1;
   }();
-  if (!sub_env || flat) D = 0;
-  // subtree membership: owner CTA of every supernode at depth >= D (D > 0); falls
-  // back to an all-top schedule when the subtree vectors exceed shared memory
+  int D = (sub_env && !flat) ? 1 : 0;  // 1: subtree phase in use
+  std::vector<int> frontier;
+  if (D) {
+    for (int sn = 0; sn < p.nsn; ++sn)
+      if (p.parent[sn] < 0) frontier.push_back(sn);
+    for (;;) {
+      int best = -1;
+      for (int i = 0; i < (int)frontier.size(); ++i) {
+        const int sn = frontier[i];
+        const int nc = p.child_ptr[sn + 1] - p.child_ptr[sn];
+        if (nc == 0 || (int)frontier.size() - 1 + nc > ncta) continue;
+        if (best < 0 || swork[sn] > swork[frontier[best]]) best = i;
+      }
+      if (best < 0) break;
+      const int sn = frontier[best];
+      frontier.erase(frontier.begin() + best);
+      for (int ci = p.child_ptr[sn]; ci < p.child_ptr[sn + 1]; ++ci) frontier.push_back(p.child_list[ci]);
+    }
+    if ((int)frontier.size() > ncta || frontier.size() <= 1) D = 0;
+    std::sort(frontier.begin(), frontier.end());
+  }
+  // subtree membership (owner CTA; -1 = top); falls back to an all-top schedule
+  // when the subtree vectors exceed shared memory
   std::vector<int> owner, roots;
   std::vector<int64_t> info;
   int64_t maxlen = 0, maxcb = 0;
@@ -94,11 +111,10 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
     info.assign(4 * (size_t)ncta, 0);
     maxlen = maxcb = 0;
     if (D > 0) {
-      for (int sn = 0; sn < p.nsn; ++sn)
-        if (depth[sn] == D) roots.push_back(sn);
+      roots = frontier;
       for (int r = 0; r < (int)roots.size(); ++r) owner[roots[r]] = r;
-      for (int sn = p.nsn - 1; sn >= 0; --sn)
-        if (depth[sn] > D) owner[sn] = owner[p.parent[sn]];
+      for (int sn = p.nsn - 1; sn >= 0; --sn)  // parents first
+        if (owner[sn] < 0 && p.parent[sn] >= 0 && owner[p.parent[sn]] >= 0) owner[sn] = owner[p.parent[sn]];
     }
     // per-CTA subtree ranges (a subtree is contiguous in postorder/elimination order)
     std::vector<int64_t> lo(roots.size(), INT64_MAX), hi(roots.size(), 0), cblo(roots.size(), INT64_MAX),
@@ -191,13 +207,24 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
     }
   };
   // top part: levels (heights) that contain top supernodes, ascending
-  std::vector<int> top_levels;
-  for (int l = 0; l < p.nlevels; ++l) {
-    bool any = false;
-    for (int sn : p.level_sn[l]) any |= owner[sn] < 0;
-    if (any) top_levels.push_back(l);
+  // top nodes scheduled by their height within the top tree (frontier subtrees
+  // are complete before the top phase starts)
+  std::vector<int> th(p.nsn, -1);
+  int ntop = 0;
+  for (int sn = 0; sn < p.nsn; ++sn) {  // postorder: children first
+    if (owner[sn] >= 0) continue;
+    int h = 0;
+    for (int ci = p.child_ptr[sn]; ci < p.child_ptr[sn + 1]; ++ci) {
+      const int c = p.child_list[ci];
+      if (owner[c] < 0) h = std::max(h, th[c] + 1);
+    }
+    th[sn] = h;
+    ntop = std::max(ntop, h + 1);
   }
-  sp->ntop = (int)top_levels.size();
+  std::vector<std::vector<int>> top_sn(ntop);
+  for (int sn = 0; sn < p.nsn; ++sn)
+    if (owner[sn] < 0) top_sn[th[sn]].push_back(sn);
+  sp->ntop = ntop;
   int nsub = 0;
   for (int r = 0; r < (int)roots.size(); ++r) nsub = std::max(nsub, p.level[roots[r]] + 1);
   sp->nsub = roots.empty() ? 0 : nsub;
@@ -214,9 +241,9 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
     for (int t = 0; t < sp->ntop; ++t) {
       std::vector<SN> sns;
       std::vector<char> cbg;
-      for (int sn : p.level_sn[top_levels[t]]) {
+      for (int sn : top_sn[t]) {
         SN x;
-        if (owner[sn] < 0 && make_sn(sn, fwd, x)) {
+        if (make_sn(sn, fwd, x)) {
           sns.push_back(x);
           cbg.push_back(1);
         }
@@ -269,6 +296,17 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
     off.push_back((int)all.size());
     if (all.empty()) all.push_back(SweepTask{});
     sp->max_wtasks = maxw;
+    if (getenv("STMHD_SWEEP_TRACE")) {
+      std::vector<int64_t> fsum(ncta, 0), nbsum(ncta, 0);
+      for (int sn = 0; sn < p.nsn; ++sn)
+        if (owner[sn] >= 0) {
+          fsum[owner[sn]] += p.ns[sn] + p.nb[sn];
+          nbsum[owner[sn]] += p.nb[sn];
+        }
+      fprintf(stderr, "[sweep-plan] n=%lld D=%d ntop=%d nsub=%d max_wtasks=%d max sub front entries %lld (nb %lld)\n",
+              (long long)p.n, D, sp->ntop, sp->nsub, maxw, (long long)*std::max_element(fsum.begin(), fsum.end()),
+              (long long)*std::max_element(nbsum.begin(), nbsum.end()));
+    }
     // shared memory: subtree vectors + per-warp task lists must fit next to the
     // per-warp gather buffers; otherwise fall back to an all-top schedule
     const int64_t tdoubles = (int64_t)warps * (((sp->nl + 1 + 3) / 4) * 16 + (int64_t)maxw * 32) / 8;
@@ -652,49 +690,91 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
       // permuted rhs, which precedes xp in scratch, and carry value 0)
       const double *x1 = a.xp + (int64_t)(k - 1) * n;
       const int nth = blockDim.x;
-      for (int i0 = threadIdx.x; i0 < hd.y; i0 += 2 * nth) {
-        const int it[2] = {i0, i0 + nth};
-        const bool live[2] = {true, i0 + nth < hd.y};
-        double acc[2];
-        int2 io[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          io[r] = live[r] ? a.prog_items[hd.x + it[r]] : make_int2(0, -1);
-          acc[r] = io[r].y >= 0 ? rhs[io[r].y] : 0.0;
-        }
-        if (k >= 1) {
-          for (int s0 = 0; s0 < hd.w; s0 += 8) {
-            int cc[2][8];
-            double vv[2][8];
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const int64_t id = hd.z + (int64_t)(s0 + q) * hd.y + it[r];
-                const bool ok = live[r] && s0 + q < hd.w;
-                cc[r][q] = ok ? __ldg(a.prog_ecol + id) : 0;
-                vv[r][q] = ok ? __ldg(vk + id) : 0.0;
-              }
-            double xv[2][8];  // all 16 loads in flight together
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const bool sm = cc[r][q] >= (1 << 30);
-                xv[r][q] = *((sm ? (const double *)sv.xs : x1) + (sm ? cc[r][q] - (1 << 30) : cc[r][q]));
-              }
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-              for (int q = 0; q < 8; ++q) acc[r] = fma(vv[r][q], xv[r][q], acc[r]);
+      // threads per item: spread an item's entries over tpi lanes when there are few
+      // items (so every load of the step is in flight at once)
+      int tpi = 1;
+      while (tpi < 32 && hd.y * tpi * 2 <= nth) tpi *= 2;
+      if (tpi == 1) {
+      const int nth = blockDim.x;
+        for (int i0 = threadIdx.x; i0 < hd.y; i0 += 2 * nth) {
+          const int it[2] = {i0, i0 + nth};
+          const bool live[2] = {true, i0 + nth < hd.y};
+          double acc[2];
+          int2 io[2];
+  #pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            io[r] = live[r] ? a.prog_items[hd.x + it[r]] : make_int2(0, -1);
+            acc[r] = io[r].y >= 0 ? rhs[io[r].y] : 0.0;
+          }
+          if (k >= 1) {
+            for (int s0 = 0; s0 < hd.w; s0 += 8) {
+              int cc[2][8];
+              double vv[2][8];
+  #pragma unroll
+              for (int r = 0; r < 2; ++r)
+  #pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                  const int64_t id = hd.z + (int64_t)(s0 + q) * hd.y + it[r];
+                  const bool ok = live[r] && s0 + q < hd.w;
+                  cc[r][q] = ok ? __ldg(a.prog_ecol + id) : 0;
+                  vv[r][q] = ok ? __ldg(vk + id) : 0.0;
+                }
+              double xv[2][8];  // all 16 loads in flight together
+  #pragma unroll
+              for (int r = 0; r < 2; ++r)
+  #pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                  const bool sm = cc[r][q] >= (1 << 30);
+                  xv[r][q] = *((sm ? (const double *)sv.xs : x1) + (sm ? cc[r][q] - (1 << 30) : cc[r][q]));
+                }
+  #pragma unroll
+              for (int r = 0; r < 2; ++r)
+  #pragma unroll
+                for (int q = 0; q < 8; ++q) acc[r] = fma(vv[r][q], xv[r][q], acc[r]);
+            }
+          }
+  #pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            if (!live[r]) continue;
+            const int kind = io[r].x >> 29, di = io[r].x & ((1 << 29) - 1);
+            if (kind == 0) sv.rhs_s[di] = acc[r];
+            else a.tbuf[di] = acc[r];
           }
         }
+      } else {
+        const int g = threadIdx.x / tpi, part = threadIdx.x & (tpi - 1), ng = nth / tpi;
+        for (int base = 0; base < hd.y; base += ng) {  // uniform trip count per warp
+          const int it = base + g;
+          const bool live = it < hd.y;
+          const int2 io = live ? a.prog_items[hd.x + it] : make_int2(0, -1);
+          double acc = 0.0;
+          if (k >= 1)
+            for (int s0 = part; s0 < hd.w; s0 += 16 * tpi) {
+              int cc[16];
+              double vv[16], xv[16];
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          if (!live[r]) continue;
-          const int kind = io[r].x >> 29, di = io[r].x & ((1 << 29) - 1);
-          if (kind == 0) sv.rhs_s[di] = acc[r];
-          else a.tbuf[di] = acc[r];
+              for (int q = 0; q < 16; ++q) {
+                const int sl = s0 + q * tpi;
+                const bool ok = live && sl < hd.w;
+                const int64_t id = hd.z + (int64_t)sl * hd.y + it;
+                cc[q] = ok ? __ldg(a.prog_ecol + id) : 0;
+                vv[q] = ok ? __ldg(vk + id) : 0.0;
+              }
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                const bool sm = cc[q] >= (1 << 30);
+                xv[q] = *((sm ? (const double *)sv.xs : x1) + (sm ? cc[q] - (1 << 30) : cc[q]));
+              }
+#pragma unroll
+              for (int q = 0; q < 16; ++q) acc = fma(vv[q], xv[q], acc);
+            }
+          for (int o = 1; o < tpi; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          if (live && part == 0) {
+            acc += io.y >= 0 ? rhs[io.y] : 0.0;
+            const int kind = io.x >> 29, di = io.x & ((1 << 29) - 1);
+            if (kind == 0) sv.rhs_s[di] = acc;
+            else a.tbuf[di] = acc;
+          }
         }
       }
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;

@@ -77,33 +77,33 @@ PC::PC(stmhd_disc_s *dd, cudaStream_t s, const double *js_, const double *fp_, c
   nnz_fp = d->I("nnz_fp");
   nnz_ca = d->H("ca_col").count;
   nnz_s1 = d->H("s1_col").count;
-  alf.alloc(nt * sizeof(double));
+  alf.alloc_async(nt * sizeof(double), s);
   STMHD_CUDA_CHECK(cudaMemcpyAsync(alf.ptr, alf_, nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
   // C_A and sub1 values (precond.py:91-105)
-  ca_vals.alloc((size_t)nt * nnz_ca * sizeof(double));
+  ca_vals.alloc_async((size_t)nt * nnz_ca * sizeof(double), s);
   ca_values_kernel<<<dim3(cdiv(nnz_ca, 256), std::min(nt, 16)), 256, 0, s>>>(
       (int)nnz_ca, nt, d->D<int>("ca_pptr"), d->D<int>("ca_a"), d->D<int>("ca_b"), d->D<double>("ca_w"),
       d->D<double>("ca_k"), js, nnz_js, alf.as<double>(), ca_vals.as<double>());
   STMHD_LAUNCH_CHECK();
   if (nt > 1) {
-    s1_vals.alloc((size_t)(nt - 1) * nnz_s1 * sizeof(double));
+    s1_vals.alloc_async((size_t)(nt - 1) * nnz_s1 * sizeof(double), s);
     s1_values_kernel<<<dim3(cdiv(nnz_s1, 256), std::min(nt - 1, 16)), 256, 0, s>>>(
         (int)nnz_s1, nt - 1, d->D<int>("s1_pptr"), d->D<double>("s1_coef"), d->D<int>("s1_idx"),
         d->D<int>("s1_which"), js, nnz_js, s1_vals.as<double>());
     STMHD_LAUNCH_CHECK();
   } else {
-    s1_vals.alloc(sizeof(double));
+    s1_vals.alloc_async(sizeof(double), s);
   }
   // workspaces
-  tu1.alloc((size_t)nt * n_u * sizeof(double));
-  tu2.alloc((size_t)nt * n_u * sizeof(double));
-  ta1.alloc((size_t)nt * n_a * sizeof(double));
-  ta2.alloc((size_t)nt * n_a * sizeof(double));
-  ta3.alloc((size_t)nt * n_a * sizeof(double));
-  tp1.alloc((size_t)nt * n_p * sizeof(double));
-  tp2.alloc((size_t)nt * n_p * sizeof(double));
-  tp3.alloc((size_t)nt * n_p * sizeof(double));
-  tj.alloc((size_t)nt * n_j * sizeof(double));
+  tu1.alloc_async((size_t)nt * n_u * sizeof(double), s);
+  tu2.alloc_async((size_t)nt * n_u * sizeof(double), s);
+  ta1.alloc_async((size_t)nt * n_a * sizeof(double), s);
+  ta2.alloc_async((size_t)nt * n_a * sizeof(double), s);
+  ta3.alloc_async((size_t)nt * n_a * sizeof(double), s);
+  tp1.alloc_async((size_t)nt * n_p * sizeof(double), s);
+  tp2.alloc_async((size_t)nt * n_p * sizeof(double), s);
+  tp3.alloc_async((size_t)nt * n_p * sizeof(double), s);
+  tj.alloc_async((size_t)nt * n_j * sizeof(double), s);
   // factorisations (precond.py:75, 96)
   fu = std::make_unique<NDFactor>();
   fu->dev = d->dev_fu.get();
