@@ -84,7 +84,7 @@ struct CplProgram {
   int64_t nent = 0;      // entries (all CTAs)
   DevBuf hdr;            // int4 per CTA {item_off, nitems, ent_off, width}
   DevBuf items;          // int2 per item {dst (kind << 29 | index), rhs row or -1}
-  DevBuf ecol;           // int per entry, [slot][item] per CTA: col | 1<<28 smem | 1<<29 lag 2; -1 pad
+  DevBuf ecol;           // int per entry, [slot][item] per CTA: source id << 28 | index (pad: 0 with value 0)
   DevBuf esrc;           // int2 per entry {coupling, value index} ({-1, 0} pad)
 };
 
@@ -104,14 +104,10 @@ struct NDSweepPlan {
   DevBuf bpos;  // int per front position: permuted position of the front entry
   DevBuf pos;   // n: elimination position of each original index
   DevBuf iperm; // n: original index at each elimination position
-  // permuted column indices of coupling matrices, keyed by their column array
-  // (owned by the same discretisation as this plan, so lifetimes match)
-  // {rowptr, colp, eidx} of a coupling matrix in elimination order
-  mutable std::map<const int *, std::unique_ptr<std::vector<DevBuf>>> colp_cache;
-  std::vector<int64_t> sub_info_h;  // host copy of sub_info
+    std::vector<int64_t> sub_info_h;  // host copy of sub_info
   std::vector<int> pos_h, iperm_h;  // host copies of pos / iperm
-  // fused slab-coupling programs (nd_sweep.cu), keyed by the coupling column arrays
-  mutable std::map<std::pair<const int *, const int *>, std::unique_ptr<struct CplProgram>> prog_cache;
+  // fused slab-coupling programs (nd_sweep.cu), keyed by the coupling index arrays
+  mutable std::map<std::vector<const void *>, std::unique_ptr<struct CplProgram>> prog_cache;
 };
 
 // Device-resident copy of a plan plus the solve schedules.
@@ -131,14 +127,20 @@ struct NDDevice {
 };
 
 // A coupling term of a sequential block sweep:
-//   rhs_k += coef * C_(k) x_(k-lag)   (C in CSR with per-slab value stride)
+//   rhs_k += coef * C_(k) x_(k-lag)          (lag 1 or 2: the sweep's own output)
+//   rhs_k += coef * C_(k) e_(k)              (ext >= 0: another stage's output)
+// C is CSR-like: row i holds entries [rowptr[i], rowend ? rowend[i] : rowptr[i+1])
+// with columns col[e] - col_off and values val[(k - val_shift) * val_stride + e].
 struct SweepCoupling {
   const int32_t *rowptr = nullptr;
+  const int32_t *rowend = nullptr;
   const int32_t *col = nullptr;
+  int col_off = 0;
   const double *val = nullptr;
   int64_t val_stride = 0;  // 0: shared matrix
   int64_t val_shift = 0;   // value block used for slab k is (k - val_shift)
-  int lag = 0;             // 0 = unused
+  int lag = 0;             // 1 or 2 (own output); 0 with ext >= 0
+  int ext = -1;            // external source stage (sweep_stages_launch), lag 0
   double coef = 0.0;
 };
 
@@ -198,6 +200,22 @@ __device__ __forceinline__ double chunk_gemv(const double *__restrict__ blk, int
   return out;
 }
 #endif
+
+// A prepared sweep (one cluster of a pipelined launch), nd_sweep.cu.
+struct SweepStage;
+struct SweepStageDeleter {
+  void operator()(SweepStage *) const;
+};
+using SweepStagePtr = std::unique_ptr<SweepStage, SweepStageDeleter>;
+SweepStagePtr sweep_stage_new();
+// Permute the stage's right-hand sides in and bind its couplings; ext[e] are stages
+// prepared before whose (permuted) output feeds the couplings with ext = e.
+void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
+                         int64_t ld_x, int nrhs, const SweepCoupling *cpl, int ncpl, SweepStage *const *ext,
+                         int next, cudaStream_t s);
+// Run prepared stages in ONE launch, one 16-CTA cluster each, pipelined slab by slab
+// (a consumer waits on per-slab release flags of its producers); then permute out.
+void sweep_stages_launch(SweepStage *const *st, int nst, cudaStream_t s);
 
 // Cluster-resident sweep in nested-dissection order (nd_sweep.cu).
 void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,

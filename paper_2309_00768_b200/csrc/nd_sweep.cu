@@ -328,16 +328,6 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
   return *sweep_plan;
 }
 
-struct SweepCpl {
-  int width;        // ELL width (max entries per row)
-  const int *colp;  // [j*n + q]: permuted column of slot j of permuted row q (-1: pad)
-  const int *eidx;  // original entry index of that slot (value lookup)
-  const double *val;
-  int64_t val_stride, val_shift;
-  int lag;
-  double coef;
-};
-
 struct SweepArgs {
   // per physical warp task lists (NDSweepPlan::wl_*), copied to shared memory
   const SweepTask *wl_tasks;
@@ -362,10 +352,16 @@ struct SweepArgs {
   int64_t fstride;
   const double *rhsp;  // nslab x n (permuted)
   double *xp;          // nslab x n (permuted)
-  double *reff, *ybuf, *cbv;
-  int nslab;
-  SweepCpl cpl[2];
-  int ncpl;
+  double *ybuf, *cbv;
+  const double *zero;  // n zeros (sources that do not exist yet read from here)
+  int nslab, ncta;
+  // pipelined launch: external sources (other stages' permuted outputs) and flags
+  const double *ext_xp[2];
+  int64_t ext_n[2];
+  const int *flag_in[2];  // per producer: [slab][cta] = epoch once slab written
+  int nwait;
+  int *flag_out;          // this stage's flags (null: not consumed)
+  int epoch;
   int vstride;  // doubles per warp: gather buffer + 2 TMA slots
   int slot;     // doubles per TMA slot (largest chunk block)
   int null_work;  // diagnostics: skip all task work (barrier/loop floor)
@@ -378,8 +374,30 @@ __device__ __forceinline__ void sweep_barrier() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ unsigned cluster_index() {
+  unsigned r;
+  asm("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(int *p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void sweep_trace(const SweepArgs &a, int &step) {
-  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (a.trace && threadIdx.x == 0 && cluster_rank() == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[step] = t;
@@ -621,15 +639,31 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
   __syncwarp();
 }
 
+// Up to three sweeps of one pipelined launch, one cluster each (cluster i runs st[i]).
+struct SweepMulti {
+  SweepArgs st[3];
+};
+
 template <bool PROF>
-__global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
+__global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant__ SweepMulti m) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long mbar[16][2];
+  __shared__ SweepArgs sa;
+  __shared__ const double *s_src[8];  // coupling sources of the current slab (by source id)
+  const unsigned cid = cluster_index();
+  const int crank = (int)cluster_rank();
+  if (threadIdx.x == 0) {
+    if (cid == 0) sa = m.st[0];
+    else if (cid == 1) sa = m.st[1];
+    else sa = m.st[2];
+  }
+  __syncthreads();
+  const SweepArgs &a = sa;
   WarpCtx w;
   w.lane = threadIdx.x & 31;
   w.wl = threadIdx.x >> 5;
   const int lane = w.lane, wl = w.wl;
-  const int gw = wl * gridDim.x + blockIdx.x;  // interleaved across CTAs (top phases)
+  const int gw = wl * a.ncta + crank;  // interleaved across CTAs (top phases)
   w.v = sm + wl * a.vstride;
   w.slot0 = w.v + (a.vstride - 2 * a.slot);
   w.slotsz = a.slot;
@@ -641,13 +675,13 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
   sv.xs = sv.ys + a.sub_len;
   sv.cbs = sv.xs + a.sub_len;
   sv.rhs_s = sv.cbs + a.sub_cb;
-  sv.first = a.sub_info[4 * blockIdx.x + 0];
-  sv.len = a.sub_info[4 * blockIdx.x + 1];
-  sv.cbfirst = a.sub_info[4 * blockIdx.x + 2];
+  sv.first = a.sub_info[4 * crank + 0];
+  sv.len = a.sub_info[4 * crank + 1];
+  sv.cbfirst = a.sub_info[4 * crank + 2];
   {
     // copy this warp's task list and level bounds into shared memory (static for
     // the whole sweep: no global round trip per level or task afterwards)
-    const int gid = blockIdx.x * a.warps + wl;
+    const int gid = crank * a.warps + wl;
     const uintptr_t base = (reinterpret_cast<uintptr_t>(sv.rhs_s + a.sub_len) + 15) & ~(uintptr_t)15;
     char *area = reinterpret_cast<char *>(base) + (size_t)wl * a.tstride;
     int *bnd = reinterpret_cast<int *>(area);
@@ -681,59 +715,72 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
     const double *rhs = a.rhsp + (int64_t)k * n;
     double *x = a.xp + (int64_t)k * n;
     if (a.prog_hdr && !a.null_work) {
-      // fused coupling (CTA-local): rhs_k + sum_c coef_c C_c x_{k-lag_c} for this CTA's
-      // items, two items per thread with all their loads in flight together; x_{k-1}
-      // of the CTA's own subtree is read from shared memory (xs)
-      const int4 hd = a.prog_hdr[blockIdx.x];
+      // fused coupling (CTA-local): rhs_k + sum_c coef_c C_c src_c for this CTA's items.
+      // Sources by id: 0 x_{k-1}, 1 x_{k-1} of the own subtree (shared memory),
+      // 2 x_{k-2}, 3/4 external stages' outputs at slab k; sources that do not exist
+      // yet read zeros.
+      if (threadIdx.x == 0) {
+        s_src[0] = k >= 1 ? a.xp + (int64_t)(k - 1) * n : a.zero;
+        s_src[1] = k >= 1 ? (const double *)sv.xs : a.zero;
+        s_src[2] = k >= 2 ? a.xp + (int64_t)(k - 2) * n : a.zero;
+        s_src[3] = a.ext_xp[0] ? a.ext_xp[0] + (int64_t)k * a.ext_n[0] : a.zero;
+        s_src[4] = a.ext_xp[1] ? a.ext_xp[1] + (int64_t)k * a.ext_n[1] : a.zero;
+        s_src[5] = s_src[6] = s_src[7] = a.zero;
+      }
+      // pipelined launch: wait until every CTA of each producer has published slab k
+      if ((int)threadIdx.x < a.nwait * a.ncta) {
+        const int e = threadIdx.x / a.ncta, c = threadIdx.x % a.ncta;
+        const int *f = a.flag_in[e] + (int64_t)k * a.ncta + c;
+        unsigned long long t0, t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while (ld_acquire_gpu(f) != a.epoch) {
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          if (t1 - t0 > 4000000000ull) __trap();  // 4 s: a producer is not running
+        }
+      }
+      __syncthreads();
+      const int4 hd = a.prog_hdr[crank];
       const double *vk = a.prog_vals + (a.prog_per_slab ? (int64_t)k * a.prog_nent : 0);
-      // x_{k-1} (lag-2 entries are offset by -n; at k = 1 they point into the
-      // permuted rhs, which precedes xp in scratch, and carry value 0)
-      const double *x1 = a.xp + (int64_t)(k - 1) * n;
       const int nth = blockDim.x;
+      constexpr int kIdx = (1 << 28) - 1;
       // threads per item: spread an item's entries over tpi lanes when there are few
       // items (so every load of the step is in flight at once)
       int tpi = 1;
       while (tpi < 32 && hd.y * tpi * 2 <= nth) tpi *= 2;
       if (tpi == 1) {
-      const int nth = blockDim.x;
         for (int i0 = threadIdx.x; i0 < hd.y; i0 += 2 * nth) {
           const int it[2] = {i0, i0 + nth};
           const bool live[2] = {true, i0 + nth < hd.y};
           double acc[2];
           int2 io[2];
-  #pragma unroll
+#pragma unroll
           for (int r = 0; r < 2; ++r) {
             io[r] = live[r] ? a.prog_items[hd.x + it[r]] : make_int2(0, -1);
             acc[r] = io[r].y >= 0 ? rhs[io[r].y] : 0.0;
           }
-          if (k >= 1) {
-            for (int s0 = 0; s0 < hd.w; s0 += 8) {
-              int cc[2][8];
-              double vv[2][8];
-  #pragma unroll
-              for (int r = 0; r < 2; ++r)
-  #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                  const int64_t id = hd.z + (int64_t)(s0 + q) * hd.y + it[r];
-                  const bool ok = live[r] && s0 + q < hd.w;
-                  cc[r][q] = ok ? __ldg(a.prog_ecol + id) : 0;
-                  vv[r][q] = ok ? __ldg(vk + id) : 0.0;
-                }
-              double xv[2][8];  // all 16 loads in flight together
-  #pragma unroll
-              for (int r = 0; r < 2; ++r)
-  #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                  const bool sm = cc[r][q] >= (1 << 30);
-                  xv[r][q] = *((sm ? (const double *)sv.xs : x1) + (sm ? cc[r][q] - (1 << 30) : cc[r][q]));
-                }
-  #pragma unroll
-              for (int r = 0; r < 2; ++r)
-  #pragma unroll
-                for (int q = 0; q < 8; ++q) acc[r] = fma(vv[r][q], xv[r][q], acc[r]);
-            }
+          for (int s0 = 0; s0 < hd.w; s0 += 8) {
+            int cc[2][8];
+            double vv[2][8];
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const int64_t id = hd.z + (int64_t)(s0 + q) * hd.y + it[r];
+                const bool ok = live[r] && s0 + q < hd.w;
+                cc[r][q] = ok ? __ldg(a.prog_ecol + id) : 0;
+                vv[r][q] = ok ? __ldg(vk + id) : 0.0;
+              }
+            double xv[2][8];  // all 16 loads in flight together
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+              for (int q = 0; q < 8; ++q) xv[r][q] = s_src[cc[r][q] >> 28][cc[r][q] & kIdx];
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+              for (int q = 0; q < 8; ++q) acc[r] = fma(vv[r][q], xv[r][q], acc[r]);
           }
-  #pragma unroll
+#pragma unroll
           for (int r = 0; r < 2; ++r) {
             if (!live[r]) continue;
             const int kind = io[r].x >> 29, di = io[r].x & ((1 << 29) - 1);
@@ -748,26 +795,22 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
           const bool live = it < hd.y;
           const int2 io = live ? a.prog_items[hd.x + it] : make_int2(0, -1);
           double acc = 0.0;
-          if (k >= 1)
-            for (int s0 = part; s0 < hd.w; s0 += 16 * tpi) {
-              int cc[16];
-              double vv[16], xv[16];
+          for (int s0 = part; s0 < hd.w; s0 += 16 * tpi) {
+            int cc[16];
+            double vv[16], xv[16];
 #pragma unroll
-              for (int q = 0; q < 16; ++q) {
-                const int sl = s0 + q * tpi;
-                const bool ok = live && sl < hd.w;
-                const int64_t id = hd.z + (int64_t)sl * hd.y + it;
-                cc[q] = ok ? __ldg(a.prog_ecol + id) : 0;
-                vv[q] = ok ? __ldg(vk + id) : 0.0;
-              }
-#pragma unroll
-              for (int q = 0; q < 16; ++q) {
-                const bool sm = cc[q] >= (1 << 30);
-                xv[q] = *((sm ? (const double *)sv.xs : x1) + (sm ? cc[q] - (1 << 30) : cc[q]));
-              }
-#pragma unroll
-              for (int q = 0; q < 16; ++q) acc = fma(vv[q], xv[q], acc);
+            for (int q = 0; q < 16; ++q) {
+              const int sl = s0 + q * tpi;
+              const bool ok = live && sl < hd.w;
+              const int64_t id = hd.z + (int64_t)sl * hd.y + it;
+              cc[q] = ok ? __ldg(a.prog_ecol + id) : 0;
+              vv[q] = ok ? __ldg(vk + id) : 0.0;
             }
+#pragma unroll
+            for (int q = 0; q < 16; ++q) xv[q] = s_src[cc[q] >> 28][cc[q] & kIdx];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc = fma(vv[q], xv[q], acc);
+          }
           for (int o = 1; o < tpi; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
           if (live && part == 0) {
             acc += io.y >= 0 ? rhs[io.y] : 0.0;
@@ -779,57 +822,6 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
       }
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step);
-    } else if (k > 0 && a.ncpl && !a.null_work) {
-      // rhs_eff = rhs_k + sum_c coef_c C_c x_{k-lag}: permuted rows, up to two rows
-      // per thread processed together (one pass), ELL slots 8 at a time
-      const int64_t nth = (int64_t)a.nw * 32;
-      for (int64_t p0 = (int64_t)gw * 32 + lane; p0 < n; p0 += 2 * nth) {
-        const int64_t prr[2] = {p0, p0 + nth};
-        double acc[2] = {0.0, 0.0};
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          if (c >= a.ncpl) break;
-          const SweepCpl &cp = a.cpl[c];
-          const int kp = k - cp.lag;
-          if (kp < 0) continue;
-          const double *xv = a.xp + (int64_t)kp * n;
-          const double *cv = cp.val + (k - cp.val_shift) * cp.val_stride;
-          double part[2] = {0.0, 0.0};
-          for (int j0 = 0; j0 < cp.width; j0 += 8) {
-            int ci[2][8], ei[2][8];
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const bool ok = j0 + q < cp.width && prr[r] < n;
-                ci[r][q] = ok ? __ldg(cp.colp + (int64_t)(j0 + q) * n + prr[r]) : -1;
-                ei[r][q] = ok ? __ldg(cp.eidx + (int64_t)(j0 + q) * n + prr[r]) : 0;
-              }
-            double cvv[2][8], xvv[2][8];  // unconditional (clamped) loads: all in flight
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const bool ok = ci[r][q] >= 0;
-                cvv[r][q] = cv[ok ? ei[r][q] : 0];
-                xvv[r][q] = xv[ok ? ci[r][q] : 0];
-              }
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-              for (int q = 0; q < 8; ++q)
-                if (ci[r][q] >= 0) part[r] += cvv[r][q] * xvv[r][q];
-          }
-          acc[0] += cp.coef * part[0];
-          acc[1] += cp.coef * part[1];
-        }
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-          if (prr[r] < n) a.reff[prr[r]] = rhs[prr[r]] + acc[r];
-      }
-      tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
-      sweep_trace(a, step);
-      rhs = a.reff;
     }
     const double *F = a.factors + (int64_t)k * a.fstride;
     // phase levels of this warp's list: subtree forward (CTA-local), top forward,
@@ -840,7 +832,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
       for (int ti = w.bnd[L]; ti < t1; ++ti) forward_task<true, PROF>(a, w.tl[ti], F, rhs, sv, w, mbar);
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
     }
-    if (a.nsub) {
+    if (a.nsub || a.prog_hdr) {  // subtree roots' updates and coupled top rows visible
       tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step);
     }
@@ -865,13 +857,18 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(SweepArgs a) {
       for (int ti = w.bnd[L]; ti < t1; ++ti) backward_task<true, PROF>(a, w.tl[ti], F, x, sv, w, mbar);
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
     }
+    if (a.flag_out) {  // pipelined launch: publish this CTA's part of x_k at gpu scope
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) st_release_gpu(a.flag_out + (int64_t)k * a.ncta + crank, a.epoch);
+    }
     if (a.nsub && k + 1 < a.nslab) {  // x_k visible to every CTA's next coupling
       tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step);
     }
   }
   if (PROF && lane == 0)
-    for (int i = 0; i < 8; ++i) a.prof[(blockIdx.x * a.warps + wl) * 8 + i] = (unsigned long long)w.acc[i];
+    for (int i = 0; i < 8; ++i) a.prof[(crank * a.warps + wl) * 8 + i] = (unsigned long long)w.acc[i];
 }
 
 __global__ void permute_in_kernel(const double *rhs, int64_t ld, const int *pos, int64_t n, int nslab,
@@ -888,55 +885,22 @@ __global__ void permute_out_kernel(const double *xp, const int *pos, int64_t n, 
 }
 
 // Coupling matrix as an ELL table in elimination order, cached in the sweep plan.
-static const std::vector<DevBuf> &permuted_ell(const NDSweepPlan &sp, const NDPlan &p, const int *rowptr,
-                                               const int *col, cudaStream_t s, int *width) {
-  auto &cache = sp.colp_cache;
-  auto it = cache.find(col);
-  if (it != cache.end()) {
-    *width = (int)(it->second->at(0).bytes / sizeof(int) / std::max<int64_t>(p.n, 1));
-    return *it->second;
-  }
-  const int64_t n = p.n;
-  std::vector<int> rp(n + 1);
-  STMHD_CUDA_CHECK(cudaMemcpyAsync(rp.data(), rowptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
-  STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-  const int nnz = rp[n];
-  std::vector<int> cl(std::max(nnz, 1));
-  if (nnz) STMHD_CUDA_CHECK(cudaMemcpy(cl.data(), col, nnz * sizeof(int), cudaMemcpyDeviceToHost));
-  std::vector<int> pos(n), iperm(n);
-  for (int sn = 0; sn < p.nsn; ++sn)
-    for (int t = 0; t < p.ns[sn]; ++t) {
-      int i = p.idx[p.idx_off[sn] + t];
-      pos[i] = (int)(p.first[sn] + t);
-      iperm[p.first[sn] + t] = i;
-    }
-  int w = 1;
-  for (int64_t i = 0; i < n; ++i) w = std::max(w, rp[i + 1] - rp[i]);
-  std::vector<int> colp((size_t)w * n, -1), eidx((size_t)w * n, 0);
-  for (int64_t q = 0; q < n; ++q) {
-    int io = iperm[q], j = 0;
-    for (int e = rp[io]; e < rp[io + 1]; ++e, ++j) {
-      colp[(size_t)j * n + q] = pos[cl[e]];
-      eidx[(size_t)j * n + q] = e;
-    }
-  }
-  auto pc = std::make_unique<std::vector<DevBuf>>();
-  pc->push_back(upload_vec(colp, s));
-  pc->push_back(upload_vec(eidx, s));
-  STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-  const std::vector<DevBuf> &r = *pc;
-  cache[col] = std::move(pc);
-  *width = w;
-  return r;
-}
-
-// Build (once per coupling set) the fused slab-coupling program: the coupling rows
-// are split by owner -- subtree rows to their CTA (x_{k-1} of the same subtree read
-// from shared memory, other columns from global memory), top rows balanced over the
-// CTAs (global x).  The end-of-slab cluster barrier makes x_{k-1} visible to all.
+// ---------------------------------------------------------------------------
+// Fused slab-coupling program (built once per coupling set and plan): the coupled
+// right-hand-side rows are split by owner -- subtree rows to their CTA (written to
+// its shared memory; x_{k-1} of the same subtree read from shared memory), top rows
+// balanced over the CTAs (written to tbuf).  Each entry is (source id << 28 | index)
+// with sources 0 x_{k-1}, 1 own-subtree x_{k-1} (shared), 2 x_{k-2}, 3 + e external
+// stage e at slab k; its value is gathered per launch by cpl_vals_kernel.
 static const CplProgram &get_program(const NDSweepPlan &sp, const NDPlan &p, const SweepCoupling *cpl, int ncpl,
-                                     cudaStream_t s) {
-  const auto key = std::make_pair(cpl[0].col, ncpl > 1 ? cpl[1].col : (const int *)nullptr);
+                                     const std::vector<int> *const *ext_pos, cudaStream_t s) {
+  std::vector<const void *> key;
+  for (int c = 0; c < ncpl; ++c) {
+    key.push_back(cpl[c].rowptr);
+    key.push_back(cpl[c].rowend);
+    key.push_back(cpl[c].col);
+    key.push_back(reinterpret_cast<const void *>((intptr_t)(cpl[c].col_off * 16 + cpl[c].lag * 4 + cpl[c].ext + 1)));
+  }
   auto it = sp.prog_cache.find(key);
   if (it != sp.prog_cache.end()) return *it->second;
   auto pg = std::make_unique<CplProgram>();
@@ -953,42 +917,53 @@ static const CplProgram &get_program(const NDSweepPlan &sp, const NDPlan &p, con
     std::vector<Ent> ents;
   };
   std::vector<std::vector<Item>> items(ncta);
-  // coupling rows in permuted order: (j permuted, coupling id, value index)
-  std::vector<std::vector<int>> rp(ncpl), cl(ncpl);
+  // coupling rows on the host: [beg[i], end[i]) and columns
+  std::vector<std::vector<int>> rb(ncpl), re(ncpl), cl(ncpl);
   for (int c = 0; c < ncpl; ++c) {
-    rp[c].resize(n + 1);
-    STMHD_CUDA_CHECK(cudaMemcpyAsync(rp[c].data(), cpl[c].rowptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    rb[c].resize(n + 1);
+    STMHD_CUDA_CHECK(cudaMemcpyAsync(rb[c].data(), cpl[c].rowptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    re[c].resize(n);
+    if (cpl[c].rowend)
+      STMHD_CUDA_CHECK(cudaMemcpyAsync(re[c].data(), cpl[c].rowend, n * sizeof(int), cudaMemcpyDeviceToHost, s));
     STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-    cl[c].resize(std::max(rp[c][n], 1));
-    if (rp[c][n])
-      STMHD_CUDA_CHECK(cudaMemcpy(cl[c].data(), cpl[c].col, rp[c][n] * sizeof(int), cudaMemcpyDeviceToHost));
+    if (!cpl[c].rowend)
+      for (int64_t i = 0; i < n; ++i) re[c][i] = rb[c][i + 1];
+    int mx = 0;
+    for (int64_t i = 0; i < n; ++i) mx = std::max(mx, re[c][i]);
+    cl[c].resize(std::max(mx, 1));
+    if (mx) STMHD_CUDA_CHECK(cudaMemcpy(cl[c].data(), cpl[c].col, mx * sizeof(int), cudaMemcpyDeviceToHost));
   }
-  bool ok = true;
-  std::vector<int64_t> top_rows;
-  for (int64_t q = 0; q < n; ++q)
-    if (owner[q] < 0) top_rows.push_back(q);
-  // entry = signed offset from x_{k-1} (lag 1 -> j, lag 2 -> j - n), or, for lag-1
-  // columns of the CTA's own subtree (still in its shared memory), 2^30 + (j - first)
   auto entries_of = [&](int64_t q, Item &itm, int own) {
     const int io = sp.iperm_h[q];
     for (int c = 0; c < ncpl; ++c)
-      for (int e = rp[c][io]; e < rp[c][io + 1]; ++e) {
-        const int64_t j = sp.pos_h[cl[c][e]];
-        int enc = (int)(j - (int64_t)(cpl[c].lag - 1) * n);
-        if (cpl[c].lag == 1 && own >= 0 && owner[j] == own) enc = (1 << 30) + (int)(j - sp.sub_info_h[4 * own]);
+      for (int e = rb[c][io]; e < re[c][io]; ++e) {
+        const int jr = cl[c][e] - cpl[c].col_off;
+        int enc;
+        if (cpl[c].ext >= 0) {
+          const std::vector<int> &ep = *ext_pos[cpl[c].ext];
+          require(jr >= 0 && jr < (int)ep.size(), "sweep coupling: external column out of range");
+          enc = ((3 + cpl[c].ext) << 28) | ep[jr];
+        } else {
+          require(jr >= 0 && jr < n && (cpl[c].lag == 1 || cpl[c].lag == 2), "sweep coupling: bad column or lag");
+          const int j = sp.pos_h[jr];
+          if (cpl[c].lag == 2) enc = (2 << 28) | j;
+          else if (own >= 0 && owner[j] == own) enc = (1 << 28) | (int)(j - sp.sub_info_h[4 * own]);
+          else enc = j;
+        }
         itm.ents.push_back({enc, c, e});
       }
   };
-  // subtree rows -> their CTA (result into shared memory)
-  for (int64_t q = 0; q < n; ++q) {
+  std::vector<int64_t> top_rows;
+  for (int64_t q = 0; q < n; ++q)
+    if (owner[q] < 0) top_rows.push_back(q);
+  for (int64_t q = 0; q < n; ++q) {  // subtree rows -> their CTA (shared memory)
     const int o = owner[q];
     if (o < 0) continue;
     Item itm{(int)(q - sp.sub_info_h[4 * o]), (int)q, {}};
     entries_of(q, itm, o);
     items[o].push_back(std::move(itm));
   }
-  // top rows -> balanced over the CTAs (result into global tbuf)
-  std::vector<int> load(ncta);
+  std::vector<int> load(ncta);  // top rows -> balanced over the CTAs (tbuf)
   for (int c = 0; c < ncta; ++c) load[c] = (int)items[c].size();
   for (int64_t q : top_rows) {
     const int d = (int)(std::min_element(load.begin(), load.end()) - load.begin());
@@ -997,67 +972,67 @@ static const CplProgram &get_program(const NDSweepPlan &sp, const NDPlan &p, con
     entries_of(q, itm, -1);
     items[d].push_back(std::move(itm));
   }
-  if (ok) {
-    require(n < (1 << 28), "sweep coupling program: index overflow");
-    std::vector<int4> hdr(ncta);
-    std::vector<int2> it2;
-    std::vector<int> ecol;
-    std::vector<int2> esrc;
-    for (int c = 0; c < ncta; ++c) {
-      int width = 0;
-      for (auto &x : items[c]) width = std::max(width, (int)x.ents.size());
-      const int ni = (int)items[c].size();
-      hdr[c] = make_int4((int)it2.size(), ni, (int)ecol.size(), width);
-      for (auto &x : items[c]) it2.push_back(make_int2(x.dst, x.rhs));
-      const size_t base = ecol.size();
-      ecol.resize(base + (size_t)width * ni, 0);  // pad: offset 0 with value 0
-      esrc.resize(base + (size_t)width * ni, make_int2(-1, 0));
-      for (int i = 0; i < ni; ++i)
-        for (int sl = 0; sl < (int)items[c][i].ents.size(); ++sl) {
-          const Ent &en = items[c][i].ents[sl];
-          ecol[base + (size_t)sl * ni + i] = en.col;
-          esrc[base + (size_t)sl * ni + i] = make_int2(en.cid, en.e);
-        }
-    }
-    if (ecol.empty()) {
-      ecol.push_back(0);
-      esrc.push_back(make_int2(-1, 0));
-    }
-    pg->nent = (int64_t)ecol.size();
-    pg->hdr = upload_vec(hdr, s);
-    pg->items = upload_vec(it2, s);
-    pg->ecol = upload_vec(ecol, s);
-    pg->esrc = upload_vec(esrc, s);
-    STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-    if (getenv("STMHD_SWEEP_TRACE")) {
-      fprintf(stderr, "[sweep-prog] ncpl %d top rows %zu nent %lld | per CTA items/width:", ncpl,
-              top_rows.size(), (long long)pg->nent);
-      for (int c = 0; c < ncta; ++c) fprintf(stderr, " %d/%d", hdr[c].y, hdr[c].w);
-      fprintf(stderr, "\n");
-    }
+  require(n < (1 << 28), "sweep coupling program: index overflow");
+  std::vector<int4> hdr(ncta);
+  std::vector<int2> it2;
+  std::vector<int> ecol;
+  std::vector<int2> esrc;
+  for (int c = 0; c < ncta; ++c) {
+    int width = 0;
+    for (auto &x : items[c]) width = std::max(width, (int)x.ents.size());
+    const int ni = (int)items[c].size();
+    hdr[c] = make_int4((int)it2.size(), ni, (int)ecol.size(), width);
+    for (auto &x : items[c]) it2.push_back(make_int2(x.dst, x.rhs));
+    const size_t base = ecol.size();
+    ecol.resize(base + (size_t)width * ni, 0);  // pad: source 0 index 0 with value 0
+    esrc.resize(base + (size_t)width * ni, make_int2(-1, 0));
+    for (int i = 0; i < ni; ++i)
+      for (int sl = 0; sl < (int)items[c][i].ents.size(); ++sl) {
+        const Ent &en = items[c][i].ents[sl];
+        ecol[base + (size_t)sl * ni + i] = en.col;
+        esrc[base + (size_t)sl * ni + i] = make_int2(en.cid, en.e);
+      }
   }
-  pg->ok = ok;
+  if (ecol.empty()) {
+    ecol.push_back(0);
+    esrc.push_back(make_int2(-1, 0));
+  }
+  if (it2.empty()) it2.push_back(make_int2(0, -1));
+  pg->nent = (int64_t)ecol.size();
+  pg->hdr = upload_vec(hdr, s);
+  pg->items = upload_vec(it2, s);
+  pg->ecol = upload_vec(ecol, s);
+  pg->esrc = upload_vec(esrc, s);
+  pg->ok = true;
+  STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (getenv("STMHD_SWEEP_TRACE")) {
+    fprintf(stderr, "[sweep-prog] ncpl %d top rows %zu nent %lld | per CTA items/width:", ncpl, top_rows.size(),
+            (long long)pg->nent);
+    for (int c = 0; c < ncta; ++c) fprintf(stderr, " %d/%d", hdr[c].y, hdr[c].w);
+    fprintf(stderr, "\n");
+  }
   const CplProgram &ref = *pg;
   sp.prog_cache[key] = std::move(pg);
   return ref;
 }
 
+constexpr int kMaxCpl = 4;
+
 struct CplVals {
-  const double *val[2];
-  int64_t stride[2], shift[2];
-  double coef[2];
-  int lag[2];
+  const double *val[kMaxCpl];
+  int64_t stride[kMaxCpl], shift[kMaxCpl];
+  double coef[kMaxCpl];
 };
 
 // vals[b][id] = coef * val_c[(b - shift_c) * stride_c + e] for the program entries
-// (b = slab when any coupling has per-slab values or a lag > 1, else a single
-// block); entries whose lag exceeds the slab are zero (their x is not defined)
+// (b = slab when any coupling has per-slab values, else a single block; blocks before
+// the first one of a coupling are zero -- their source reads zeros anyway)
 __global__ void cpl_vals_kernel(const int2 *esrc, int64_t nent, CplVals cv, int per_slab, double *vals) {
   const int b = blockIdx.y;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < nent; id += (int64_t)gridDim.x * blockDim.x) {
     const int2 sr = esrc[id];
     double v = 0.0;
-    if (sr.x >= 0 && !(per_slab && b < cv.lag[sr.x])) {
+    if (sr.x >= 0) {
       const int64_t blk = per_slab && cv.stride[sr.x] ? (int64_t)b - cv.shift[sr.x] : 0;
       if (blk >= 0) v = cv.coef[sr.x] * cv.val[sr.x][blk * cv.stride[sr.x] + sr.y];
     }
@@ -1065,12 +1040,32 @@ __global__ void cpl_vals_kernel(const int2 *esrc, int64_t nent, CplVals cv, int 
   }
 }
 
-void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,
-              const SweepCoupling *cpl, int ncpl, cudaStream_t s) {
+// ---------------------------------------------------------------------------
+// Stages
+
+struct SweepStage {
+  const NDFactor *fac = nullptr;
+  const NDSweepPlan *sp = nullptr;
+  SweepArgs a{};
+  size_t smem = 0;
+  double *x = nullptr;
+  int64_t ld_x = 0;
+  int nrhs = 0;
+  DevBuf scratch, zero, pvals, flags;
+  int64_t flags_slabs = 0;
+};
+
+void SweepStageDeleter::operator()(SweepStage *p) const { delete p; }
+SweepStagePtr sweep_stage_new() { return SweepStagePtr(new SweepStage()); }
+
+static constexpr int kCluster = 16, kWarps = 16;
+
+void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
+                         int64_t ld_x, int nrhs, const SweepCoupling *cpl, int ncpl, SweepStage *const *ext,
+                         int next, cudaStream_t s) {
   const NDDevice &dev = *fac.dev;
   const NDPlan &p = *dev.plan;
-  static const int cluster = std::max(2, std::min(16, env_int2("STMHD_SWEEP_CLUSTER", 16)));
-  const int warps = 16;
+  const int cluster = kCluster, warps = kWarps;
   // per warp: gather buffer (max front, rounded to 16 doubles) + two TMA slots
   int64_t maxb = 2;
   for (int sn = 0; sn < p.nsn; ++sn) maxb = std::max({maxb, p.bsz_f[sn], p.bsz_b[sn]});
@@ -1079,22 +1074,33 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   const int64_t smem_doubles = 224 * 1024 / 8;
   const NDSweepPlan &sp = dev.get_sweep_plan(cluster, warps, smem_doubles - (int64_t)warps * vstride, s);
   const int64_t n = p.n;
-  static DevBuf scratch;
-  const size_t need = ((size_t)2 * nrhs * n + 3 * n + p.cbv_size + 16) * sizeof(double);
-  if (scratch.bytes < need) {
+  st.fac = &fac;
+  st.sp = &sp;
+  st.x = x;
+  st.ld_x = ld_x;
+  st.nrhs = nrhs;
+  // scratch: rhsp | xp | ybuf | cbv | tbuf; zero: n zeros, never written
+  const size_t need = ((size_t)2 * nrhs * n + 2 * n + p.cbv_size + 16) * sizeof(double);
+  if (st.scratch.bytes < need) {
     STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-    scratch.alloc(need * 5 / 4);
+    st.scratch.alloc(need);
   }
-  double *rhsp = scratch.as<double>();
+  if (st.zero.bytes < (size_t)n * sizeof(double)) {
+    STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
+    st.zero.alloc((size_t)n * sizeof(double));
+    STMHD_CUDA_CHECK(cudaMemsetAsync(st.zero.ptr, 0, st.zero.bytes, s));
+  }
+  double *rhsp = st.scratch.as<double>();
   double *xp = rhsp + (int64_t)nrhs * n;
-  double *reff = xp + (int64_t)nrhs * n;
-  double *ybuf = reff + n;
+  double *zero = st.zero.as<double>();
+  double *ybuf = xp + (int64_t)nrhs * n;
   double *cbv = ybuf + n;
   double *tbuf = cbv + p.cbv_size;
   permute_in_kernel<<<dim3(std::min<int64_t>(cdiv(n, 256), 256), nrhs), 256, 0, s>>>(rhs, ld_rhs, sp.pos.as<int>(), n,
                                                                                     nrhs, rhsp);
   STMHD_LAUNCH_CHECK();
-  SweepArgs a{};
+  SweepArgs &a = st.a;
+  a = SweepArgs{};
   a.wl_tasks = sp.wl_tasks.as<SweepTask>();
   a.wl_off = sp.wl_off.as<int>();
   a.wl_bnd = sp.wl_bnd.as<int>();
@@ -1115,64 +1121,92 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   a.fstride = fac.nbatch == 1 ? 0 : p.factor_size;
   a.rhsp = rhsp;
   a.xp = xp;
-  a.reff = reff;
+  a.zero = zero;
   a.ybuf = ybuf;
   a.cbv = cbv;
   a.nslab = nrhs;
-  require(ncpl <= 2, "sweep: at most two coupling terms");
-  a.ncpl = ncpl;
-  for (int c = 0; c < ncpl; ++c) {
-    int width = 0;
-    const std::vector<DevBuf> &pcs = permuted_ell(sp, p, cpl[c].rowptr, cpl[c].col, s, &width);
-    a.cpl[c].width = width;
-    a.cpl[c].colp = pcs[0].as<int>();
-    a.cpl[c].eidx = pcs[1].as<int>();
-    a.cpl[c].val = cpl[c].val;
-    a.cpl[c].val_stride = cpl[c].val_stride;
-    a.cpl[c].val_shift = cpl[c].val_shift;
-    a.cpl[c].lag = cpl[c].lag;
-    a.cpl[c].coef = cpl[c].coef;
-  }
-  static const int fused_env = env_int2("STMHD_SWEEP_FUSED", 1);
-  if (fused_env && ncpl > 0 && sp.nsub > 0) {
-    const CplProgram &pg = get_program(sp, p, cpl, ncpl, s);
-    if (pg.ok) {
-      int per_slab = 0;
-      CplVals cv{};
-      for (int c = 0; c < ncpl; ++c) {
-        per_slab |= cpl[c].val_stride != 0 || cpl[c].lag > 1;
-        cv.lag[c] = cpl[c].lag;
-        cv.val[c] = cpl[c].val;
-        cv.stride[c] = cpl[c].val_stride;
-        cv.shift[c] = cpl[c].val_shift;
-        cv.coef[c] = cpl[c].coef;
-      }
-      const int nblk = per_slab ? nrhs : 1;
-      static DevBuf pvals;
-      const size_t vneed = (size_t)nblk * pg.nent * sizeof(double);
-      if (pvals.bytes < vneed) {
-        STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-        pvals.alloc(vneed * 5 / 4);
-      }
-      cpl_vals_kernel<<<dim3((unsigned)std::min<int64_t>(cdiv(pg.nent, 256), 1024), nblk), 256, 0, s>>>(
-          pg.esrc.as<int2>(), pg.nent, cv, per_slab, pvals.as<double>());
-      STMHD_LAUNCH_CHECK();
-      a.prog_hdr = pg.hdr.as<int4>();
-      a.prog_items = pg.items.as<int2>();
-      a.prog_ecol = pg.ecol.as<int>();
-      a.prog_vals = pvals.as<double>();
-      a.prog_nent = pg.nent;
-      a.prog_per_slab = per_slab;
-      a.tbuf = tbuf;
+  a.ncta = cluster;
+  require(ncpl <= kMaxCpl && next <= 2, "sweep: at most four coupling terms and two external sources");
+  if (ncpl > 0) {
+    const std::vector<int> *ext_pos[2] = {nullptr, nullptr};
+    for (int e = 0; e < next; ++e) {
+      require(ext[e] && ext[e]->sp && ext[e]->nrhs == nrhs, "sweep: external stage not prepared for these slabs");
+      ext_pos[e] = &ext[e]->sp->pos_h;
+      a.ext_xp[e] = ext[e]->a.xp;
+      a.ext_n[e] = ext[e]->a.n;
     }
+    for (int c = 0; c < ncpl; ++c) require(cpl[c].ext < next, "sweep: coupling refers to a missing external stage");
+    const CplProgram &pg = get_program(sp, p, cpl, ncpl, ext_pos, s);
+    int per_slab = 0;
+    CplVals cv{};
+    for (int c = 0; c < ncpl; ++c) {
+      per_slab |= cpl[c].val_stride != 0;
+      cv.val[c] = cpl[c].val;
+      cv.stride[c] = cpl[c].val_stride;
+      cv.shift[c] = cpl[c].val_shift;
+      cv.coef[c] = cpl[c].coef;
+    }
+    const int nblk = per_slab ? nrhs : 1;
+    const size_t vneed = (size_t)nblk * pg.nent * sizeof(double);
+    if (st.pvals.bytes < vneed) {
+      STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
+      st.pvals.alloc(vneed);
+    }
+    cpl_vals_kernel<<<dim3((unsigned)std::min<int64_t>(cdiv(pg.nent, 256), 1024), nblk), 256, 0, s>>>(
+        pg.esrc.as<int2>(), pg.nent, cv, per_slab, st.pvals.as<double>());
+    STMHD_LAUNCH_CHECK();
+    a.prog_hdr = pg.hdr.as<int4>();
+    a.prog_items = pg.items.as<int2>();
+    a.prog_ecol = pg.ecol.as<int>();
+    a.prog_vals = st.pvals.as<double>();
+    a.prog_nent = pg.nent;
+    a.prog_per_slab = per_slab;
+    a.tbuf = tbuf;
   }
   a.slot = slot;
   a.vstride = vstride;
   a.null_work = env_int2("STMHD_SWEEP_NULL", 0);
-  const int threads = warps * 32;
-  const size_t smem =
-      ((size_t)warps * a.vstride + 3 * a.sub_len + a.sub_cb + 1) * sizeof(double) + (size_t)warps * a.tstride;
-  require(smem <= 224 * 1024, "nd sweep: subtree vectors or fronts too large for shared memory");
+  st.smem = ((size_t)warps * a.vstride + 3 * a.sub_len + a.sub_cb + 1) * sizeof(double) + (size_t)warps * a.tstride;
+  require(st.smem <= 224 * 1024, "nd sweep: subtree vectors or fronts too large for shared memory");
+  // consumers wait on their producers' flags (set at launch)
+  a.nwait = next;
+  for (int e = 0; e < next; ++e) a.flag_in[e] = nullptr;
+  st.a.flag_out = nullptr;
+}
+
+void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
+  require(nst >= 1 && nst <= 3, "sweep: 1 to 3 stages per launch");
+  static int epoch = 0;
+  ++epoch;
+  SweepMulti m{};
+  size_t smem = 0;
+  for (int i = 0; i < nst; ++i) {
+    SweepStage &st = *stg[i];
+    st.a.epoch = epoch;
+    if (nst > 1) {  // every stage publishes per-slab flags
+      const int64_t need = (int64_t)st.nrhs * kCluster;
+      if (st.flags_slabs < need) {
+        st.flags.alloc(need * sizeof(int));
+        STMHD_CUDA_CHECK(cudaMemsetAsync(st.flags.ptr, 0, need * sizeof(int), s));
+        st.flags_slabs = need;
+      }
+      st.a.flag_out = st.flags.as<int>();
+    } else {
+      st.a.flag_out = nullptr;
+    }
+    smem = std::max(smem, st.smem);
+  }
+  for (int i = 0; i < nst; ++i) {
+    SweepStage &st = *stg[i];
+    for (int e = 0; e < st.a.nwait; ++e) {
+      int prod = -1;
+      for (int j = 0; j < i; ++j)
+        if (stg[j]->a.xp == st.a.ext_xp[e]) prod = j;
+      require(prod >= 0, "sweep: an external source must be an earlier stage of the same launch");
+      st.a.flag_in[e] = stg[prod]->a.flag_out;
+    }
+    m.st[i] = st.a;
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncAttributes fa{};
@@ -1184,57 +1218,74 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
     }
     attr = true;
   }
+  SweepStage &s0 = *stg[0];
+  const int64_t n0 = s0.a.n;
+  const int nrhs0 = s0.nrhs;
   static const int trace_on = env_int2("STMHD_SWEEP_TRACE", 0);
   DevBuf tr;
   int nsteps = 0;
-  if (trace_on) {
-    nsteps = 4 + nrhs * (2 * p.nlevels + 4);
+  if (trace_on) {  // stage 0 only
+    nsteps = 4 + nrhs0 * (2 * s0.fac->dev->plan->nlevels + 4);
     tr.alloc(nsteps * sizeof(unsigned long long));
     STMHD_CUDA_CHECK(cudaMemsetAsync(tr.ptr, 0, tr.bytes, s));
-    a.trace = tr.as<unsigned long long>();
+    m.st[0].trace = tr.as<unsigned long long>();
   }
   static const int prof_on = env_int2("STMHD_SWEEP_PROF", 0);
   DevBuf pr;
   if (prof_on) {
-    pr.alloc((size_t)cluster * warps * 8 * sizeof(unsigned long long));
-    a.prof = pr.as<unsigned long long>();
+    pr.alloc((size_t)kCluster * kWarps * 8 * sizeof(unsigned long long));
+    m.st[0].prof = pr.as<unsigned long long>();
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cluster);
-  cfg.blockDim = dim3(threads);
+  cfg.gridDim = dim3(kCluster * nst);
+  cfg.blockDim = dim3(kWarps * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = cluster;
+  at[0].val.clusterDim.x = kCluster;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  int nat = 1;
+  if (nst > 1) {  // the stages wait on each other: all clusters must be co-resident
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    nat = 2;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = 1;
-  void *args[] = {&a};
+  cfg.numAttrs = nat;
+  void *args[] = {&m};
   STMHD_CUDA_CHECK(cudaLaunchKernelExC(
       &cfg, prof_on ? (const void *)nd_sweep_kernel<true> : (const void *)nd_sweep_kernel<false>, args));
   count_launch();
-  permute_out_kernel<<<dim3(std::min<int64_t>(cdiv(n, 256), 256), nrhs), 256, 0, s>>>(xp, sp.pos.as<int>(), n, nrhs, x,
-                                                                                     ld_x);
-  STMHD_LAUNCH_CHECK();
+  for (int i = 0; i < nst; ++i) {
+    SweepStage &st = *stg[i];
+    const int64_t n = st.a.n;
+    permute_out_kernel<<<dim3(std::min<int64_t>(cdiv(n, 256), 256), st.nrhs), 256, 0, s>>>(
+        st.a.xp, st.sp->pos.as<int>(), n, st.nrhs, st.x, st.ld_x);
+    STMHD_LAUNCH_CHECK();
+  }
   if (trace_on) {
+    const SweepArgs &a = s0.a;
+    const NDPlan &p = *s0.fac->dev->plan;
     std::vector<unsigned long long> h(nsteps);
     STMHD_CUDA_CHECK(cudaMemcpyAsync(h.data(), tr.ptr, nsteps * 8, cudaMemcpyDeviceToHost, s));
     STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
     const bool fz = a.prog_hdr != nullptr;
     auto entries = [&](int k) {
-      return (int)fz + (k > 0 && a.ncpl && !fz) + (a.nsub ? 1 : 0) + 2 * a.ntop + (a.nsub && k + 1 < a.nslab);
+      return (int)fz + ((a.nsub || fz) ? 1 : 0) + 2 * a.ntop + (a.nsub && k + 1 < a.nslab);
     };
     const int per = entries(1), base = 1 + entries(0);
-    fprintf(stderr, "[sweep] n=%lld levels=%d top=%d sub=%d fused=%d total=%.1f us | slab1 (us):", (long long)n,
-            p.nlevels, a.ntop, a.nsub, (int)fz, (*std::max_element(h.begin(), h.end()) - h[0]) / 1e3);
+    fprintf(stderr, "[sweep] n=%lld levels=%d top=%d sub=%d fused=%d stages=%d total=%.1f us | slab1 (us):",
+            (long long)n0, p.nlevels, a.ntop, a.nsub, (int)fz, nst,
+            (*std::max_element(h.begin(), h.end()) - h[0]) / 1e3);
     for (int i = 0; i < per && base + i < nsteps; ++i) fprintf(stderr, " %.2f", (h[base + i] - h[base + i - 1]) / 1e3);
     fprintf(stderr, "\n[sweep] factor/slab %.2f MB nslab %d (batch %d) smem %zu B vstride %d slot %d sub_len %lld sub_cb %lld\n",
-            p.factor_size * 8e-6, nrhs, fac.nbatch, smem, a.vstride, a.slot, (long long)a.sub_len, (long long)a.sub_cb);
+            p.factor_size * 8e-6, nrhs0, s0.fac->nbatch, smem, a.vstride, a.slot, (long long)a.sub_len,
+            (long long)a.sub_cb);
   }
   if (prof_on) {
-    const int nwp = cluster * warps;
+    const int nwp = kCluster * kWarps;
     std::vector<unsigned long long> h((size_t)nwp * 8);
     STMHD_CUDA_CHECK(cudaMemcpyAsync(h.data(), pr.ptr, h.size() * 8, cudaMemcpyDeviceToHost, s));
     STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -1244,13 +1295,25 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
         mean[i] += (double)h[w * 8 + i] / nwp;
         mx[i] = std::max(mx[i], (double)h[w * 8 + i]);
       }
-    const double us = 1.0 / 1963.0 / nrhs;  // cycles -> us per slab at the loaded SM clock
+    const double us = 1.0 / 1963.0 / nrhs0;  // cycles -> us per slab at the loaded SM clock
     fprintf(stderr,
             "[sweep-prof] per slab per warp (us) mean/max: gather %.2f/%.2f wait %.2f/%.2f gemv %.2f/%.2f "
             "barrier %.2f/%.2f | tasks %.1f/%.0f chunks %.1f/%.0f | gemv-only fwd %.2f bwd %.2f\n",
             mean[0] * us, mx[0] * us, mean[1] * us, mx[1] * us, mean[2] * us, mx[2] * us, mean[3] * us, mx[3] * us,
-            mean[4] / nrhs, mx[4] / nrhs, mean[5] / nrhs, mx[5] / nrhs, mean[6] * us, mean[7] * us);
+            mean[4] / nrhs0, mx[4] / nrhs0, mean[5] / nrhs0, mx[5] / nrhs0, mean[6] * us, mean[7] * us);
   }
+}
+
+void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,
+              const SweepCoupling *cpl, int ncpl, cudaStream_t s) {
+  // one stage per factor structure (reused across calls and factorisations; launches
+  // are stream ordered)
+  static std::map<const NDDevice *, SweepStagePtr> stages;
+  SweepStagePtr &sp = stages[fac.dev];
+  if (!sp) sp = sweep_stage_new();
+  sweep_stage_prepare(*sp, fac, rhs, ld_rhs, x, ld_x, nrhs, cpl, ncpl, nullptr, 0, s);
+  SweepStage *one = sp.get();
+  sweep_stages_launch(&one, 1, s);
 }
 
 }  // namespace stmhd

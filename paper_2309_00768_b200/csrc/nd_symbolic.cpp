@@ -1,4 +1,5 @@
 // Host symbolic analysis for the nested-dissection supernodal LU (see nd.hpp).
+#include <cstdlib>
 #include <algorithm>
 #include <numeric>
 #include <queue>
@@ -263,7 +264,10 @@ NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const in
   p.bsz_f.assign(S, 0);
   p.bsz_b.assign(S, 0);
   // rows per chunk: the largest power of two <= 32 whose block fits kChunkMax doubles
-  const int64_t kChunkMax = 640;
+  static const int64_t kChunkMax = [] {
+    const char *e = getenv("STMHD_CHUNK_MAX");
+    return e ? (int64_t)atoi(e) : (int64_t)640;
+  }();
   auto rows_per_chunk = [&](int64_t K) {
     int R = 32;
     while (R > 1 && (int64_t)R * K > kChunkMax) R >>= 1;

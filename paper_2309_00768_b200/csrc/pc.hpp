@@ -14,6 +14,7 @@ struct PC {
   DevBuf alf, ca_vals, s1_vals;
   DevBuf tu1, tu2, ta1, ta2, ta3, tp1, tp2, tp3, tj;
   std::unique_ptr<NDFactor> fu, ca, fa, fpf;
+  SweepStagePtr st_wave, st_mj, st_vel;  // pipelined apply_inverse (TRIANGULAR)
 
   PC(stmhd_disc_s *d, cudaStream_t s, const double *js, const double *fp, const double *alf, int variant);
   void ensure_forward_factors(cudaStream_t s);
@@ -32,7 +33,9 @@ struct PC {
   void apply_velocity(const double *in, int64_t li, double *out, int64_t lo, cudaStream_t s);
   void coupling_u(const double *z, int64_t lz, double beta, const double *xs, int64_t lxs, double alpha,
                   const double *xp, int64_t lxp, double alpha_p, double *out, int64_t lo, cudaStream_t s);
+  void wave_couplings(SweepCoupling *c) const;
   void apply_inverse(const double *r, double *x, cudaStream_t s);
+  void apply_inverse_pipelined(const double *r, double *x, cudaStream_t s);
   void apply_forward(const double *x, double *out, cudaStream_t s);
   void op(int which, const double *in, double *out, cudaStream_t s);
 };

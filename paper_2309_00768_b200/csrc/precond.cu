@@ -169,8 +169,9 @@ void PC::apply_potential(const double *in, int64_t li, double *out, int64_t lo, 
   spmv(a, s, 8);
 }
 
-void PC::solve_wave(const double *in, int64_t li, double *out, int64_t lo, cudaStream_t s) {
-  SweepCoupling c[2];
+// C~_A sweep couplings (precond.py:194-205): sub-diagonal S1_k (per slab) and the
+// shared second sub-diagonal S2
+void PC::wave_couplings(SweepCoupling *c) const {
   c[0].rowptr = d->D<int>("s1_rowptr");
   c[0].col = d->D<int>("s1_col");
   c[0].val = s1_vals.as<double>();
@@ -184,6 +185,11 @@ void PC::solve_wave(const double *in, int64_t li, double *out, int64_t lo, cudaS
   c[1].val = s2.val;
   c[1].lag = 2;
   c[1].coef = -1.0;
+}
+
+void PC::solve_wave(const double *in, int64_t li, double *out, int64_t lo, cudaStream_t s) {
+  SweepCoupling c[2];
+  wave_couplings(c);
   ca->sweep(in, li, out, lo, nt, c, 2, s);
 }
 
@@ -372,7 +378,86 @@ void PC::coupling_u(const double *z, int64_t lz, double beta, const double *xs, 
   spmv(a, s, 8);
 }
 
+// TRIANGULAR P_T^{-1} (precond.py:270-300) with the three sequential sweeps of one
+// application -- the C~_A wave sweep (x_A), the M_j solves (x_j = M_j^{-1}(r_j - K x_A))
+// and the F_u sweep (rhs r_u - B^T x_p - Z_j x_j - Z_a x_A) -- in ONE launch, one
+// cluster each, pipelined slab by slab: slab k of a consumer starts as soon as its
+// producers have published slab k.  Same arithmetic as apply_inverse's sequential
+// path up to the summation order of the coupled right-hand sides.
+void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
+  const double *r_u = r, *r_p = r + o_p, *r_j = r + o_j, *r_a = r + o_a;
+  // batched (slab-parallel) pre-steps: wave right-hand side and the pressure block
+  d->lu_ma->solve(r_a, slab, ta1.as<double>(), n_a, nt, s);
+  apply_potential(ta1.as<double>(), n_a, ta2.as<double>(), n_a, s);
+  pressure_schur_inverse(r_p, slab, x + o_p, slab, s);
+  {  // tu1 = r_u - B^T x_p
+    SpmvArgs a;
+    a.nrows = n_u;
+    a.nslab = nt;
+    a.y = tu1.as<double>();
+    a.y_stride = n_u;
+    a.z = r_u;
+    a.z_stride = slab;
+    a.beta = 1.0;
+    a.t[0] = csr_term(d->csr("divt"), x + o_p, slab, -1.0);
+    a.nterms = 1;
+    spmv(a, s, 8);
+  }
+  if (!st_wave) {
+    st_wave = sweep_stage_new();
+    st_mj = sweep_stage_new();
+    st_vel = sweep_stage_new();
+  }
+  SweepCoupling cw[2];
+  wave_couplings(cw);
+  sweep_stage_prepare(*st_wave, *ca, ta2.as<double>(), n_a, x + o_a, slab, nt, cw, 2, nullptr, 0, s);
+  SweepCoupling cj;  // -K_jA x_A
+  DCsr mix = d->csr("mixja");
+  cj.rowptr = mix.rowptr;
+  cj.col = mix.col;
+  cj.val = mix.val;
+  cj.ext = 0;
+  cj.coef = -1.0;
+  SweepStage *wj[1] = {st_wave.get()};
+  sweep_stage_prepare(*st_mj, *d->lu_mj, r_j, slab, x + o_j, slab, nt, &cj, 1, wj, 1, s);
+  SweepCoupling cu[3];
+  DCsr m = d->csr("mu_dt");  // + M_u/dt x_u(k-1)
+  cu[0].rowptr = m.rowptr;
+  cu[0].col = m.col;
+  cu[0].val = m.val;
+  cu[0].lag = 1;
+  cu[0].coef = 1.0;
+  cu[1].rowptr = d->D<int>("js_seg0");  // - Z_j x_j: u rows, z_j segment, slab columns o_j + j
+  cu[1].rowend = d->D<int>("js_seg1");
+  cu[1].col = d->D<int>("js_col");
+  cu[1].col_off = (int)o_j;
+  cu[1].val = js;
+  cu[1].val_stride = nnz_js;
+  cu[1].ext = 0;
+  cu[1].coef = -1.0;
+  cu[2].rowptr = d->D<int>("js_seg1");  // - Z_a x_A: u rows, z_a segment, slab columns o_a + a
+  cu[2].rowend = d->D<int>("js_rowptr") + 1;
+  cu[2].col = d->D<int>("js_col");
+  cu[2].col_off = (int)o_a;
+  cu[2].val = js;
+  cu[2].val_stride = nnz_js;
+  cu[2].ext = 1;
+  cu[2].coef = -1.0;
+  SweepStage *ju[2] = {st_mj.get(), st_wave.get()};
+  sweep_stage_prepare(*st_vel, *fu, tu1.as<double>(), n_u, x, slab, nt, cu, 3, ju, 2, s);
+  SweepStage *all[3] = {st_wave.get(), st_mj.get(), st_vel.get()};
+  sweep_stages_launch(all, 3, s);
+}
+
 void PC::apply_inverse(const double *r, double *x, cudaStream_t s) {
+  static const int pipelined = [] {
+    const char *e = getenv("STMHD_PC_PIPELINE");
+    return e ? atoi(e) : 1;
+  }();
+  if (variant == 0 && pipelined) {
+    apply_inverse_pipelined(r, x, s);
+    return;
+  }
   const double *r_u = r, *r_p = r + o_p, *r_j = r + o_j, *r_a = r + o_a;
   int64_t lr_u = slab, lr_p = slab, lr_a = slab;
   if (variant == 2) {

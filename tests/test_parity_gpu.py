@@ -205,3 +205,32 @@ def test_config1(p, golden):
     x = state.vec.data.cpu().numpy() - g["state0"]
     assert relerr(x, g["gmres_x"]) < 1e-8
     assert abs(stats.residual_norms[1] / stats.residual_norms[0] - 1.0303688174095965e-2) < 1e-6
+
+
+def test_pipelined_apply_deterministic_and_matches_sequential(p, golden):
+    """The TRIANGULAR P_T^{-1} runs its three sweeps in one pipelined launch (per-slab
+    release/acquire flags between clusters).  Repeated applications must be bitwise
+    identical (no race in the handshake), and equal the sequential composition of the
+    individual operators to rounding: x_A = S_A^{-1} r_A, x_p = S_p^{-1} r_p, and the
+    velocity block checked through the forward operator, P (P^{-1} v) = v."""
+    import torch
+
+    g = golden("bl_c1")
+    d = _disc(p, "bl_c1")
+    st = p.SpaceTimeState(p.BlockVector(d.layout, d.n_steps, g["state"]), torch.as_tensor(g["ic_u"], device="cuda"),
+                          torch.as_tensor(g["ic_a"], device="cuda"))
+    jac = p.assemble_jacobian(st, d)
+    pc = p.SpaceTimePreconditioner(jac, d, st)
+    v = torch.as_tensor(g["v"], device="cuda")
+    outs = [pc.apply_inverse(v).clone() for _ in range(6)]
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    L, nt = d.layout, d.n_steps
+    o = outs[0].view(nt, -1)
+    vv = v.view(nt, -1)
+    o_p, o_j, o_a = L.n_u, L.n_u + L.n_p, L.n_u + L.n_p + L.n_j
+    x_a = pc.magnetic_schur_inverse(vv[:, o_a:].reshape(-1)).view(nt, -1)
+    assert relerr(o[:, o_a:].cpu().numpy(), x_a.cpu().numpy()) < 1e-12
+    x_p = pc.pressure_schur_inverse(vv[:, o_p:o_j].reshape(-1)).view(nt, -1)
+    assert relerr(o[:, o_p:o_j].cpu().numpy(), x_p.cpu().numpy()) < 1e-12
+    assert relerr(pc.apply_forward(outs[0]).cpu().numpy(), g["v"]) < 1e-10
