@@ -210,9 +210,16 @@ using SweepStagePtr = std::unique_ptr<SweepStage, SweepStageDeleter>;
 SweepStagePtr sweep_stage_new();
 // Permute the stage's right-hand sides in and bind its couplings; ext[e] are stages
 // prepared before whose (permuted) output feeds the couplings with ext = e.
+// vals_tag != 0: the coupling values are unchanged since the last prepare with the
+// same tag (a preconditioner's lifetime), so their gathered copy is reused.
 void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
                          int64_t ld_x, int nrhs, const SweepCoupling *cpl, int ncpl, SweepStage *const *ext,
-                         int next, cudaStream_t s);
+                         int next, cudaStream_t s, int64_t vals_tag = 0);
+// After every slab k, add sum_c coef_c C_c src_c(k) to target's right-hand side of
+// slab k (before publishing slab k).  Sources: this stage's x_k (ext < 0) or its
+// external stages.  Call after both stages are prepared, before the launch.
+void sweep_stage_set_post(SweepStage &st, SweepStage &target, const SweepCoupling *cpl, int ncpl, cudaStream_t s,
+                          int64_t vals_tag = 0);
 // Run prepared stages in ONE launch, one 16-CTA cluster each, pipelined slab by slab
 // (a consumer waits on per-slab release flags of its producers); then permute out.
 void sweep_stages_launch(SweepStage *const *st, int nst, cudaStream_t s);

@@ -344,6 +344,14 @@ struct SweepArgs {
   int64_t prog_nent;
   int prog_per_slab;
   double *tbuf;                // coupled right-hand side of the top rows
+  // post-slab program (pipelined launch): after slab k, post_out[k] += C x(k)
+  const int4 *post_hdr;
+  const int2 *post_items;
+  const int *post_ecol;
+  const double *post_vals;
+  int64_t post_nent, post_n;
+  int post_per_slab;
+  double *post_out;            // another stage's permuted right-hand sides (nslab x post_n)
   const int4 *g3p;
   const int *bpos;
   int nlevels, nw;
@@ -639,6 +647,96 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
   __syncwarp();
 }
 
+// Run this CTA's items of a coupling program.  MODE 0 (slab start): rhs rows, item
+// dst kind 0 -> the subtree's shared rhs_s, kind 1 -> tbuf.  MODE 1 (after a slab):
+// out[dst] += sum, the rows of another stage's right-hand side.  srcs: source table.
+template <int MODE>
+__device__ __forceinline__ void run_program(const int4 hd, const int2 *items, const int *ecol, const double *vk,
+                                            const double *rhs, double *out, const SubView &sv, double *tbuf,
+                                            const double *const *srcs) {
+  const int nth = blockDim.x;
+  constexpr int kIdx = (1 << 28) - 1;
+  // threads per item: spread an item's entries over tpi lanes when there are few
+  // items (so every load of the step is in flight at once)
+  int tpi = 1;
+  while (tpi < 32 && hd.y * tpi * 2 <= nth) tpi *= 2;
+  if (tpi == 1) {
+    for (int i0 = threadIdx.x; i0 < hd.y; i0 += 2 * nth) {
+      const int it[2] = {i0, i0 + nth};
+      const bool live[2] = {true, i0 + nth < hd.y};
+      double acc[2];
+      int2 io[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        io[r] = live[r] ? items[hd.x + it[r]] : make_int2(0, -1);
+        acc[r] = io[r].y >= 0 ? rhs[io[r].y] : 0.0;
+      }
+      for (int s0 = 0; s0 < hd.w; s0 += 8) {
+        int cc[2][8];
+        double vv[2][8];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int64_t id = hd.z + (int64_t)(s0 + q) * hd.y + it[r];
+            const bool ok = live[r] && s0 + q < hd.w;
+            cc[r][q] = ok ? __ldg(ecol + id) : 0;
+            vv[r][q] = ok ? __ldg(vk + id) : 0.0;
+          }
+        double xv[2][8];  // all 16 loads in flight together
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) xv[r][q] = srcs[cc[r][q] >> 28][cc[r][q] & kIdx];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[r] = fma(vv[r][q], xv[r][q], acc[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        if (!live[r]) continue;
+        const int kind = io[r].x >> 29, di = io[r].x & ((1 << 29) - 1);
+        if (MODE == 1) out[io[r].x] += acc[r];
+        else if (kind == 0) sv.rhs_s[di] = acc[r];
+        else tbuf[di] = acc[r];
+      }
+    }
+  } else {
+    const int g = threadIdx.x / tpi, part = threadIdx.x & (tpi - 1), ng = nth / tpi;
+    for (int base = 0; base < hd.y; base += ng) {  // uniform trip count per warp
+      const int it = base + g;
+      const bool live = it < hd.y;
+      const int2 io = live ? items[hd.x + it] : make_int2(0, -1);
+      double acc = 0.0;
+      for (int s0 = part; s0 < hd.w; s0 += 16 * tpi) {
+        int cc[16];
+        double vv[16], xv[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int sl = s0 + q * tpi;
+          const bool ok = live && sl < hd.w;
+          const int64_t id = hd.z + (int64_t)sl * hd.y + it;
+          cc[q] = ok ? __ldg(ecol + id) : 0;
+          vv[q] = ok ? __ldg(vk + id) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) xv[q] = srcs[cc[q] >> 28][cc[q] & kIdx];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc = fma(vv[q], xv[q], acc);
+      }
+      for (int o = 1; o < tpi; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (live && part == 0) {
+        acc += io.y >= 0 ? rhs[io.y] : 0.0;
+        const int kind = io.x >> 29, di = io.x & ((1 << 29) - 1);
+        if (MODE == 1) out[io.x] += acc;
+        else if (kind == 0) sv.rhs_s[di] = acc;
+        else tbuf[di] = acc;
+      }
+    }
+  }
+}
+
 // Up to three sweeps of one pipelined launch, one cluster each (cluster i runs st[i]).
 struct SweepMulti {
   SweepArgs st[3];
@@ -725,7 +823,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
         s_src[2] = k >= 2 ? a.xp + (int64_t)(k - 2) * n : a.zero;
         s_src[3] = a.ext_xp[0] ? a.ext_xp[0] + (int64_t)k * a.ext_n[0] : a.zero;
         s_src[4] = a.ext_xp[1] ? a.ext_xp[1] + (int64_t)k * a.ext_n[1] : a.zero;
-        s_src[5] = s_src[6] = s_src[7] = a.zero;
+        s_src[5] = s_src[6] = s_src[7] = a.zero;  // 5: own x_k (post-slab program only)
       }
       // pipelined launch: wait until every CTA of each producer has published slab k
       if ((int)threadIdx.x < a.nwait * a.ncta) {
@@ -739,87 +837,8 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
         }
       }
       __syncthreads();
-      const int4 hd = a.prog_hdr[crank];
       const double *vk = a.prog_vals + (a.prog_per_slab ? (int64_t)k * a.prog_nent : 0);
-      const int nth = blockDim.x;
-      constexpr int kIdx = (1 << 28) - 1;
-      // threads per item: spread an item's entries over tpi lanes when there are few
-      // items (so every load of the step is in flight at once)
-      int tpi = 1;
-      while (tpi < 32 && hd.y * tpi * 2 <= nth) tpi *= 2;
-      if (tpi == 1) {
-        for (int i0 = threadIdx.x; i0 < hd.y; i0 += 2 * nth) {
-          const int it[2] = {i0, i0 + nth};
-          const bool live[2] = {true, i0 + nth < hd.y};
-          double acc[2];
-          int2 io[2];
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            io[r] = live[r] ? a.prog_items[hd.x + it[r]] : make_int2(0, -1);
-            acc[r] = io[r].y >= 0 ? rhs[io[r].y] : 0.0;
-          }
-          for (int s0 = 0; s0 < hd.w; s0 += 8) {
-            int cc[2][8];
-            double vv[2][8];
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const int64_t id = hd.z + (int64_t)(s0 + q) * hd.y + it[r];
-                const bool ok = live[r] && s0 + q < hd.w;
-                cc[r][q] = ok ? __ldg(a.prog_ecol + id) : 0;
-                vv[r][q] = ok ? __ldg(vk + id) : 0.0;
-              }
-            double xv[2][8];  // all 16 loads in flight together
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-              for (int q = 0; q < 8; ++q) xv[r][q] = s_src[cc[r][q] >> 28][cc[r][q] & kIdx];
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-              for (int q = 0; q < 8; ++q) acc[r] = fma(vv[r][q], xv[r][q], acc[r]);
-          }
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            if (!live[r]) continue;
-            const int kind = io[r].x >> 29, di = io[r].x & ((1 << 29) - 1);
-            if (kind == 0) sv.rhs_s[di] = acc[r];
-            else a.tbuf[di] = acc[r];
-          }
-        }
-      } else {
-        const int g = threadIdx.x / tpi, part = threadIdx.x & (tpi - 1), ng = nth / tpi;
-        for (int base = 0; base < hd.y; base += ng) {  // uniform trip count per warp
-          const int it = base + g;
-          const bool live = it < hd.y;
-          const int2 io = live ? a.prog_items[hd.x + it] : make_int2(0, -1);
-          double acc = 0.0;
-          for (int s0 = part; s0 < hd.w; s0 += 16 * tpi) {
-            int cc[16];
-            double vv[16], xv[16];
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const int sl = s0 + q * tpi;
-              const bool ok = live && sl < hd.w;
-              const int64_t id = hd.z + (int64_t)sl * hd.y + it;
-              cc[q] = ok ? __ldg(a.prog_ecol + id) : 0;
-              vv[q] = ok ? __ldg(vk + id) : 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < 16; ++q) xv[q] = s_src[cc[q] >> 28][cc[q] & kIdx];
-#pragma unroll
-            for (int q = 0; q < 16; ++q) acc = fma(vv[q], xv[q], acc);
-          }
-          for (int o = 1; o < tpi; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-          if (live && part == 0) {
-            acc += io.y >= 0 ? rhs[io.y] : 0.0;
-            const int kind = io.x >> 29, di = io.x & ((1 << 29) - 1);
-            if (kind == 0) sv.rhs_s[di] = acc;
-            else a.tbuf[di] = acc;
-          }
-        }
-      }
+      run_program<0>(a.prog_hdr[crank], a.prog_items, a.prog_ecol, vk, rhs, nullptr, sv, a.tbuf, s_src);
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step);
     }
@@ -856,6 +875,20 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
       for (int ti = w.bnd[L]; ti < t1; ++ti) backward_task<true, PROF>(a, w.tl[ti], F, x, sv, w, mbar);
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+    }
+    if (a.post_hdr && !a.null_work) {
+      // post-slab program: rows of another stage's right-hand side from this stage's
+      // x_k (all CTAs' parts: cluster barrier) and external sources at slab k
+      sweep_barrier();
+      if (threadIdx.x == 0) {
+        s_src[3] = a.ext_xp[0] ? a.ext_xp[0] + (int64_t)k * a.ext_n[0] : a.zero;
+        s_src[4] = a.ext_xp[1] ? a.ext_xp[1] + (int64_t)k * a.ext_n[1] : a.zero;
+        s_src[5] = a.xp + (int64_t)k * n;
+      }
+      __syncthreads();
+      const double *vk = a.post_vals + (a.post_per_slab ? (int64_t)k * a.post_nent : 0);
+      run_program<1>(a.post_hdr[crank], a.post_items, a.post_ecol, vk, nullptr, a.post_out + (int64_t)k * a.post_n,
+                     sv, nullptr, s_src);
     }
     if (a.flag_out) {  // pipelined launch: publish this CTA's part of x_k at gpu scope
       __threadfence();
@@ -1051,8 +1084,13 @@ struct SweepStage {
   double *x = nullptr;
   int64_t ld_x = 0;
   int nrhs = 0;
-  DevBuf scratch, zero, pvals, flags;
+  DevBuf scratch, zero, pvals, flags, post_vals;
   int64_t flags_slabs = 0;
+  // gathered coupling values are reused while (tag, program) are unchanged (tag 0:
+  // always regather)
+  int64_t vals_tag = 0, post_tag = 0;
+  const std::vector<int> *ext_pos[2] = {nullptr, nullptr};
+  const CplProgram *vals_prog = nullptr, *post_prog = nullptr;
 };
 
 void SweepStageDeleter::operator()(SweepStage *p) const { delete p; }
@@ -1060,9 +1098,33 @@ SweepStagePtr sweep_stage_new() { return SweepStagePtr(new SweepStage()); }
 
 static constexpr int kCluster = 16, kWarps = 16;
 
+// gathered values of a program: vals[b][id] (b = slab if any coupling is per-slab)
+static int gather_values(const CplProgram &pg, const SweepCoupling *cpl, int ncpl, int nrhs, DevBuf &buf,
+                         cudaStream_t s) {
+  int per_slab = 0;
+  CplVals cv{};
+  for (int c = 0; c < ncpl; ++c) {
+    per_slab |= cpl[c].val_stride != 0;
+    cv.val[c] = cpl[c].val;
+    cv.stride[c] = cpl[c].val_stride;
+    cv.shift[c] = cpl[c].val_shift;
+    cv.coef[c] = cpl[c].coef;
+  }
+  const int nblk = per_slab ? nrhs : 1;
+  const size_t vneed = (size_t)nblk * pg.nent * sizeof(double);
+  if (buf.bytes < vneed) {
+    STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
+    buf.alloc(vneed);
+  }
+  cpl_vals_kernel<<<dim3((unsigned)std::min<int64_t>(cdiv(pg.nent, 256), 1024), nblk), 256, 0, s>>>(
+      pg.esrc.as<int2>(), pg.nent, cv, per_slab, buf.as<double>());
+  STMHD_LAUNCH_CHECK();
+  return per_slab;
+}
+
 void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
                          int64_t ld_x, int nrhs, const SweepCoupling *cpl, int ncpl, SweepStage *const *ext,
-                         int next, cudaStream_t s) {
+                         int next, cudaStream_t s, int64_t vals_tag) {
   const NDDevice &dev = *fac.dev;
   const NDPlan &p = *dev.plan;
   const int cluster = kCluster, warps = kWarps;
@@ -1127,34 +1189,23 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   a.nslab = nrhs;
   a.ncta = cluster;
   require(ncpl <= kMaxCpl && next <= 2, "sweep: at most four coupling terms and two external sources");
+  for (int e = 0; e < next; ++e) {
+    require(ext[e] && ext[e]->sp && ext[e]->nrhs == nrhs, "sweep: external stage not prepared for these slabs");
+    st.ext_pos[e] = &ext[e]->sp->pos_h;
+  }
+  st.post_prog = nullptr;
   if (ncpl > 0) {
     const std::vector<int> *ext_pos[2] = {nullptr, nullptr};
-    for (int e = 0; e < next; ++e) {
-      require(ext[e] && ext[e]->sp && ext[e]->nrhs == nrhs, "sweep: external stage not prepared for these slabs");
-      ext_pos[e] = &ext[e]->sp->pos_h;
-      a.ext_xp[e] = ext[e]->a.xp;
-      a.ext_n[e] = ext[e]->a.n;
-    }
+    for (int e = 0; e < next; ++e) ext_pos[e] = st.ext_pos[e];
     for (int c = 0; c < ncpl; ++c) require(cpl[c].ext < next, "sweep: coupling refers to a missing external stage");
     const CplProgram &pg = get_program(sp, p, cpl, ncpl, ext_pos, s);
     int per_slab = 0;
-    CplVals cv{};
-    for (int c = 0; c < ncpl; ++c) {
-      per_slab |= cpl[c].val_stride != 0;
-      cv.val[c] = cpl[c].val;
-      cv.stride[c] = cpl[c].val_stride;
-      cv.shift[c] = cpl[c].val_shift;
-      cv.coef[c] = cpl[c].coef;
+    for (int c = 0; c < ncpl; ++c) per_slab |= cpl[c].val_stride != 0;
+    if (!(vals_tag && st.vals_tag == vals_tag && st.vals_prog == &pg)) {
+      per_slab = gather_values(pg, cpl, ncpl, nrhs, st.pvals, s);
+      st.vals_tag = vals_tag;
+      st.vals_prog = &pg;
     }
-    const int nblk = per_slab ? nrhs : 1;
-    const size_t vneed = (size_t)nblk * pg.nent * sizeof(double);
-    if (st.pvals.bytes < vneed) {
-      STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-      st.pvals.alloc(vneed);
-    }
-    cpl_vals_kernel<<<dim3((unsigned)std::min<int64_t>(cdiv(pg.nent, 256), 1024), nblk), 256, 0, s>>>(
-        pg.esrc.as<int2>(), pg.nent, cv, per_slab, st.pvals.as<double>());
-    STMHD_LAUNCH_CHECK();
     a.prog_hdr = pg.hdr.as<int4>();
     a.prog_items = pg.items.as<int2>();
     a.prog_ecol = pg.ecol.as<int>();
@@ -1166,12 +1217,134 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   a.slot = slot;
   a.vstride = vstride;
   a.null_work = env_int2("STMHD_SWEEP_NULL", 0);
+  a.post_hdr = nullptr;  // set by sweep_stage_set_post for this launch
   st.smem = ((size_t)warps * a.vstride + 3 * a.sub_len + a.sub_cb + 1) * sizeof(double) + (size_t)warps * a.tstride;
   require(st.smem <= 224 * 1024, "nd sweep: subtree vectors or fronts too large for shared memory");
   // consumers wait on their producers' flags (set at launch)
   a.nwait = next;
-  for (int e = 0; e < next; ++e) a.flag_in[e] = nullptr;
+  for (int e = 0; e < next; ++e) {
+    a.flag_in[e] = nullptr;
+    a.ext_xp[e] = ext[e]->a.xp;
+    a.ext_n[e] = ext[e]->a.n;
+  }
   st.a.flag_out = nullptr;
+}
+
+// Post-slab program: rows of `target`'s (permuted) right-hand side, target_rhs[k] +=
+// sum_c coef_c C_c src_c, with sources this stage's x_k (couplings with ext < 0) or the
+// external stages of this stage at slab k.  Built once per coupling set.
+static const CplProgram &get_post_program(const NDSweepPlan &sp, const NDSweepPlan &tp, int64_t n_t,
+                                          const SweepCoupling *cpl, int ncpl,
+                                          const std::vector<int> *const *ext_pos, cudaStream_t s) {
+  std::vector<const void *> key{&tp, nullptr};  // (target plan, marker) distinguishes it from rhs programs
+  for (int c = 0; c < ncpl; ++c) {
+    key.push_back(cpl[c].rowptr);
+    key.push_back(cpl[c].rowend);
+    key.push_back(cpl[c].col);
+    key.push_back(reinterpret_cast<const void *>((intptr_t)(cpl[c].col_off * 16 + cpl[c].ext + 1)));
+  }
+  auto it = sp.prog_cache.find(key);
+  if (it != sp.prog_cache.end()) return *it->second;
+  const int ncta = sp.ncta;
+  std::vector<std::vector<int>> rb(ncpl), re(ncpl), cl(ncpl);
+  for (int c = 0; c < ncpl; ++c) {
+    rb[c].resize(n_t + 1);
+    STMHD_CUDA_CHECK(cudaMemcpyAsync(rb[c].data(), cpl[c].rowptr, (n_t + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    re[c].resize(n_t);
+    if (cpl[c].rowend)
+      STMHD_CUDA_CHECK(cudaMemcpyAsync(re[c].data(), cpl[c].rowend, n_t * sizeof(int), cudaMemcpyDeviceToHost, s));
+    STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (!cpl[c].rowend)
+      for (int64_t i = 0; i < n_t; ++i) re[c][i] = rb[c][i + 1];
+    int mx = 0;
+    for (int64_t i = 0; i < n_t; ++i) mx = std::max(mx, re[c][i]);
+    cl[c].resize(std::max(mx, 1));
+    if (mx) STMHD_CUDA_CHECK(cudaMemcpy(cl[c].data(), cpl[c].col, mx * sizeof(int), cudaMemcpyDeviceToHost));
+  }
+  // contiguous blocks of target rows per CTA
+  std::vector<int4> hdr(ncta);
+  std::vector<int2> it2;
+  std::vector<int> ecol;
+  std::vector<int2> esrc;
+  for (int c = 0; c < ncta; ++c) {
+    const int64_t q0 = n_t * c / ncta, q1 = n_t * (c + 1) / ncta;
+    std::vector<std::vector<int2>> ents(q1 - q0);  // {enc, cid}, e in a parallel list
+    std::vector<std::vector<int>> eids(q1 - q0);
+    int width = 0;
+    for (int64_t q = q0; q < q1; ++q) {
+      const int io = tp.iperm_h[q];
+      for (int cc = 0; cc < ncpl; ++cc)
+        for (int e = rb[cc][io]; e < re[cc][io]; ++e) {
+          const int jr = cl[cc][e] - cpl[cc].col_off;
+          int enc;
+          if (cpl[cc].ext >= 0) {
+            const std::vector<int> &ep = *ext_pos[cpl[cc].ext];
+            require(jr >= 0 && jr < (int)ep.size(), "sweep post program: external column out of range");
+            enc = ((3 + cpl[cc].ext) << 28) | ep[jr];
+          } else {
+            require(jr >= 0 && jr < (int)sp.pos_h.size(), "sweep post program: column out of range");
+            enc = (5 << 28) | sp.pos_h[jr];
+          }
+          ents[q - q0].push_back(make_int2(enc, cc));
+          eids[q - q0].push_back(e);
+        }
+      width = std::max(width, (int)ents[q - q0].size());
+    }
+    const int ni = (int)(q1 - q0);
+    hdr[c] = make_int4((int)it2.size(), ni, (int)ecol.size(), width);
+    for (int64_t q = q0; q < q1; ++q) it2.push_back(make_int2((int)q, -1));
+    const size_t base = ecol.size();
+    ecol.resize(base + (size_t)width * ni, 0);
+    esrc.resize(base + (size_t)width * ni, make_int2(-1, 0));
+    for (int i = 0; i < ni; ++i)
+      for (int sl = 0; sl < (int)ents[i].size(); ++sl) {
+        ecol[base + (size_t)sl * ni + i] = ents[i][sl].x;
+        esrc[base + (size_t)sl * ni + i] = make_int2(ents[i][sl].y, eids[i][sl]);
+      }
+  }
+  if (ecol.empty()) {
+    ecol.push_back(0);
+    esrc.push_back(make_int2(-1, 0));
+  }
+  if (it2.empty()) it2.push_back(make_int2(0, -1));
+  auto pg = std::make_unique<CplProgram>();
+  pg->nent = (int64_t)ecol.size();
+  pg->hdr = upload_vec(hdr, s);
+  pg->items = upload_vec(it2, s);
+  pg->ecol = upload_vec(ecol, s);
+  pg->esrc = upload_vec(esrc, s);
+  pg->ok = true;
+  STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
+  const CplProgram &ref = *pg;
+  sp.prog_cache[key] = std::move(pg);
+  return ref;
+}
+
+void sweep_stage_set_post(SweepStage &st, SweepStage &target, const SweepCoupling *cpl, int ncpl, cudaStream_t s,
+                          int64_t vals_tag) {
+  require(st.sp && target.sp && st.nrhs == target.nrhs, "sweep post program: stages not prepared");
+  require(ncpl <= kMaxCpl, "sweep post program: at most four terms");
+  const std::vector<int> *ext_pos[2] = {nullptr, nullptr};
+  // external sources of the post program are this stage's external stages
+  for (int c = 0; c < ncpl; ++c) require(cpl[c].ext < st.a.nwait, "sweep post program: missing external stage");
+  for (int e = 0; e < st.a.nwait; ++e) ext_pos[e] = st.ext_pos[e];
+  const CplProgram &pg = get_post_program(*st.sp, *target.sp, target.a.n, cpl, ncpl, ext_pos, s);
+  int per_slab = 0;
+  for (int c = 0; c < ncpl; ++c) per_slab |= cpl[c].val_stride != 0;
+  if (!(vals_tag && st.post_tag == vals_tag && st.post_prog == &pg)) {
+    per_slab = gather_values(pg, cpl, ncpl, st.nrhs, st.post_vals, s);
+    st.post_tag = vals_tag;
+    st.post_prog = &pg;
+  }
+  SweepArgs &a = st.a;
+  a.post_hdr = pg.hdr.as<int4>();
+  a.post_items = pg.items.as<int2>();
+  a.post_ecol = pg.ecol.as<int>();
+  a.post_vals = st.post_vals.as<double>();
+  a.post_nent = pg.nent;
+  a.post_per_slab = per_slab;
+  a.post_out = const_cast<double *>(target.a.rhsp);  // target rhsp is its scratch (written here, read after the flag)
+  a.post_n = target.a.n;
 }
 
 void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
@@ -1218,7 +1391,9 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
     }
     attr = true;
   }
-  SweepStage &s0 = *stg[0];
+  static const int trace_stage = env_int2("STMHD_SWEEP_TRACE_STAGE", 0);
+  const int ts = std::min(std::max(trace_stage, 0), nst - 1);
+  SweepStage &s0 = *stg[ts];
   const int64_t n0 = s0.a.n;
   const int nrhs0 = s0.nrhs;
   static const int trace_on = env_int2("STMHD_SWEEP_TRACE", 0);
@@ -1228,13 +1403,13 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
     nsteps = 4 + nrhs0 * (2 * s0.fac->dev->plan->nlevels + 4);
     tr.alloc(nsteps * sizeof(unsigned long long));
     STMHD_CUDA_CHECK(cudaMemsetAsync(tr.ptr, 0, tr.bytes, s));
-    m.st[0].trace = tr.as<unsigned long long>();
+    m.st[ts].trace = tr.as<unsigned long long>();
   }
   static const int prof_on = env_int2("STMHD_SWEEP_PROF", 0);
   DevBuf pr;
   if (prof_on) {
     pr.alloc((size_t)kCluster * kWarps * 8 * sizeof(unsigned long long));
-    m.st[0].prof = pr.as<unsigned long long>();
+    m.st[ts].prof = pr.as<unsigned long long>();
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kCluster * nst);
@@ -1311,7 +1486,7 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   static std::map<const NDDevice *, SweepStagePtr> stages;
   SweepStagePtr &sp = stages[fac.dev];
   if (!sp) sp = sweep_stage_new();
-  sweep_stage_prepare(*sp, fac, rhs, ld_rhs, x, ld_x, nrhs, cpl, ncpl, nullptr, 0, s);
+  sweep_stage_prepare(*sp, fac, rhs, ld_rhs, x, ld_x, nrhs, cpl, ncpl, nullptr, 0, s, 0);
   SweepStage *one = sp.get();
   sweep_stages_launch(&one, 1, s);
 }

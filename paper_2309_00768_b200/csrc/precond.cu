@@ -410,7 +410,11 @@ void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
   }
   SweepCoupling cw[2];
   wave_couplings(cw);
-  sweep_stage_prepare(*st_wave, *ca, ta2.as<double>(), n_a, x + o_a, slab, nt, cw, 2, nullptr, 0, s);
+  // gathered coupling values depend only on this preconditioner's values: reuse them
+  static int64_t next_tag = 0;
+  if (!vals_tag) vals_tag = ++next_tag;
+  const int64_t tag = vals_tag;
+  sweep_stage_prepare(*st_wave, *ca, ta2.as<double>(), n_a, x + o_a, slab, nt, cw, 2, nullptr, 0, s, tag);
   SweepCoupling cj;  // -K_jA x_A
   DCsr mix = d->csr("mixja");
   cj.rowptr = mix.rowptr;
@@ -419,32 +423,34 @@ void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
   cj.ext = 0;
   cj.coef = -1.0;
   SweepStage *wj[1] = {st_wave.get()};
-  sweep_stage_prepare(*st_mj, *d->lu_mj, r_j, slab, x + o_j, slab, nt, &cj, 1, wj, 1, s);
-  SweepCoupling cu[3];
-  DCsr m = d->csr("mu_dt");  // + M_u/dt x_u(k-1)
-  cu[0].rowptr = m.rowptr;
-  cu[0].col = m.col;
-  cu[0].val = m.val;
-  cu[0].lag = 1;
-  cu[0].coef = 1.0;
-  cu[1].rowptr = d->D<int>("js_seg0");  // - Z_j x_j: u rows, z_j segment, slab columns o_j + j
-  cu[1].rowend = d->D<int>("js_seg1");
-  cu[1].col = d->D<int>("js_col");
-  cu[1].col_off = (int)o_j;
-  cu[1].val = js;
-  cu[1].val_stride = nnz_js;
-  cu[1].ext = 0;
-  cu[1].coef = -1.0;
-  cu[2].rowptr = d->D<int>("js_seg1");  // - Z_a x_A: u rows, z_a segment, slab columns o_a + a
-  cu[2].rowend = d->D<int>("js_rowptr") + 1;
-  cu[2].col = d->D<int>("js_col");
-  cu[2].col_off = (int)o_a;
-  cu[2].val = js;
-  cu[2].val_stride = nnz_js;
-  cu[2].ext = 1;
-  cu[2].coef = -1.0;
-  SweepStage *ju[2] = {st_mj.get(), st_wave.get()};
-  sweep_stage_prepare(*st_vel, *fu, tu1.as<double>(), n_u, x, slab, nt, cu, 3, ju, 2, s);
+  sweep_stage_prepare(*st_mj, *d->lu_mj, r_j, slab, x + o_j, slab, nt, &cj, 1, wj, 1, s, tag);
+  SweepCoupling cu;  // + M_u/dt x_u(k-1); waits on the M_j stage (which adds the Z terms)
+  DCsr m = d->csr("mu_dt");
+  cu.rowptr = m.rowptr;
+  cu.col = m.col;
+  cu.val = m.val;
+  cu.lag = 1;
+  cu.coef = 1.0;
+  SweepStage *ju[1] = {st_mj.get()};
+  sweep_stage_prepare(*st_vel, *fu, tu1.as<double>(), n_u, x, slab, nt, &cu, 1, ju, 1, s, tag);
+  // after slab k of the M_j stage: rhs_u(k) += -Z_j x_j(k) - Z_a x_A(k)
+  SweepCoupling cz[2];
+  cz[0].rowptr = d->D<int>("js_seg0");  // z_j segment of the u rows, slab columns o_j + j
+  cz[0].rowend = d->D<int>("js_seg1");
+  cz[0].col = d->D<int>("js_col");
+  cz[0].col_off = (int)o_j;
+  cz[0].val = js;
+  cz[0].val_stride = nnz_js;
+  cz[0].coef = -1.0;                    // source: the M_j stage's own x_j(k)
+  cz[1].rowptr = d->D<int>("js_seg1");  // z_a segment, slab columns o_a + a
+  cz[1].rowend = d->D<int>("js_rowptr") + 1;
+  cz[1].col = d->D<int>("js_col");
+  cz[1].col_off = (int)o_a;
+  cz[1].val = js;
+  cz[1].val_stride = nnz_js;
+  cz[1].ext = 0;                        // source: the wave stage's x_A(k)
+  cz[1].coef = -1.0;
+  sweep_stage_set_post(*st_mj, *st_vel, cz, 2, s, tag);
   SweepStage *all[3] = {st_wave.get(), st_mj.get(), st_vel.get()};
   sweep_stages_launch(all, 3, s);
 }
