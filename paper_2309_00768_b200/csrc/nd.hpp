@@ -100,6 +100,16 @@ struct NDSweepPlan {
   // start of every phase level in it (nl = 2 nsub + 2 ntop levels, nl + 1 bounds)
   int nl = 0, max_wtasks = 0;
   DevBuf wl_tasks, wl_off, wl_bnd;
+  // dense top (dense = 1): after the subtree forward phase the top unknowns are
+  //   x_T = K z_T,  z_T = top rows of the coupled rhs + the subtree roots' updates,
+  // K = (A^{-1})_TT (inverse of the top Schur complement, NDFactor::ktop) -- one GEMV
+  // step instead of 2 * ntop tree levels.  Top unknowns in elimination order.
+  int dense = 0, ntT = 0, kc = 0, nch = 0, kpad = 0;
+  DevBuf ztab;              // int4 x 2 per top unknown {pos, cb0, cb1, cb2}, {cb3, -1, -1, -1}
+  DevBuf tidx;              // n: top index of a permuted position, or -1
+  DevBuf tsn, tchild;       // top supernodes (postorder) and their top children (K construction)
+  int ntsn = 0;
+  int64_t tcb_total = 0;    // sum of nb over top supernodes
   DevBuf g3p;   // int4 per front position: {permuted rhs index or -1, cb1, cb2, 0}
   DevBuf bpos;  // int per front position: permuted position of the front entry
   DevBuf pos;   // n: elimination position of each original index
@@ -123,7 +133,7 @@ struct NDDevice {
   int max_front = 0;
   void build(const NDPlan &p, cudaStream_t s);
   mutable std::unique_ptr<NDSweepPlan> sweep_plan;
-  const NDSweepPlan &get_sweep_plan(int ncta, int warps, int64_t sub_budget, cudaStream_t s, bool flat = false) const;
+  const NDSweepPlan &get_sweep_plan(int ncta, int warps, int64_t sub_budget, cudaStream_t s, int mode = 0) const;
 };
 
 // A coupling term of a sequential block sweep:
@@ -159,6 +169,12 @@ struct NDFactor {
   int nbatch = 0;
   DevBuf factors;  // nbatch * factor_size doubles
   DevBuf status;   // int: 0 ok, 1+ singular (first failing supernode+1)
+  uint64_t gen = 0;  // bumped by every factorisation
+  // dense inverse of the top Schur complement per batch entry (nd_sweep.cu), built
+  // lazily for the sweep plan that uses it: [nbatch][n_T][kpad] doubles
+  mutable DevBuf ktop;
+  mutable const void *ktop_plan = nullptr;
+  mutable uint64_t ktop_gen = ~0ull;
   void factor(const double *values, int64_t value_stride, cudaStream_t s);
   // x_b = A_b^{-1} rhs_b (b < nrhs; factor b, or 0 if nbatch == 1).
   void solve(const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,

@@ -383,6 +383,7 @@ void NDDevice::build(const NDPlan &p, cudaStream_t s) {
 
 void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s) {
   const NDPlan &p = *dev->plan;
+  ++gen;  // invalidates derived data (dense top inverse)
   if (factors.bytes != (size_t)nbatch * p.factor_size * sizeof(double))
     factors.alloc_async((size_t)nbatch * p.factor_size * sizeof(double), s);
   if (!status.ptr) status.alloc(sizeof(int));

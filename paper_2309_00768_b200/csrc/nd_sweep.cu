@@ -19,6 +19,7 @@
 //  * the next slab's factors are bulk-prefetched into L2 while a slab runs;
 //  * couplings are ELL tables in elimination order.
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <map>
 
@@ -31,8 +32,18 @@ static int env_int2(const char *name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
+// Top supernode for the dense-top construction (postorder).
+struct TopSN {
+  int ns, nb, first, goff;  // columns, boundary, first position, front table offset
+  int fl_off, fu_off, rf, rb, bszf, bszb;  // chunk layout of FL (f x ns) and FU (ns x f)
+  int tcb_off;              // offset of its update block in the construction scratch
+  int nchild, child0;       // top children in tchild[child0 .. child0 + nchild)
+  int pad[3];
+};
+
 const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_budget, cudaStream_t s,
-                                            bool flat) const {
+                                            int mode) const {
+  const bool flat = mode >= 2;  // 0: subtrees + dense top, 1: subtrees only, 2: all levels cluster-wide
   if (sweep_plan && sweep_plan->ncta == ncta && sweep_plan->warps == warps) return *sweep_plan;
   const NDPlan &p = *plan;
   auto sp = std::make_unique<NDSweepPlan>();
@@ -230,6 +241,50 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
   sp->nsub = roots.empty() ? 0 : nsub;
   sp->sub_len = maxlen;
   sp->sub_cb = maxcb;
+  // ---- dense top: one GEMV with K = (A^{-1})_TT replaces the top tree levels ----
+  static const int dense_env = env_int2("STMHD_SWEEP_DENSE_TOP", 1);
+  std::vector<int> tpos, tidx_h(p.n, -1);
+  std::vector<int4> ztab;
+  if (dense_env && mode == 0 && sp->nsub > 0 && ntop > 0) {
+    for (int sn = 0; sn < p.nsn; ++sn)  // top unknowns in elimination order
+      if (owner[sn] < 0)
+        for (int t = 0; t < p.ns[sn]; ++t) {
+          const int q = (int)(p.first[sn] + t);
+          tidx_h[q] = (int)tpos.size();
+          tpos.push_back(q);
+        }
+    const int nT = (int)tpos.size();
+    std::vector<std::array<int, 4>> zc(nT, {-1, -1, -1, -1});
+    bool ok = nT > 0 && nT <= 4096;
+    for (int r : roots) {  // subtree roots' updates land on top unknowns
+      for (int a = 0; a < p.nb[r] && ok; ++a) {
+        const int tgt = bpos[p.idx_off[r] + p.ns[r] + a];
+        const int i = tgt >= 0 ? tidx_h[tgt] : -1;
+        if (i < 0) {
+          ok = false;
+          break;
+        }
+        int sl = 0;
+        while (sl < 4 && zc[i][sl] >= 0) ++sl;
+        if (sl == 4) {
+          ok = false;
+          break;
+        }
+        zc[i][sl] = (int)(p.cbv_off[r] + a);
+      }
+    }
+    if (ok) {
+      sp->dense = 1;
+      sp->ntT = nT;
+      sp->nch = (nT + 639) / 640;
+      sp->kc = ((nT + sp->nch - 1) / sp->nch + 1) / 2 * 2;  // even: 16-byte aligned chunks
+      sp->kpad = sp->nch * sp->kc;
+      for (int i = 0; i < nT; ++i) {
+        ztab.push_back(make_int4(tpos[i], zc[i][0], zc[i][1], zc[i][2]));
+        ztab.push_back(make_int4(zc[i][3], -1, -1, -1));
+      }
+    }
+  }
   // per direction: top tasks per [top level][global warp], subtree tasks per
   // [cta][local level][warp]
   std::vector<std::vector<SweepTask>> top_t[2], sub_t[2];
@@ -273,7 +328,27 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
   build_dir(false);
   // per physical warp (cta c, warp w; top-phase global warp id w * ncta + c): its
   // list in kernel order and the bound of every phase level
-  sp->nl = 2 * sp->nsub + 2 * sp->ntop;
+  // dense top: one phase level of row tasks (row i of K: nch column chunks of kc)
+  std::vector<std::vector<SweepTask>> dense_t(W);
+  if (sp->dense) {
+    for (int i = 0; i < sp->ntT; ++i) {
+      SweepTask t{};
+      t.foff = i * sp->kpad;
+      t.goff = 0;
+      t.first = tpos[i];
+      t.cboff = 0;
+      t.c0 = 0;
+      t.c1 = (short)sp->nch;
+      t.ns = (short)sp->kc;
+      t.f = (short)sp->kc;
+      t.rows = 1;
+      t.R = 1;
+      t.flags = 2;
+      t.bsz = sp->kc;
+      dense_t[i % W].push_back(t);
+    }
+  }
+  sp->nl = 2 * sp->nsub + (sp->dense ? 1 : 2 * sp->ntop);
   {
     std::vector<SweepTask> all;
     std::vector<int> off, bnd;
@@ -287,8 +362,12 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
           all.insert(all.end(), v.begin(), v.end());
         };
         for (int h = 0; h < sp->nsub; ++h) add(sub_t[1][((size_t)c * sp->nsub + h) * warps + w]);
-        for (int t = 0; t < sp->ntop; ++t) add(top_t[1][(size_t)t * W + w * ncta + c]);
-        for (int t = sp->ntop - 1; t >= 0; --t) add(top_t[0][(size_t)t * W + w * ncta + c]);
+        if (sp->dense) {
+          add(dense_t[w * ncta + c]);
+        } else {
+          for (int t = 0; t < sp->ntop; ++t) add(top_t[1][(size_t)t * W + w * ncta + c]);
+          for (int t = sp->ntop - 1; t >= 0; --t) add(top_t[0][(size_t)t * W + w * ncta + c]);
+        }
         for (int h = sp->nsub - 1; h >= 0; --h) add(sub_t[0][((size_t)c * sp->nsub + h) * warps + w]);
         bnd.push_back((int)(all.size() - o));
         maxw = std::max(maxw, (int)(all.size() - o));
@@ -310,12 +389,54 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
     // shared memory: subtree vectors + per-warp task lists must fit next to the
     // per-warp gather buffers; otherwise fall back to an all-top schedule
     const int64_t tdoubles = (int64_t)warps * (((sp->nl + 1 + 3) / 4) * 16 + (int64_t)maxw * 32) / 8;
-    if (!flat && D > 0 && 3 * maxlen + maxcb + tdoubles > sub_budget) return get_sweep_plan(ncta, warps, sub_budget, s, true);
+    if (!flat && D > 0 && 3 * maxlen + maxcb + tdoubles + sp->kpad + 2 > sub_budget)
+      return get_sweep_plan(ncta, warps, sub_budget, s, sp->dense ? 1 : 2);
     sp->wl_tasks = upload_vec(all, s);
     sp->wl_off = upload_vec(off, s);
     sp->wl_bnd = upload_vec(bnd, s);
   }
   sp->sub_info = upload_vec(info, s);
+  if (sp->dense) {
+    sp->ztab = upload_vec(ztab, s);
+    sp->tidx = upload_vec(tidx_h, s);
+    std::vector<int> tsn_index(p.nsn, -1);
+    std::vector<TopSN> tsn;
+    std::vector<int4> tch;
+    int64_t tcb = 0;
+    for (int sn = 0; sn < p.nsn; ++sn) {
+      if (owner[sn] >= 0) continue;
+      require(p.fl_off[sn] < INT32_MAX && p.fu_off[sn] < INT32_MAX && p.idx_off[sn] < INT32_MAX,
+              "nd sweep: factor too large for the dense-top construction");
+      TopSN t{};
+      t.ns = p.ns[sn];
+      t.nb = p.nb[sn];
+      t.first = (int)p.first[sn];
+      t.goff = (int)p.idx_off[sn];
+      t.fl_off = (int)p.fl_off[sn];
+      t.fu_off = (int)p.fu_off[sn];
+      t.rf = p.rf[sn];
+      t.rb = p.rb[sn];
+      t.bszf = (int)p.bsz_f[sn];
+      t.bszb = (int)p.bsz_b[sn];
+      t.tcb_off = (int)tcb;
+      tcb += p.nb[sn];
+      t.child0 = (int)tch.size();
+      for (int ci = p.child_ptr[sn]; ci < p.child_ptr[sn + 1]; ++ci) {
+        const int c = p.child_list[ci];
+        if (owner[c] >= 0) continue;  // subtree roots: their updates are inputs (z_T)
+        require(tsn_index[c] >= 0, "nd sweep: top tree not in postorder");
+        tch.push_back(make_int4(tsn_index[c], (int)p.emap_off[c], p.nb[c], 0));
+      }
+      t.nchild = (int)tch.size() - t.child0;
+      tsn_index[sn] = (int)tsn.size();
+      tsn.push_back(t);
+    }
+    if (tch.empty()) tch.push_back(make_int4(0, 0, 0, 0));
+    sp->ntsn = (int)tsn.size();
+    sp->tcb_total = tcb;
+    sp->tsn = upload_vec(tsn, s);
+    sp->tchild = upload_vec(tch, s);
+  }
   sp->sub_info_h = info;
   sp->pos_h = pos;
   sp->iperm_h = iperm;
@@ -344,6 +465,11 @@ struct SweepArgs {
   int64_t prog_nent;
   int prog_per_slab;
   double *tbuf;                // coupled right-hand side of the top rows
+  // dense top (NDSweepPlan::dense): z_T gather table and K = (A^{-1})_TT per slab
+  int dense, ntT, kpad;
+  const int4 *ztab;
+  const double *ktop;
+  int64_t kstride;             // doubles per slab of ktop (0: one K for all slabs)
   // post-slab program (pipelined launch): after slab k, post_out[k] += C x(k)
   const int4 *post_hdr;
   const int2 *post_items;
@@ -443,6 +569,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
 // Per-CTA view of the subtree vectors kept in shared memory.
 struct SubView {
   double *ys, *xs, *cbs, *rhs_s;  // rhs_s: coupled right-hand side of the subtree rows (fused mode)
+  double *zs;                     // dense top: z_T (kpad doubles)
   int64_t first, len, cbfirst;
 };
 
@@ -474,8 +601,9 @@ __device__ __forceinline__ void ring_issue(const SweepArgs &a, WarpCtx &w, unsig
   if (w.rslab < a.nslab && w.nt > 0) {
     const SweepTask &t = w.tl[w.rt];
     const int sl = w.icount & 1;
-    tma_load(w.slot0 + sl * w.slotsz, a.factors + (int64_t)w.rslab * a.fstride + t.foff + (int64_t)w.rc * t.bsz,
-             t.bsz, &mbar[w.wl][sl]);
+    const double *base = (t.flags & 2) ? a.ktop + (int64_t)w.rslab * a.kstride  // dense-top row chunk
+                                       : a.factors + (int64_t)w.rslab * a.fstride;
+    tma_load(w.slot0 + sl * w.slotsz, base + t.foff + (int64_t)w.rc * t.bsz, t.bsz, &mbar[w.wl][sl]);
     ++w.icount;
     if (++w.rc == t.c1) {
       if (++w.rt == w.nt) {
@@ -647,6 +775,28 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
   __syncwarp();
 }
 
+// Dense-top row task: x[first] = K[row] . z_T, the row streamed as nch column chunks
+// of kc doubles through the warp's TMA ring (R = 1: lane k covers columns k + 32 q).
+template <bool PROF>
+__device__ __forceinline__ void dense_task(const SweepArgs &a, const SweepTask &tk, const double *zs, double *x,
+                                           WarpCtx &w, unsigned long long (*mbar)[2]) {
+  const int lane = w.lane;
+  double acc = 0.0;
+  for (int c = tk.c0; c < tk.c1; ++c) {
+    const int sl = w.jc & 1;
+    mbar_wait(&mbar[w.wl][sl], (unsigned)(w.jc >> 1) & 1u);
+    acc += chunk_gemv_smem(w.slot0 + sl * w.slotsz, tk.ns, 32, lane, 1, zs + (int64_t)c * tk.ns, lane);
+    __syncwarp();
+    ++w.jc;
+    if (lane == 0) ring_issue(a, w, mbar);
+  }
+  if (PROF) {
+    w.acc[4] += 1;
+    w.acc[5] += tk.c1 - tk.c0;
+  }
+  if (lane == 0) x[tk.first] = acc;
+}
+
 // Run this CTA's items of a coupling program.  MODE 0 (slab start): rhs rows, item
 // dst kind 0 -> the subtree's shared rhs_s, kind 1 -> tbuf.  MODE 1 (after a slab):
 // out[dst] += sum, the rows of another stage's right-hand side.  srcs: source table.
@@ -773,6 +923,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   sv.xs = sv.ys + a.sub_len;
   sv.cbs = sv.xs + a.sub_len;
   sv.rhs_s = sv.cbs + a.sub_cb;
+  sv.zs = sv.rhs_s + a.sub_len;
   sv.first = a.sub_info[4 * crank + 0];
   sv.len = a.sub_info[4 * crank + 1];
   sv.cbfirst = a.sub_info[4 * crank + 2];
@@ -780,7 +931,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     // copy this warp's task list and level bounds into shared memory (static for
     // the whole sweep: no global round trip per level or task afterwards)
     const int gid = crank * a.warps + wl;
-    const uintptr_t base = (reinterpret_cast<uintptr_t>(sv.rhs_s + a.sub_len) + 15) & ~(uintptr_t)15;
+    const uintptr_t base = (reinterpret_cast<uintptr_t>(sv.zs + a.kpad) + 15) & ~(uintptr_t)15;
     char *area = reinterpret_cast<char *>(base) + (size_t)wl * a.tstride;
     int *bnd = reinterpret_cast<int *>(area);
     SweepTask *tl = reinterpret_cast<SweepTask *>(area + ((a.nl + 1 + 3) / 4) * 16);
@@ -855,21 +1006,44 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step);
     }
-    for (int t = 0; t < a.ntop; ++t, ++L) {
-      const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
-      for (int ti = w.bnd[L]; ti < t1; ++ti) forward_task<false, PROF>(a, w.tl[ti], F, rhs, sv, w, mbar);
-      tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
-      sweep_trace(a, step);
-    }
-    for (int t = a.ntop - 1; t >= 0; --t, ++L) {
-      const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
-      for (int ti = w.bnd[L]; ti < t1; ++ti) backward_task<false, PROF>(a, w.tl[ti], F, x, sv, w, mbar);
-      if (t > 0 || a.nsub || k + 1 < a.nslab) {
-        tb = pclock<PROF>();
-        sweep_barrier();
-        if (PROF) w.acc[3] += pclock<PROF>() - tb;
+    if (a.dense) {
+      // z_T = coupled rhs of the top unknowns + the subtree roots' updates (all CTAs
+      // gather the whole vector), then x_T = K z_T as row tasks
+      const double *rt = a.prog_hdr ? a.tbuf : rhs;
+      for (int i = threadIdx.x; i < a.kpad; i += blockDim.x) {
+        double z = 0.0;
+        if (i < a.ntT) {
+          const int4 t0 = a.ztab[2 * i], t1 = a.ztab[2 * i + 1];
+          const double r0 = rt[t0.x];
+          const double c0 = t0.y >= 0 ? a.cbv[t0.y] : 0.0, c1 = t0.z >= 0 ? a.cbv[t0.z] : 0.0;
+          const double c2 = t0.w >= 0 ? a.cbv[t0.w] : 0.0, c3 = t1.x >= 0 ? a.cbv[t1.x] : 0.0;
+          z = r0 + ((c0 + c1) + (c2 + c3));
+        }
+        sv.zs[i] = z;
       }
+      tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+      const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
+      for (int ti = w.bnd[L]; ti < t1; ++ti) dense_task<PROF>(a, w.tl[ti], sv.zs, x, w, mbar);
+      ++L;
+      tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;  // x_T visible
       sweep_trace(a, step);
+    } else {
+      for (int t = 0; t < a.ntop; ++t, ++L) {
+        const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
+        for (int ti = w.bnd[L]; ti < t1; ++ti) forward_task<false, PROF>(a, w.tl[ti], F, rhs, sv, w, mbar);
+        tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+        sweep_trace(a, step);
+      }
+      for (int t = a.ntop - 1; t >= 0; --t, ++L) {
+        const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
+        for (int ti = w.bnd[L]; ti < t1; ++ti) backward_task<false, PROF>(a, w.tl[ti], F, x, sv, w, mbar);
+        if (t > 0 || a.nsub || k + 1 < a.nslab) {
+          tb = pclock<PROF>();
+          sweep_barrier();
+          if (PROF) w.acc[3] += pclock<PROF>() - tb;
+        }
+        sweep_trace(a, step);
+      }
     }
     for (int h = a.nsub - 1; h >= 0; --h, ++L) {
       const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
@@ -1074,6 +1248,117 @@ __global__ void cpl_vals_kernel(const int2 *esrc, int64_t nent, CplVals cv, int 
 }
 
 // ---------------------------------------------------------------------------
+// Dense top operator K = (A^{-1})_TT, one per batch entry: push 32 identity columns
+// at a time through the top supernodes' forward (FL) and backward (FU) factors --
+// exactly the operations of the sweep's top levels, applied to a block of
+// right-hand sides.  Warp per row, lane per column; fronts staged in shared memory.
+struct TopKArgs {
+  const TopSN *tsn;
+  const int4 *tchild;
+  const int *emap, *tidx, *bpos;
+  const double *factors;
+  int64_t fstride;
+  int ntsn, nT, kpad, nbatch, ncb;
+  double *scratch;    // per CTA: Xw (nT x 32) | CBw (tcb_total x 32)
+  int64_t scr_stride;
+  double *K;          // [nbatch][nT][kpad]
+  int64_t kstride;
+};
+
+__global__ void __launch_bounds__(256) topk_kernel(TopKArgs g) {
+  extern __shared__ __align__(16) double V[];  // front x 32
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double *Xw = g.scratch + (int64_t)blockIdx.x * g.scr_stride;
+  double *CBw = Xw + (int64_t)g.nT * 32;
+  const int nitems = g.nbatch * g.ncb;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int b = item / g.ncb, col = (item % g.ncb) * 32 + lane;
+    const double *F = g.factors + (int64_t)b * g.fstride;
+    for (int si = 0; si < g.ntsn; ++si) {  // forward, postorder
+      const TopSN t = g.tsn[si];
+      const int f = t.ns + t.nb;
+      for (int r = wl; r < f; r += nw) V[r * 32 + lane] = (r < t.ns && g.tidx[t.first + r] == col) ? 1.0 : 0.0;
+      __syncthreads();
+      for (int c = 0; c < t.nchild; ++c) {  // extend-add the top children's updates
+        const int4 ch = g.tchild[t.child0 + c];
+        const int cb0 = g.tsn[ch.x].tcb_off;
+        for (int a = wl; a < ch.z; a += nw) V[g.emap[ch.y + a] * 32 + lane] += CBw[(int64_t)(cb0 + a) * 32 + lane];
+        __syncthreads();
+      }
+      for (int r = wl; r < f; r += nw) {
+        const double *row = F + t.fl_off + (int64_t)(r / t.rf) * t.bszf + (r % t.rf);
+        double acc = 0.0;
+        for (int k = 0; k < t.ns; ++k) acc = fma(__ldg(row + (int64_t)k * t.rf), V[k * 32 + lane], acc);
+        if (r < t.ns) Xw[(int64_t)g.tidx[t.first + r] * 32 + lane] = acc;  // y
+        else CBw[(int64_t)(t.tcb_off + r - t.ns) * 32 + lane] = V[r * 32 + lane] - acc;
+      }
+      __syncthreads();
+    }
+    for (int si = g.ntsn - 1; si >= 0; --si) {  // backward, reverse postorder
+      const TopSN t = g.tsn[si];
+      const int f = t.ns + t.nb;
+      for (int r = wl; r < f; r += nw) {
+        const int pos = r < t.ns ? t.first + r : g.bpos[t.goff + r];
+        V[r * 32 + lane] = Xw[(int64_t)g.tidx[pos] * 32 + lane];  // own y, or the ancestors' x
+      }
+      __syncthreads();
+      for (int k = wl; k < t.ns; k += nw) {
+        const double *row = F + t.fu_off + (int64_t)(k / t.rb) * t.bszb + (k % t.rb);
+        double acc = 0.0;
+        for (int r = 0; r < f; ++r) acc = fma(__ldg(row + (int64_t)r * t.rb), V[r * 32 + lane], acc);
+        Xw[(int64_t)g.tidx[t.first + k] * 32 + lane] = acc;
+      }
+      __syncthreads();
+    }
+    if (col < g.nT)
+      for (int i = wl; i < g.nT; i += nw) g.K[(int64_t)b * g.kstride + (int64_t)i * g.kpad + col] = Xw[(int64_t)i * 32 + lane];
+    __syncthreads();
+  }
+}
+
+static void build_dense_top(const NDFactor &fac, const NDSweepPlan &sp, cudaStream_t s) {
+  const NDPlan &p = *fac.dev->plan;
+  const int64_t kstride = (int64_t)sp.ntT * sp.kpad;
+  const size_t kbytes = (size_t)fac.nbatch * kstride * sizeof(double);
+  if (fac.ktop.bytes != kbytes) fac.ktop.alloc_async(kbytes, s);
+  STMHD_CUDA_CHECK(cudaMemsetAsync(fac.ktop.ptr, 0, kbytes, s));  // padded columns stay zero
+  int fmax = 1;
+  for (int sn = 0; sn < p.nsn; ++sn) fmax = std::max(fmax, p.ns[sn] + p.nb[sn]);
+  TopKArgs g{};
+  g.tsn = sp.tsn.as<TopSN>();
+  g.tchild = sp.tchild.as<int4>();
+  g.emap = fac.dev->emap.as<int>();
+  g.tidx = sp.tidx.as<int>();
+  g.bpos = sp.bpos.as<int>();
+  g.factors = fac.factors.as<double>();
+  g.fstride = fac.nbatch == 1 ? 0 : p.factor_size;
+  g.ntsn = sp.ntsn;
+  g.nT = sp.ntT;
+  g.kpad = sp.kpad;
+  g.nbatch = fac.nbatch;
+  g.ncb = (sp.ntT + 31) / 32;
+  const int nitems = g.nbatch * g.ncb;
+  const int grid = std::max(1, std::min(nitems, 2 * num_sms()));
+  g.scr_stride = (int64_t)(sp.ntT + sp.tcb_total) * 32;
+  DevBuf scr;
+  scr.alloc_async((size_t)grid * g.scr_stride * sizeof(double), s);
+  g.scratch = scr.as<double>();
+  g.K = fac.ktop.as<double>();
+  g.kstride = kstride;
+  const size_t smem = (size_t)fmax * 32 * sizeof(double);
+  require(smem <= 200 * 1024, "dense top: front too large");
+  static size_t attr = 0;
+  if (smem > attr) {
+    STMHD_CUDA_CHECK(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  topk_kernel<<<grid, 256, smem, s>>>(g);
+  STMHD_LAUNCH_CHECK();
+  fac.ktop_plan = &sp;
+  fac.ktop_gen = fac.gen;
+}
+
+// ---------------------------------------------------------------------------
 // Stages
 
 struct SweepStage {
@@ -1214,11 +1499,21 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
     a.prog_per_slab = per_slab;
     a.tbuf = tbuf;
   }
+  a.dense = sp.dense;
+  a.ntT = sp.ntT;
+  a.kpad = sp.kpad;
+  if (sp.dense) {
+    if (fac.ktop_plan != &sp || fac.ktop_gen != fac.gen) build_dense_top(fac, sp, s);
+    a.ztab = sp.ztab.as<int4>();
+    a.ktop = fac.ktop.as<double>();
+    a.kstride = fac.nbatch == 1 ? 0 : (int64_t)sp.ntT * sp.kpad;
+  }
   a.slot = slot;
   a.vstride = vstride;
   a.null_work = env_int2("STMHD_SWEEP_NULL", 0);
   a.post_hdr = nullptr;  // set by sweep_stage_set_post for this launch
-  st.smem = ((size_t)warps * a.vstride + 3 * a.sub_len + a.sub_cb + 1) * sizeof(double) + (size_t)warps * a.tstride;
+  st.smem = ((size_t)warps * a.vstride + 3 * a.sub_len + a.sub_cb + a.kpad + 2) * sizeof(double) +
+            (size_t)warps * a.tstride;
   require(st.smem <= 224 * 1024, "nd sweep: subtree vectors or fronts too large for shared memory");
   // consumers wait on their producers' flags (set at launch)
   a.nwait = next;
@@ -1448,7 +1743,7 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
     STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
     const bool fz = a.prog_hdr != nullptr;
     auto entries = [&](int k) {
-      return (int)fz + ((a.nsub || fz) ? 1 : 0) + 2 * a.ntop + (a.nsub && k + 1 < a.nslab);
+      return (int)fz + ((a.nsub || fz) ? 1 : 0) + (a.dense ? 1 : 2 * a.ntop) + (a.nsub && k + 1 < a.nslab);
     };
     const int per = entries(1), base = 1 + entries(0);
     fprintf(stderr, "[sweep] n=%lld levels=%d top=%d sub=%d fused=%d stages=%d total=%.1f us | slab1 (us):",
