@@ -71,7 +71,8 @@ struct alignas(16) SweepTask {
   short c0, c1;         // chunk range
   short ns, f, rows;    // columns, front size, rows of the step (f forward, ns backward)
   unsigned char R;      // rows per chunk (power of two <= 32)
-  unsigned char flags;  // 1 = write the update vector to global memory
+  unsigned char flags;  // 1: update vector to global memory; 4: front table rides in the ring first
+                        // (8: backward table = aligned bpos at cboff, else forward g3 at goff); 2: dense top row
   int bsz;              // doubles per chunk block
 };
 static_assert(sizeof(SweepTask) == 32, "SweepTask must stay 32 bytes");
@@ -112,6 +113,7 @@ struct NDSweepPlan {
   int64_t tcb_total = 0;    // sum of nb over top supernodes
   DevBuf g3p;   // int4 per front position: {permuted rhs index or -1, cb1, cb2, 0}
   DevBuf bpos;  // int per front position: permuted position of the front entry
+  DevBuf bpos4; // bpos per supernode, each block 16-byte aligned (TMA ring table items)
   DevBuf pos;   // n: elimination position of each original index
   DevBuf iperm; // n: original index at each elimination position
     std::vector<int64_t> sub_info_h;  // host copy of sub_info

@@ -167,6 +167,21 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
     x = {sn, rows, K, R, (rows + R - 1) / R, 2.0, 1.0 + (double)((K + 16 * (32 / R) - 1) / (16 * (32 / R)))};
     return true;
   };
+  // front tables as TMA ring items: forward g3 (int4 per entry, 16-byte aligned at
+  // idx_off) and a 16-byte aligned copy of bpos per supernode; a table rides in the
+  // ring ahead of its task's chunks when it fits a slot (slot = largest chunk block)
+  int64_t slot_dbl = 2;
+  for (int sn = 0; sn < p.nsn; ++sn) slot_dbl = std::max({slot_dbl, p.bsz_f[sn], p.bsz_b[sn]});
+  slot_dbl = (slot_dbl + 15) / 16 * 16;
+  static const int tables_env = env_int2("STMHD_SWEEP_TABLES", 1);
+  std::vector<int> boff(p.nsn), bpos4;
+  for (int sn = 0; sn < p.nsn; ++sn) {
+    const int f = p.ns[sn] + p.nb[sn];
+    boff[sn] = (int)bpos4.size();
+    bpos4.insert(bpos4.end(), bpos.begin() + p.idx_off[sn], bpos.begin() + p.idx_off[sn] + f);
+    while (bpos4.size() % 4) bpos4.push_back(0);
+  }
+  if (bpos4.empty()) bpos4.push_back(0);
   auto make_task = [&](const SN &x, int c0, int c1, bool fwd, bool cb_global) {
     const int64_t foff = fwd ? p.fl_off[x.s] : p.fu_off[x.s];
     const int f = p.ns[x.s] + p.nb[x.s];
@@ -186,6 +201,9 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
     t.R = (unsigned char)x.R;
     t.flags = cb_global ? 1 : 0;
     t.bsz = (int)(fwd ? p.bsz_f[x.s] : p.bsz_b[x.s]);
+    const int64_t tbl_dbl = fwd ? 2LL * f : ((int64_t)f + 3) / 4 * 2;  // table size in doubles
+    if (tables_env && tbl_dbl <= slot_dbl) t.flags |= fwd ? 4 : (4 | 8);
+    if (!fwd) t.cboff = boff[x.s];  // backward tasks: offset of the aligned bpos copy
     return t;
   };
   // LPT of a set of supernodes onto `nw` warps; pieces split big supernodes
@@ -442,6 +460,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
   sp->iperm_h = iperm;
   sp->g3p = upload_vec(g3, s);
   sp->bpos = upload_vec(bpos, s);
+  sp->bpos4 = upload_vec(bpos4, s);
   sp->pos = upload_vec(pos, s);
   sp->iperm = upload_vec(iperm, s);
   STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -480,6 +499,7 @@ struct SweepArgs {
   double *post_out;            // another stage's permuted right-hand sides (nslab x post_n)
   const int4 *g3p;
   const int *bpos;
+  const int *bpos4;            // 16-byte aligned bpos copy (ring table items)
   int nlevels, nw;
   int64_t n;
   const double *factors;
@@ -501,6 +521,7 @@ struct SweepArgs {
   int null_work;  // diagnostics: skip all task work (barrier/loop floor)
   unsigned long long *trace;
   unsigned long long *prof;  // PROF instantiation: 6 counters per warp
+  unsigned long long *tline; // PROF instantiation: per-warp event timeline of slab 1, CTA 0 (128 per warp)
 };
 
 __device__ __forceinline__ void sweep_barrier() {
@@ -546,7 +567,9 @@ __device__ __forceinline__ unsigned smem_u32(const void *p) {
 // one lane: stream `dbl` doubles from global `src` into shared `dst`, completing on `bar`
 __device__ __forceinline__ void tma_load(double *dst, const double *src, int dbl, unsigned long long *bar) {
   const unsigned bytes = (unsigned)dbl * 8u;
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  // no cross-proxy fence: the slot's previous contents were only READ through the
+  // generic proxy, and those loads completed (their values were consumed before the
+  // __syncwarp that precedes every issue)
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
@@ -586,7 +609,17 @@ struct WarpCtx {
   int icount, rt, rc, rslab;    // TMA ring cursor (lane 0): two chunks ahead of jc
   // PROF instantiation: cycles in gather / TMA wait / GEMV+store / barriers, tasks, chunks
   long long acc[8];
+  unsigned long long *tl_out;  // timeline (PROF, slab 1 of CTA 0) or null
+  int tl_n;
 };
+
+__device__ __forceinline__ void tl_mark(WarpCtx &w, unsigned code) {
+  if (w.tl_out && w.lane == 0 && w.tl_n < 128) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    w.tl_out[w.tl_n++] = ((unsigned long long)code << 56) | (t & ((1ull << 56) - 1));
+  }
+}
 
 template <bool PROF>
 __device__ __forceinline__ long long pclock() {
@@ -594,24 +627,50 @@ __device__ __forceinline__ long long pclock() {
   else return 0;
 }
 
-// Issue the next chunk of the warp's chunk sequence into the free slot (lane 0).
-// The ring runs across task, level and slab boundaries (factors do not depend on
-// the data), so a warp's next chunks are in flight while it waits at a barrier.
+// First ring item of a task: its front table (flags & 4) or its first chunk.
+__device__ __forceinline__ int first_item(const SweepTask &t) { return (t.flags & 4) ? t.c0 - 1 : t.c0; }
+
+// Global source and size (doubles) of ring item (task t, index c, slab) -- the
+// task's front table (c < c0) or one of its chunks.
+__device__ __forceinline__ const double *item_src(const SweepArgs &a, const SweepTask &t, int c, int slab,
+                                                  int &dbl) {
+  if (c < t.c0) {
+    if (t.flags & 8) {
+      dbl = (t.f + 3) / 4 * 2;
+      return reinterpret_cast<const double *>(a.bpos4 + t.cboff);
+    }
+    dbl = 2 * t.f;
+    return reinterpret_cast<const double *>(a.g3p + t.goff);
+  }
+  dbl = t.bsz;
+  const double *base = (t.flags & 2) ? a.ktop + (int64_t)slab * a.kstride  // dense-top row chunk
+                                     : a.factors + (int64_t)slab * a.fstride;
+  return base + t.foff + (int64_t)c * t.bsz;
+}
+
+// Advance a (task, item, slab) cursor along the warp's item sequence.
+__device__ __forceinline__ void item_next(const WarpCtx &w, int &t, int &c, int &slab) {
+  if (++c == w.tl[t].c1) {
+    if (++t == w.nt) {
+      t = 0;
+      ++slab;
+    }
+    c = first_item(w.tl[t]);
+  }
+}
+
+// Issue the next item of the warp's sequence into the free slot (lane 0).  The ring
+// runs across task, level and slab boundaries (factors do not depend on the data),
+// so a warp's next items are in flight while it waits at a barrier.  (An L2 bulk
+// prefetch cursor further ahead along the same sequence was measured slower.)
 __device__ __forceinline__ void ring_issue(const SweepArgs &a, WarpCtx &w, unsigned long long (*mbar)[2]) {
   if (w.rslab < a.nslab && w.nt > 0) {
-    const SweepTask &t = w.tl[w.rt];
     const int sl = w.icount & 1;
-    const double *base = (t.flags & 2) ? a.ktop + (int64_t)w.rslab * a.kstride  // dense-top row chunk
-                                       : a.factors + (int64_t)w.rslab * a.fstride;
-    tma_load(w.slot0 + sl * w.slotsz, base + t.foff + (int64_t)w.rc * t.bsz, t.bsz, &mbar[w.wl][sl]);
+    int dbl;
+    const double *src = item_src(a, w.tl[w.rt], w.rc, w.rslab, dbl);
+    tma_load(w.slot0 + sl * w.slotsz, src, dbl, &mbar[w.wl][sl]);
     ++w.icount;
-    if (++w.rc == t.c1) {
-      if (++w.rt == w.nt) {
-        w.rt = 0;
-        ++w.rslab;
-      }
-      w.rc = w.tl[w.rt].c0;
-    }
+    item_next(w, w.rt, w.rc, w.rslab);
   }
 }
 
@@ -645,6 +704,10 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
   const int lane = w.lane;
   long long t0 = pclock<PROF>();
   const int4 *g = a.g3p + tk.goff;
+  if (tk.flags & 4) {  // front table arrived through the ring
+    mbar_wait(&mbar[w.wl][w.jc & 1], (unsigned)(w.jc >> 1) & 1u);
+    g = reinterpret_cast<const int4 *>(w.slot0 + (w.jc & 1) * w.slotsz);
+  }
   const double *cbsrc = SUB ? sv.cbs - sv.cbfirst : a.cbv;
   // fused coupling: subtree rows come from shared memory, top rows from tbuf
   const bool fused = a.prog_hdr != nullptr;
@@ -652,7 +715,7 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
   for (int b0 = lane; b0 < tk.f; b0 += 256) {
     int4 gg[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) gg[q] = (b0 + 32 * q < tk.f) ? __ldg(g + b0 + 32 * q) : make_int4(-1, -1, -1, 0);
+    for (int q = 0; q < 8; ++q) gg[q] = (b0 + 32 * q < tk.f) ? g[b0 + 32 * q] : make_int4(-1, -1, -1, 0);
     double vv[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q)
@@ -663,6 +726,11 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
       if (b0 + 32 * q < tk.f) w.v[b0 + 32 * q] = vv[q];
   }
   __syncwarp();
+  if (PROF) tl_mark(w, 2);
+  if (tk.flags & 4) {  // table consumed: its slot goes back to the ring
+    ++w.jc;
+    if (lane == 0) ring_issue(a, w, mbar);
+  }
   if (PROF) {
     const long long t1 = pclock<PROF>();
     w.acc[0] += t1 - t0;
@@ -700,6 +768,7 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
       const long long t1 = pclock<PROF>();
       w.acc[2] += t1 - t0;
       t0 = t1;
+      tl_mark(w, 3);
     }
   }
   __syncwarp();
@@ -712,13 +781,17 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
   const int lane = w.lane;
   long long t0 = pclock<PROF>();
   const int *bp = a.bpos + tk.goff;
+  if (tk.flags & 4) {  // front table arrived through the ring
+    mbar_wait(&mbar[w.wl][w.jc & 1], (unsigned)(w.jc >> 1) & 1u);
+    bp = reinterpret_cast<const int *>(w.slot0 + (w.jc & 1) * w.slotsz);
+  }
   const double *y = (SUB ? sv.ys - sv.first : a.ybuf) + tk.first;
   for (int b0 = lane; b0 < tk.f; b0 += 256) {
     int ii[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int t = b0 + 32 * q;
-      ii[q] = (t >= tk.ns && t < tk.f) ? __ldg(bp + t) : -1;
+      ii[q] = (t >= tk.ns && t < tk.f) ? bp[t] : -1;
     }
     double vv[8];
 #pragma unroll
@@ -735,6 +808,11 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
       if (b0 + 32 * q < tk.f) w.v[b0 + 32 * q] = vv[q];
   }
   __syncwarp();
+  if (PROF) tl_mark(w, 2);
+  if (tk.flags & 4) {
+    ++w.jc;
+    if (lane == 0) ring_issue(a, w, mbar);
+  }
   if (PROF) {
     const long long t1 = pclock<PROF>();
     w.acc[0] += t1 - t0;
@@ -770,6 +848,7 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
       const long long t1 = pclock<PROF>();
       w.acc[2] += t1 - t0;
       t0 = t1;
+      tl_mark(w, 3);
     }
   }
   __syncwarp();
@@ -779,7 +858,7 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
 // of kc doubles through the warp's TMA ring (R = 1: lane k covers columns k + 32 q).
 template <bool PROF>
 __device__ __forceinline__ void dense_task(const SweepArgs &a, const SweepTask &tk, const double *zs, double *x,
-                                           WarpCtx &w, unsigned long long (*mbar)[2]) {
+                                           int k, WarpCtx &w, unsigned long long (*mbar)[2]) {
   const int lane = w.lane;
   double acc = 0.0;
   for (int c = tk.c0; c < tk.c1; ++c) {
@@ -789,6 +868,7 @@ __device__ __forceinline__ void dense_task(const SweepArgs &a, const SweepTask &
     __syncwarp();
     ++w.jc;
     if (lane == 0) ring_issue(a, w, mbar);
+    if (PROF) tl_mark(w, 3);
   }
   if (PROF) {
     w.acc[4] += 1;
@@ -917,6 +997,8 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   w.slotsz = a.slot;
   w.jc = w.icount = w.rt = w.rc = w.rslab = 0;
   for (int i = 0; i < 8; ++i) w.acc[i] = 0;
+  w.tl_out = nullptr;
+  w.tl_n = 0;
   long long tb = 0;
   SubView sv;
   sv.ys = sm + (int64_t)a.warps * a.vstride;
@@ -945,13 +1027,13 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     w.tl = tl;
     w.bnd = bnd;
     w.nt = nt;
-    if (nt > 0) w.rc = tl[0].c0;
+    if (nt > 0) w.rc = first_item(tl[0]);
   }
   if (lane == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[wl][0])) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[wl][1])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    if (!a.null_work) {  // fill the TMA ring
+    if (!a.null_work && w.nt > 0) {  // fill the TMA ring
       ring_issue(a, w, mbar);
       ring_issue(a, w, mbar);
     }
@@ -999,7 +1081,12 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     int L = 0;
     for (int h = 0; h < a.nsub; ++h, ++L) {
       const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
+      if (PROF) {
+        w.tl_out = (a.tline && k == 1 && crank == 0) ? a.tline + (size_t)wl * 128 : nullptr;
+        tl_mark(w, 1);
+      }
       for (int ti = w.bnd[L]; ti < t1; ++ti) forward_task<true, PROF>(a, w.tl[ti], F, rhs, sv, w, mbar);
+      if (PROF) tl_mark(w, 4);
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
     }
     if (a.nsub || a.prog_hdr) {  // subtree roots' updates and coupled top rows visible
@@ -1009,6 +1096,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     if (a.dense) {
       // z_T = coupled rhs of the top unknowns + the subtree roots' updates (all CTAs
       // gather the whole vector), then x_T = K z_T as row tasks
+      if (PROF) tl_mark(w, 5);
       const double *rt = a.prog_hdr ? a.tbuf : rhs;
       for (int i = threadIdx.x; i < a.kpad; i += blockDim.x) {
         double z = 0.0;
@@ -1022,8 +1110,11 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
         sv.zs[i] = z;
       }
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+      sweep_trace(a, step);
       const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
-      for (int ti = w.bnd[L]; ti < t1; ++ti) dense_task<PROF>(a, w.tl[ti], sv.zs, x, w, mbar);
+      if (PROF) tl_mark(w, 1);
+      for (int ti = w.bnd[L]; ti < t1; ++ti) dense_task<PROF>(a, w.tl[ti], sv.zs, x, k, w, mbar);
+      if (PROF) tl_mark(w, 4);
       ++L;
       tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;  // x_T visible
       sweep_trace(a, step);
@@ -1047,7 +1138,9 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     }
     for (int h = a.nsub - 1; h >= 0; --h, ++L) {
       const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
+      if (PROF) tl_mark(w, 5);
       for (int ti = w.bnd[L]; ti < t1; ++ti) backward_task<true, PROF>(a, w.tl[ti], F, x, sv, w, mbar);
+      if (PROF) tl_mark(w, 6);
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
     }
     if (a.post_hdr && !a.null_work) {
@@ -1461,6 +1554,7 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   a.sub_cb = sp.sub_cb;
   a.g3p = sp.g3p.as<int4>();
   a.bpos = sp.bpos.as<int>();
+  a.bpos4 = sp.bpos4.as<int>();
   a.nlevels = p.nlevels;
   a.nw = cluster * warps;
   a.n = n;
@@ -1702,9 +1796,13 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
   }
   static const int prof_on = env_int2("STMHD_SWEEP_PROF", 0);
   DevBuf pr;
+  DevBuf tlb;
   if (prof_on) {
     pr.alloc((size_t)kCluster * kWarps * 8 * sizeof(unsigned long long));
     m.st[ts].prof = pr.as<unsigned long long>();
+    tlb.alloc((size_t)kWarps * 128 * sizeof(unsigned long long));
+    STMHD_CUDA_CHECK(cudaMemsetAsync(tlb.ptr, 0, tlb.bytes, s));
+    m.st[ts].tline = tlb.as<unsigned long long>();
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kCluster * nst);
@@ -1743,7 +1841,7 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
     STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
     const bool fz = a.prog_hdr != nullptr;
     auto entries = [&](int k) {
-      return (int)fz + ((a.nsub || fz) ? 1 : 0) + (a.dense ? 1 : 2 * a.ntop) + (a.nsub && k + 1 < a.nslab);
+      return (int)fz + ((a.nsub || fz) ? 1 : 0) + (a.dense ? 2 : 2 * a.ntop) + (a.nsub && k + 1 < a.nslab);
     };
     const int per = entries(1), base = 1 + entries(0);
     fprintf(stderr, "[sweep] n=%lld levels=%d top=%d sub=%d fused=%d stages=%d total=%.1f us | slab1 (us):",
@@ -1771,6 +1869,23 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
             "barrier %.2f/%.2f | tasks %.1f/%.0f chunks %.1f/%.0f | gemv-only fwd %.2f bwd %.2f\n",
             mean[0] * us, mx[0] * us, mean[1] * us, mx[1] * us, mean[2] * us, mx[2] * us, mean[3] * us, mx[3] * us,
             mean[4] / nrhs0, mx[4] / nrhs0, mean[5] / nrhs0, mx[5] / nrhs0, mean[6] * us, mean[7] * us);
+    // timeline of slab 1, CTA 0: per warp, events (1 level start fwd, 2 gathered, 3 chunk, 4 level done fwd,
+    // 5 level start bwd, 6 level done bwd) in us from the first event
+    std::vector<unsigned long long> tv((size_t)kWarps * 128);
+    STMHD_CUDA_CHECK(cudaMemcpy(tv.data(), tlb.ptr, tv.size() * 8, cudaMemcpyDeviceToHost));
+    unsigned long long t0 = ~0ull;
+    for (auto v : tv)
+      if (v) t0 = std::min(t0, v & ((1ull << 56) - 1));
+    for (int wv = 0; wv < kWarps; ++wv) {
+      fprintf(stderr, "[tl] w%02d:", wv);
+      for (int i = 0; i < 128; ++i) {
+        const unsigned long long v = tv[(size_t)wv * 128 + i];
+        if (!v) break;
+        const char *c = "?SGCEsE";
+        fprintf(stderr, " %c%.2f", c[(v >> 56) & 7], ((v & ((1ull << 56) - 1)) - t0) / 1e3);
+      }
+      fprintf(stderr, "\n");
+    }
   }
 }
 
