@@ -44,6 +44,7 @@ from .spacetime import (  # noqa: F401
     residual,
 )
 from .precond import SpaceTimePreconditioner, Variant, compute_alfven_scaling  # noqa: F401
-from .solver import NewtonConfig, SolveStats, compute_overhead_ratios, solve_all_at_once  # noqa: F401
+from .solver import (NewtonConfig, SolveStats, compute_overhead_ratios, solve_all_at_once,  # noqa: F401
+                     solve_sequential)
 
 __version__ = "0.1.0"

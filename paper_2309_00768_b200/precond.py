@@ -148,6 +148,28 @@ class SpaceTimePreconditioner:
         x = as_device(x).contiguous()
         return self._into(x, torch.empty_like(x), 1)
 
+    # -- single time-step counterpart (precond.py:344-387) -----------------------------
+    def _single(self, k, v, direction):
+        """Slab k of the space-time operator applied to e_k (x) v.  P_T^{-1} is block
+        lower triangular in time and P_T block lower bidiagonal, so with zero input
+        in every other slab this is exactly the single-step operator of slab k
+        (no time coupling) -- computed with the same device kernels."""
+        if not 0 <= k < self.n_steps:
+            raise IndexError(f"slab {k} out of range 0..{self.n_steps - 1}")
+        L = self.layout.slab_size
+        full = torch.zeros(self.n_steps * L, dtype=torch.float64, device="cuda")
+        full[k * L:(k + 1) * L] = as_device(v).reshape(-1)
+        out = self._into(full, torch.empty_like(full), direction)
+        return out[k * L:(k + 1) * L].clone()
+
+    def apply_single_step_inverse(self, k: int, r_slab):
+        """Back-substitution of the single-step preconditioner at slab k (precond.py:344-366)."""
+        return self._single(k, r_slab, 0)
+
+    def apply_single_step(self, k: int, x_slab):
+        """Forward application of the single-step preconditioner at slab k (precond.py:368-387)."""
+        return self._single(k, x_slab, 1)
+
     def _op(self, name, v):
         code, field = OPS[name]
         v = as_device(v).contiguous()

@@ -153,3 +153,24 @@ def test_c5_velocity_fields_divergence_free_and_normalised():
     u = c5_velocity_fields(coords, 3, 0)
     assert u.shape == (3, (n + 1) ** 2, 2)
     np.testing.assert_allclose(np.sqrt((u ** 2).sum(-1)).max(axis=1), 1.0, rtol=1e-14)
+
+
+def test_overhead_ratio_arithmetic_and_errors():
+    """reference tests/test_solver.py:76-106 (pure host logic)."""
+    from paper_2309_00768_b200 import ConfigurationError, SolveStats, compute_overhead_ratios
+
+    st = SolveStats(mode="spacetime", newton_iters=6, gmres_iters=[2] * 6)
+    seq = SolveStats(mode="sequential", newton_iters=6, gmres_iters=[2] * 6, per_step_newton=[3, 3],
+                     per_step_gmres=[[2, 1, 1], [1, 1, 2]])
+    nr, gr = compute_overhead_ratios(st, seq)
+    assert nr == pytest.approx(2.0) and gr == pytest.approx(3.0)
+    assert seq.effective_steps == 2 and seq.avg_newton_per_step == 3 and seq.avg_gmres_per_step == 4
+    st = SolveStats(mode="spacetime", newton_iters=4, gmres_iters=[3, 3, 3, 3])
+    seq = SolveStats(mode="sequential", newton_iters=4, gmres_iters=[3] * 4, per_step_newton=[4],
+                     per_step_gmres=[[3, 3, 3, 3]])
+    assert compute_overhead_ratios(st, seq) == (1.0, 1.0)
+    frozen = SolveStats(mode="sequential", per_step_newton=[0, 0], per_step_gmres=[[], []])
+    with pytest.raises(ConfigurationError):
+        compute_overhead_ratios(st, frozen)
+    with pytest.raises(ConfigurationError):
+        compute_overhead_ratios(seq, st)
