@@ -569,7 +569,7 @@ void PC::apply_inverse(const double *r, double *x, cudaStream_t s) {
 }
 
 void PC::apply_forward(const double *xin, double *out, cudaStream_t s) {
-  require(variant == 0, "apply_forward: only the TRIANGULAR variant is implemented on the device");
+  // precond.py:303-340
   const double *x_u = xin, *x_p = xin + o_p, *x_j = xin + o_j, *x_a = xin + o_a;
   // o_j = M_j x_j + K_jA x_a
   {
@@ -584,10 +584,91 @@ void PC::apply_forward(const double *xin, double *out, cudaStream_t s) {
     spmv(a, s, 8);
   }
   magnetic_schur_apply(x_a, slab, out + o_a, slab, s);
-  // o_u = F_u x_u (bidiagonal) + Z_j x_j + Z_a x_a + B^T x_p
+  if (variant == 0) {
+    // o_u = F_u x_u (bidiagonal) + Z_j x_j + Z_a x_a + B^T x_p
+    apply_velocity(x_u, slab, tu1.as<double>(), n_u, s);
+    coupling_u(tu1.as<double>(), n_u, 1.0, xin, slab, 1.0, x_p, slab, 1.0, out, slab, s);
+    pressure_schur_apply(x_p, slab, out + o_p, slab, s);
+    return;
+  }
+  // SIMPLIFIED / FULL: velocity-pressure upper factor t_u = F_u x_u + B^T x_p
   apply_velocity(x_u, slab, tu1.as<double>(), n_u, s);
-  coupling_u(tu1.as<double>(), n_u, 1.0, xin, slab, 1.0, x_p, slab, 1.0, out, slab, s);
+  {
+    SpmvArgs a;
+    a.nrows = n_u;
+    a.nslab = nt;
+    a.y = tu1.as<double>();
+    a.y_stride = n_u;
+    a.z = tu1.as<double>();
+    a.z_stride = n_u;
+    a.beta = 1.0;
+    a.t[0] = csr_term(d->csr("divt"), x_p, slab, 1.0);
+    a.nterms = 1;
+    spmv(a, s, 8);
+  }
   pressure_schur_apply(x_p, slab, out + o_p, slab, s);
+  // velocity-pressure lower factor: o_p += B F_u^{-1} t_u
+  solve_velocity(tu1.as<double>(), n_u, tu2.as<double>(), n_u, s);
+  {
+    SpmvArgs a;
+    a.nrows = n_p;
+    a.nslab = nt;
+    a.y = out + o_p;
+    a.y_stride = slab;
+    a.z = out + o_p;
+    a.z_stride = slab;
+    a.beta = 1.0;
+    a.t[0] = csr_term(d->csr("div"), tu2.as<double>(), n_u, 1.0);
+    a.nterms = 1;
+    spmv(a, s, 8);
+  }
+  // o_u = t_u + Z_j x_j + Z_a x_a (the velocity-magnetic upper factor absorbed F_u^{-1})
+  coupling_u(tu1.as<double>(), n_u, 1.0, xin, slab, 1.0, nullptr, 0, 0.0, out, slab, s);
+  if (variant == 2) {
+    // velocity-magnetic lower factor: o_A += Y F_u^{-1}(o_u - Z_j M_j^{-1} o_j)
+    d->lu_mj->solve(out + o_j, slab, tj.as<double>(), n_j, nt, s);
+    SpmvArgs a;
+    a.nrows = n_u;
+    a.nslab = nt;
+    a.y = tu1.as<double>();
+    a.y_stride = n_u;
+    a.z = out;
+    a.z_stride = slab;
+    a.beta = 1.0;
+    SpTerm zj;
+    zj.beg = d->D<int>("js_seg0");
+    zj.end = d->D<int>("js_seg1");
+    zj.col = d->D<int>("js_col");
+    zj.val = js;
+    zj.val_stride = nnz_js;
+    zj.x = tj.as<double>();
+    zj.x_stride = n_j;
+    zj.col_off = (int)o_j;
+    zj.alpha = -1.0;
+    a.t[0] = zj;
+    a.nterms = 1;
+    spmv(a, s, 8);
+    solve_velocity(tu1.as<double>(), n_u, tu2.as<double>(), n_u, s);
+    SpmvArgs b;
+    b.nrows = n_a;
+    b.nslab = nt;
+    b.y = out + o_a;
+    b.y_stride = slab;
+    b.z = out + o_a;
+    b.z_stride = slab;
+    b.beta = 1.0;
+    SpTerm y;
+    y.beg = d->D<int>("js_rowptr") + o_a;
+    y.end = d->D<int>("js_seg0") + o_a;
+    y.col = d->D<int>("js_col");
+    y.val = js;
+    y.val_stride = nnz_js;
+    y.x = tu2.as<double>();
+    y.x_stride = n_u;
+    b.t[0] = y;
+    b.nterms = 1;
+    spmv(b, s, 8);
+  }
 }
 
 void PC::op(int which, const double *in, double *out, cudaStream_t s) {

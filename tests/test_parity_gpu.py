@@ -234,3 +234,28 @@ def test_pipelined_apply_deterministic_and_matches_sequential(p, golden):
     x_p = pc.pressure_schur_inverse(vv[:, o_p:o_j].reshape(-1)).view(nt, -1)
     assert relerr(o[:, o_p:o_j].cpu().numpy(), x_p.cpu().numpy()) < 1e-12
     assert relerr(pc.apply_forward(outs[0]).cpu().numpy(), g["v"]) < 1e-10
+
+
+@pytest.mark.parametrize("case_name,prob,dx", [("variants_island", "island_coalescence", 0.5),
+                                                ("variants_tearing", "tearing_mode", 0.25)])
+@pytest.mark.parametrize("variant", ["triangular", "simplified", "full"])
+def test_variants_match_reference_and_round_trip(p, golden, case_name, prob, dx, variant):
+    """All three P_T variants, inverse and forward application, against the
+    reference (golden vectors) and the round trips of reference
+    tests/test_precond.py:187-196."""
+    import torch
+
+    g = golden(case_name)
+    d = p.discretize(p.by_name(prob), dx, 0.5, 1.0)
+    st = p.SpaceTimeState(p.BlockVector(d.layout, d.n_steps, g["state"]), torch.as_tensor(g["ic_u"], device="cuda"),
+                          torch.as_tensor(g["ic_a"], device="cuda"))
+    jac = p.assemble_jacobian(st, d)
+    pc = p.SpaceTimePreconditioner(jac, d, st, variant)
+    x = g["x"]
+    assert relerr(pc.apply_inverse(x).cpu().numpy(), g[f"inv_{variant}"]) < 1e-10
+    assert relerr(pc.apply_forward(x).cpu().numpy(), g[f"fwd_{variant}"]) < 1e-10
+    rng = np.random.default_rng(5)
+    for _ in range(3):
+        y = rng.standard_normal(jac.size)
+        assert relerr(pc.apply_inverse(pc.apply_forward(y)).cpu().numpy(), y) <= 1e-9
+        assert relerr(pc.apply_forward(pc.apply_inverse(y)).cpu().numpy(), y) <= 1e-9
