@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(KT) update_partial(const double *V, int64_t ld
 }
 
 __global__ void normalize_kernel(const double *x, double *y, int64_t n, const double *nrm2) {
-  const double inv = 1.0 / sqrt(*nrm2);
+  const double nv = *nrm2;
+  const double inv = nv > 0.0 ? 1.0 / sqrt(nv) : 0.0;  // zero vector on breakdown (the host stops there)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = x[i] * inv;
 }

@@ -219,6 +219,8 @@ class _Workspace:
                       Z=torch.empty((m, n), dtype=torch.float64, device=DEV),
                       dev=torch.zeros(2 * (m + 2), dtype=torch.float64, device=DEV),
                       host=torch.zeros(2 * (m + 2), dtype=torch.float64).pin_memory(),
+                      host2=torch.zeros(2 * (m + 2), dtype=torch.float64).pin_memory(),
+                      ev=[torch.cuda.Event(), torch.cuda.Event()],
                       work=torch.empty(int(lib.stmhd_gs_work_size(n, m + 1)) + 8, dtype=torch.float64, device=DEV),
                       y=torch.zeros(m, dtype=torch.float64, device=DEV),
                       r=torch.empty(n, dtype=torch.float64, device=DEV))
@@ -281,6 +283,45 @@ def gmres(apply_a, apply_pinv, b, x0=None, config: GmresConfig | None = None) ->
         torch.div(r, beta, out=V[0])
         g[0] = beta
         last = -1
+        hosts = (ws["host"], ws["host2"])
+        evs = ws["ev"]
+
+        def process(jj):
+            """Givens update of column jj (its Hessenberg entries are in hosts[jj % 2]);
+            returns True when the cycle stops at jj (converged or breakdown)."""
+            nonlocal total, last, converged
+            evs[jj % 2].synchronize()
+            hv = hosts[jj % 2].numpy()
+            nv = jj + 1
+            col = hv[:nv] + hv[m_alloc + 1: m_alloc + 1 + nv]
+            nrm2 = hv[2 * m_alloc + 3]
+            if not (np.all(np.isfinite(col)) and np.isfinite(nrm2)):
+                raise BreakdownError("non-finite vector in Arnoldi process")
+            hnorm = float(np.sqrt(max(nrm2, 0.0)))
+            H[:nv, jj] = col
+            H[jj + 1, jj] = hnorm
+            for i in range(jj):
+                t = cs[i] * H[i, jj] + sn[i] * H[i + 1, jj]
+                H[i + 1, jj] = -sn[i] * H[i, jj] + cs[i] * H[i + 1, jj]
+                H[i, jj] = t
+            den = np.hypot(H[jj, jj], H[jj + 1, jj])
+            cs[jj], sn[jj] = H[jj, jj] / den, H[jj + 1, jj] / den
+            H[jj, jj] = den
+            H[jj + 1, jj] = 0.0
+            g[jj + 1] = -sn[jj] * g[jj]
+            g[jj] = cs[jj] * g[jj]
+            total += 1
+            last = jj
+            residuals.append(abs(float(g[jj + 1])))
+            if residuals[-1] <= tol:
+                converged = True
+                return True
+            return den == 0.0
+
+        # The host Givens update of column j-1 runs while iteration j is already on the
+        # device (one-iteration lag): the GPU never waits for the host.  Numbers are
+        # identical to the unlagged loop; a cycle that stops at j-1 discards iteration j.
+        stopped = False
         for j in range(m):
             P_into(V[j], Z[j])
             w = V[j + 1]
@@ -292,36 +333,14 @@ def gmres(apply_a, apply_pinv, b, x0=None, config: GmresConfig | None = None) ->
                                            0, _lib.ptr(work)))
             _lib.check(lib.stmhd_gs_update(sp_, _lib.ptr(V), n, nv, _lib.ptr(h2), _lib.ptr(w), n, 0,
                                            _lib.ptr(nrm), _lib.ptr(work)))
-            host.copy_(dev, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            hv = host.numpy()
-            col = hv[:nv] + hv[m_alloc + 1: m_alloc + 1 + nv]
-            nrm2 = hv[2 * m_alloc + 3]
-            if not (np.all(np.isfinite(col)) and np.isfinite(nrm2)):
-                raise BreakdownError("non-finite vector in Arnoldi process")
-            hnorm = float(np.sqrt(max(nrm2, 0.0)))
-            H[:nv, j] = col
-            H[j + 1, j] = hnorm
-            for i in range(j):
-                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
-                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
-                H[i, j] = t
-            den = np.hypot(H[j, j], H[j + 1, j])
-            cs[j], sn[j] = H[j, j] / den, H[j + 1, j] / den
-            H[j, j] = den
-            H[j + 1, j] = 0.0
-            g[j + 1] = -sn[j] * g[j]
-            g[j] = cs[j] * g[j]
-            total += 1
-            last = j
-            residuals.append(abs(float(g[j + 1])))
-            if residuals[-1] <= tol:
-                converged = True
+            hosts[j % 2].copy_(dev, non_blocking=True)
+            evs[j % 2].record()
+            _lib.check(lib.stmhd_gs_normalize(sp_, _lib.ptr(w), _lib.ptr(w), n, _lib.ptr(nrm)))
+            if j > 0 and process(j - 1):
+                stopped = True
                 break
-            if den == 0.0:
-                break
-            if hnorm > 0:
-                _lib.check(lib.stmhd_gs_normalize(sp_, _lib.ptr(w), _lib.ptr(w), n, _lib.ptr(nrm)))
+        if not stopped:
+            process(m - 1)
         if last >= 0:
             y = np.zeros(last + 1)
             for i in range(last, -1, -1):
