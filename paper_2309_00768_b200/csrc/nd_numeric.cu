@@ -386,7 +386,7 @@ void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s
   ++gen;  // invalidates derived data (dense top inverse)
   if (factors.bytes != (size_t)nbatch * p.factor_size * sizeof(double))
     factors.alloc_async((size_t)nbatch * p.factor_size * sizeof(double), s);
-  if (!status.ptr) status.alloc(sizeof(int));
+  if (!status.ptr) status.alloc_async(sizeof(int), s);
   STMHD_CUDA_CHECK(cudaMemsetAsync(status.ptr, 0, sizeof(int), s));
   // chunk the batch so front workspace + staging stay below ~3 GiB
   int64_t per = (std::max<int64_t>(p.front_size, 1) + p.stage_size) * (int64_t)sizeof(double);

@@ -1358,6 +1358,41 @@ struct TopKArgs {
   int64_t kstride;
 };
 
+// acc[i] = sum_k blk(r0 + i, k) V[k][lane], i < 4 (rows >= nrows give 0), for a factor
+// block stored as row chunks [K][R] (element (r, k) at (r / R) * bsz + k * R + r % R).
+__device__ __forceinline__ void topk_rows4(const double *blk, int R, int bsz, int r0, int nrows, int K,
+                                           const double *V, int lane, double acc[4]) {
+  const double *row[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = min(r0 + i, nrows - 1);
+    row[i] = blk + (int64_t)(r / R) * bsz + (r % R);
+    acc[i] = 0.0;
+  }
+  int k = 0;
+  for (; k + 4 <= K; k += 4) {
+    double fv[4][4], vv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      vv[j] = V[(k + j) * 32 + lane];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fv[i][j] = __ldg(row[i] + (int64_t)(k + j) * R);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = fma(fv[i][j], vv[j], acc[i]);
+  }
+  for (; k < K; ++k) {
+    const double v = V[k * 32 + lane];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = fma(__ldg(row[i] + (int64_t)k * R), v, acc[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (r0 + i >= nrows) acc[i] = 0.0;
+}
+
 __global__ void __launch_bounds__(256) topk_kernel(TopKArgs g) {
   extern __shared__ __align__(16) double V[];  // front x 32
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -1378,12 +1413,16 @@ __global__ void __launch_bounds__(256) topk_kernel(TopKArgs g) {
         for (int a = wl; a < ch.z; a += nw) V[g.emap[ch.y + a] * 32 + lane] += CBw[(int64_t)(cb0 + a) * 32 + lane];
         __syncthreads();
       }
-      for (int r = wl; r < f; r += nw) {
-        const double *row = F + t.fl_off + (int64_t)(r / t.rf) * t.bszf + (r % t.rf);
-        double acc = 0.0;
-        for (int k = 0; k < t.ns; ++k) acc = fma(__ldg(row + (int64_t)k * t.rf), V[k * 32 + lane], acc);
-        if (r < t.ns) Xw[(int64_t)g.tidx[t.first + r] * 32 + lane] = acc;  // y
-        else CBw[(int64_t)(t.tcb_off + r - t.ns) * 32 + lane] = V[r * 32 + lane] - acc;
+      for (int r0 = wl * 4; r0 < f; r0 += nw * 4) {  // 4 rows per warp, 16 factor loads in flight
+        double acc[4];
+        topk_rows4(F + t.fl_off, t.rf, t.bszf, r0, f, t.ns, V, lane, acc);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = r0 + i;
+          if (r >= f) break;
+          if (r < t.ns) Xw[(int64_t)g.tidx[t.first + r] * 32 + lane] = acc[i];  // y
+          else CBw[(int64_t)(t.tcb_off + r - t.ns) * 32 + lane] = V[r * 32 + lane] - acc[i];
+        }
       }
       __syncthreads();
     }
@@ -1395,11 +1434,12 @@ __global__ void __launch_bounds__(256) topk_kernel(TopKArgs g) {
         V[r * 32 + lane] = Xw[(int64_t)g.tidx[pos] * 32 + lane];  // own y, or the ancestors' x
       }
       __syncthreads();
-      for (int k = wl; k < t.ns; k += nw) {
-        const double *row = F + t.fu_off + (int64_t)(k / t.rb) * t.bszb + (k % t.rb);
-        double acc = 0.0;
-        for (int r = 0; r < f; ++r) acc = fma(__ldg(row + (int64_t)r * t.rb), V[r * 32 + lane], acc);
-        Xw[(int64_t)g.tidx[t.first + k] * 32 + lane] = acc;
+      for (int k0 = wl * 4; k0 < t.ns; k0 += nw * 4) {
+        double acc[4];
+        topk_rows4(F + t.fu_off, t.rb, t.bszb, k0, t.ns, f, V, lane, acc);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (k0 + i < t.ns) Xw[(int64_t)g.tidx[t.first + k0 + i] * 32 + lane] = acc[i];
       }
       __syncthreads();
     }
@@ -1490,10 +1530,7 @@ static int gather_values(const CplProgram &pg, const SweepCoupling *cpl, int ncp
   }
   const int nblk = per_slab ? nrhs : 1;
   const size_t vneed = (size_t)nblk * pg.nent * sizeof(double);
-  if (buf.bytes < vneed) {
-    STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-    buf.alloc(vneed);
-  }
+  if (buf.bytes < vneed) buf.alloc_async(vneed, s);
   cpl_vals_kernel<<<dim3((unsigned)std::min<int64_t>(cdiv(pg.nent, 256), 1024), nblk), 256, 0, s>>>(
       pg.esrc.as<int2>(), pg.nent, cv, per_slab, buf.as<double>());
   STMHD_LAUNCH_CHECK();
@@ -1521,13 +1558,11 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   st.nrhs = nrhs;
   // scratch: rhsp | xp | ybuf | cbv | tbuf; zero: n zeros, never written
   const size_t need = ((size_t)2 * nrhs * n + 2 * n + p.cbv_size + 16) * sizeof(double);
-  if (st.scratch.bytes < need) {
-    STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-    st.scratch.alloc(need);
-  }
+  // stage buffers come from the stream-ordered pool: growing or freeing them never
+  // synchronises the device (a new preconditioner per Newton step reuses the blocks)
+  if (st.scratch.bytes < need) st.scratch.alloc_async(need, s);
   if (st.zero.bytes < (size_t)n * sizeof(double)) {
-    STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-    st.zero.alloc((size_t)n * sizeof(double));
+    st.zero.alloc_async((size_t)n * sizeof(double), s);
     STMHD_CUDA_CHECK(cudaMemsetAsync(st.zero.ptr, 0, st.zero.bytes, s));
   }
   double *rhsp = st.scratch.as<double>();
@@ -1748,7 +1783,7 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
     if (nst > 1) {  // every stage publishes per-slab flags
       const int64_t need = (int64_t)st.nrhs * kCluster;
       if (st.flags_slabs < need) {
-        st.flags.alloc(need * sizeof(int));
+        st.flags.alloc_async(need * sizeof(int), s);
         STMHD_CUDA_CHECK(cudaMemsetAsync(st.flags.ptr, 0, need * sizeof(int), s));
         st.flags_slabs = need;
       }
