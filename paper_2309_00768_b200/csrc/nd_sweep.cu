@@ -2,22 +2,25 @@
 // factors (reference: solve_velocity / solve_wave / solve_potential /
 // solve_pressure_cd, pkg/src/stmhd/precond.py:122-205):
 //
-//   x_k = A_k^{-1} ( rhs_k + sum_c coef_c C_c x_{k-lag_c} ),  k = 0..nt-1.
+//   x_k = A_k^{-1} ( rhs_k + sum_c coef_c C_c src_c ),  k = 0..nt-1,
 //
+// src_c = x_{k-lag} (lag 1, 2) or another sweep's x_k (pipelined launch).
 // The slabs are strictly sequential, so the sweep is latency bound.  One
-// thread-block cluster runs the whole sweep in a single launch (hardware
-// cluster barrier between tree levels; a software grid barrier costs 2.3 us,
-// tools/bench_barrier.py).  Inside:
-//  * everything runs in the nested-dissection ordering, so a supernode's own
-//    unknowns are contiguous; rhs / solutions are permuted in and out by two
-//    bandwidth-bound kernels around the sweep;
-//  * each warp owns a contiguous range of row chunks of one supernode per
-//    level (LPT balanced); a chunk's factor block [K][R] is one contiguous
-//    range that the TMA engine copies into the warp's shared-memory slot
-//    (cp.async.bulk + mbarrier, double buffered), overlapped with the front
-//    gather; the GEMV then reads shared memory;
-//  * the next slab's factors are bulk-prefetched into L2 while a slab runs;
-//  * couplings are ELL tables in elimination order.
+// 16-CTA thread-block cluster runs a whole sweep in one launch (hardware cluster
+// barrier; a software grid barrier costs 2.3 us, tools/bench_barrier.py).  Per slab:
+//  1. coupling program (CTA-local): the coupled rhs of this CTA's rows, all loads
+//     of a row batch in flight (sources through a shared-memory pointer table);
+//  2. subtree forward: the bottom of the nested-dissection tree is cut into <= 16
+//     balanced subtrees, one per CTA; their levels are separated by __syncthreads
+//     and their vectors live in that CTA's shared memory;
+//  3. dense top: x_T = K z_T, K = (A^{-1})_TT built once per factorisation
+//     (topk_kernel), one GEMV step instead of 2 * (top levels) cluster steps;
+//  4. subtree backward (CTA-local);  5. (pipelined launch) post-slab program and
+//     per-slab release flag for the consuming sweep.
+// Every warp walks a static item sequence (front tables, factor chunks, K rows)
+// held in shared memory; a TMA ring (cp.async.bulk + mbarrier, two slots) keeps
+// its next items in flight across task, level and slab boundaries.  Vectors run in
+// the nested-dissection ordering, permuted in and out around the launch.
 #include <algorithm>
 #include <array>
 #include <cstdlib>
