@@ -100,6 +100,7 @@ struct NDSweepPlan {
   // (subtree forward levels, top forward, top backward, subtree backward) and the
   // start of every phase level in it (nl = 2 nsub + 2 ntop levels, nl + 1 bounds)
   int nl = 0, max_wtasks = 0;
+  int vstride = 0;          // doubles of shared memory per warp (gather buffer + two TMA slots)
   DevBuf wl_tasks, wl_off, wl_bnd;
   // dense top (dense = 1): after the subtree forward phase the top unknowns are
   //   x_T = K z_T,  z_T = top rows of the coupled rhs + the subtree roots' updates,
@@ -111,6 +112,10 @@ struct NDSweepPlan {
   DevBuf tsn, tchild;       // top supernodes (postorder) and their top children (K construction)
   int ntsn = 0;
   int64_t tcb_total = 0;    // sum of nb over top supernodes
+  // per-CTA subtree front tables kept in shared memory (dense mode): ints per CTA
+  // block [tab_ptr[c], tab_ptr[c+1]): forward int32 entries, then backward uint16 pairs
+  int tab_ints = 0;
+  DevBuf tab, tab_ptr, tab_nf;
   DevBuf g3p;   // int4 per front position: {permuted rhs index or -1, cb1, cb2, 0}
   DevBuf bpos;  // int per front position: permuted position of the front entry
   DevBuf bpos4; // bpos per supernode, each block 16-byte aligned (TMA ring table items)
@@ -135,7 +140,7 @@ struct NDDevice {
   int max_front = 0;
   void build(const NDPlan &p, cudaStream_t s);
   mutable std::unique_ptr<NDSweepPlan> sweep_plan;
-  const NDSweepPlan &get_sweep_plan(int ncta, int warps, int64_t sub_budget, cudaStream_t s, int mode = 0) const;
+  const NDSweepPlan &get_sweep_plan(int ncta, int warps, int64_t smem_budget, cudaStream_t s, int mode = 0) const;
 };
 
 // A coupling term of a sequential block sweep:

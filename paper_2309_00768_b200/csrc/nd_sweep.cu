@@ -44,9 +44,22 @@ struct TopSN {
   int pad[3];
 };
 
-const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_budget, cudaStream_t s,
+// Shared memory per warp: gather buffer (largest front it gathers, rounded to 16
+// doubles) + two TMA slots of the largest ring item.
+static int sweep_slot(const NDPlan &p) {
+  int64_t maxb = 2;
+  for (int sn = 0; sn < p.nsn; ++sn) maxb = std::max({maxb, p.bsz_f[sn], p.bsz_b[sn]});
+  return (int)((maxb + 15) / 16 * 16);
+}
+
+// mode ladder (first that fits shared memory wins): 0 subtrees + dense top + resident
+// subtree tables, 1 subtrees + dense top, 2 subtrees + tree top, 3 all levels cluster-wide
+const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_budget, cudaStream_t s,
                                             int mode) const {
-  const bool flat = mode >= 2;  // 0: subtrees + dense top, 1: subtrees only, 2: all levels cluster-wide
+  const bool flat = mode >= 3;
+  const int slot_sz = sweep_slot(*plan);
+  const int64_t vstride_max = (std::max(max_front, 1) + 15) / 16 * 16 + 2 * slot_sz;
+  const int64_t sub_budget = smem_budget - (int64_t)warps * vstride_max;  // conservative (largest front)
   if (sweep_plan && sweep_plan->ncta == ncta && sweep_plan->warps == warps) return *sweep_plan;
   const NDPlan &p = *plan;
   auto sp = std::make_unique<NDSweepPlan>();
@@ -266,7 +279,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
   static const int dense_env = env_int2("STMHD_SWEEP_DENSE_TOP", 1);
   std::vector<int> tpos, tidx_h(p.n, -1);
   std::vector<int4> ztab;
-  if (dense_env && mode == 0 && sp->nsub > 0 && ntop > 0) {
+  if (dense_env && mode <= 1 && sp->nsub > 0 && ntop > 0) {
     for (int sn = 0; sn < p.nsn; ++sn)  // top unknowns in elimination order
       if (owner[sn] < 0)
         for (int t = 0; t < p.ns[sn]; ++t) {
@@ -306,6 +319,61 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
       }
     }
   }
+  // ---- subtree front tables resident in shared memory (dense mode) ----
+  // forward (internal subtree supernodes only; leaves gather rhs rows alone): int32
+  // per front entry = child update indices (y, z) relative to the CTA's update block
+  // as two int16; backward (every subtree supernode, boundary entries t >= ns): uint16
+  // = own-subtree index, or 0x8000 | top index (x_T is staged in shared memory).
+  static const int stab_env = env_int2("STMHD_SWEEP_SMEM_TABLES", 1);
+  std::vector<int> ftab_off(p.nsn, -1), btab_off(p.nsn, -1), sn_of_first(p.n, -1);
+  std::vector<int> tab_all, tab_ptr(ncta + 1, 0), tab_nf(ncta, 0);
+  bool stab = stab_env && mode == 0 && sp->dense && sp->nsub > 0 && maxlen < 32768 && maxcb < 32768 &&
+              sp->ntT < 32768;
+  if (stab) {
+    for (int sn = 0; sn < p.nsn; ++sn) sn_of_first[p.first[sn]] = sn;
+    for (int c = 0; c < ncta && c < (int)roots.size(); ++c) {
+      const int64_t sf = info[4 * c], cbf = info[4 * c + 2];
+      std::vector<int> fw;
+      std::vector<unsigned short> bw;
+      for (int sn = 0; sn < p.nsn; ++sn) {
+        if (owner[sn] != c) continue;
+        const int f = p.ns[sn] + p.nb[sn];
+        const int64_t o = p.idx_off[sn];
+        if (p.child_ptr[sn + 1] > p.child_ptr[sn]) {
+          ftab_off[sn] = (int)fw.size();
+          for (int t = 0; t < f; ++t) {
+            const int y = g3[o + t].y >= 0 ? (int)(g3[o + t].y - cbf) : -1;
+            const int z = g3[o + t].z >= 0 ? (int)(g3[o + t].z - cbf) : -1;
+            fw.push_back((int)((unsigned)(y & 0xffff) | ((unsigned)(z & 0xffff) << 16)));
+          }
+        }
+        btab_off[sn] = (int)bw.size();
+        for (int t = p.ns[sn]; t < f; ++t) {
+          const int q = bpos[o + t];
+          const int64_t rel = q - sf;
+          if (rel >= 0 && rel < info[4 * c + 1]) bw.push_back((unsigned short)rel);
+          else {
+            require(tidx_h[q] >= 0, "nd sweep: subtree boundary outside the top");
+            bw.push_back((unsigned short)(0x8000 | tidx_h[q]));
+          }
+        }
+      }
+      while (bw.size() % 8) bw.push_back(0);  // 16-byte blocks
+      tab_nf[c] = (int)fw.size();
+      while (fw.size() % 4) fw.push_back(0);
+      // block layout (ints): fwd entries, then the uint16 backward entries packed in pairs
+      const size_t base = tab_all.size();
+      tab_all.insert(tab_all.end(), fw.begin(), fw.end());
+      for (size_t i = 0; i < bw.size(); i += 2) tab_all.push_back((int)((unsigned)bw[i] | ((unsigned)bw[i + 1] << 16)));
+      tab_ptr[c + 1] = (int)tab_all.size();
+      tab_nf[c] = (int)fw.size();  // padded forward length (start of the backward entries)
+      static_cast<void>(base);
+    }
+    for (int c = (int)roots.size(); c < ncta; ++c) tab_ptr[c + 1] = tab_ptr[c];
+    int maxtab = 0;
+    for (int c = 0; c < ncta; ++c) maxtab = std::max(maxtab, tab_ptr[c + 1] - tab_ptr[c]);
+    sp->tab_ints = (maxtab + 3) / 4 * 4;
+  }
   // per direction: top tasks per [top level][global warp], subtree tasks per
   // [cta][local level][warp]
   std::vector<std::vector<SweepTask>> top_t[2], sub_t[2];
@@ -342,6 +410,22 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
           }
         std::vector<std::vector<SweepTask>> per;
         schedule(sns, warps, fwd, per, cbg);
+        if (stab)  // tables in shared memory (flags 16: leaf, no forward table; 32: shared table)
+          for (auto &pw : per)
+            for (SweepTask &t : pw) {
+              const int sn = sn_of_first[t.first];
+              t.flags &= (unsigned char)~(4 | 8);
+              if (fwd) {
+                if (ftab_off[sn] < 0) t.flags |= 16;
+                else {
+                  t.flags |= 32;
+                  t.goff = ftab_off[sn];
+                }
+              } else {
+                t.flags |= 32;
+                t.cboff = btab_off[sn];
+              }
+            }
         for (int w = 0; w < warps; ++w) st[((size_t)c * sp->nsub + h) * warps + w] = std::move(per[w]);
       }
   };
@@ -410,8 +494,16 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
     // shared memory: subtree vectors + per-warp task lists must fit next to the
     // per-warp gather buffers; otherwise fall back to an all-top schedule
     const int64_t tdoubles = (int64_t)warps * (((sp->nl + 1 + 3) / 4) * 16 + (int64_t)maxw * 32) / 8;
-    if (!flat && D > 0 && 3 * maxlen + maxcb + tdoubles + sp->kpad + 2 > sub_budget)
-      return get_sweep_plan(ncta, warps, sub_budget, s, sp->dense ? 1 : 2);
+    // gather buffer: in dense mode only subtree fronts are gathered
+    int fmax = 1;
+    for (int sn = 0; sn < p.nsn; ++sn)
+      if (!sp->dense || owner[sn] >= 0) fmax = std::max(fmax, p.ns[sn] + p.nb[sn]);
+    sp->vstride = (int)((fmax + 15) / 16 * 16 + 2 * slot_sz);
+    const int64_t need = (int64_t)warps * sp->vstride + 3 * maxlen + maxcb + tdoubles + sp->kpad + sp->tab_ints / 2 + 4;
+    if (!flat && D > 0 && need > smem_budget) {
+      const int next = sp->tab_ints ? 1 : (sp->dense ? 2 : 3);
+      return get_sweep_plan(ncta, warps, smem_budget, s, next);
+    }
     sp->wl_tasks = upload_vec(all, s);
     sp->wl_off = upload_vec(off, s);
     sp->wl_bnd = upload_vec(bnd, s);
@@ -464,6 +556,12 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t sub_bud
   sp->g3p = upload_vec(g3, s);
   sp->bpos = upload_vec(bpos, s);
   sp->bpos4 = upload_vec(bpos4, s);
+  if (stab) {
+    if (tab_all.empty()) tab_all.push_back(0);
+    sp->tab = upload_vec(tab_all, s);
+    sp->tab_ptr = upload_vec(tab_ptr, s);
+    sp->tab_nf = upload_vec(tab_nf, s);
+  }
   sp->pos = upload_vec(pos, s);
   sp->iperm = upload_vec(iperm, s);
   STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -487,6 +585,9 @@ struct SweepArgs {
   int64_t prog_nent;
   int prog_per_slab;
   double *tbuf;                // coupled right-hand side of the top rows
+  // per-CTA subtree front tables resident in shared memory (NDSweepPlan::tab)
+  const int *tab, *tab_ptr, *tab_nf;
+  int tab_ints;
   // dense top (NDSweepPlan::dense): z_T gather table and K = (A^{-1})_TT per slab
   int dense, ntT, kpad;
   const int4 *ztab;
@@ -595,7 +696,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
 // Per-CTA view of the subtree vectors kept in shared memory.
 struct SubView {
   double *ys, *xs, *cbs, *rhs_s;  // rhs_s: coupled right-hand side of the subtree rows (fused mode)
-  double *zs;                     // dense top: z_T (kpad doubles)
+  double *zs;                     // dense top: z_T (kpad doubles); x_T during the subtree backward
+  const int *ftab;                // subtree forward tables (shared memory) or null
+  const unsigned short *btab;     // subtree backward tables
   int64_t first, len, cbfirst;
 };
 
@@ -715,6 +818,21 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
   // fused coupling: subtree rows come from shared memory, top rows from tbuf
   const bool fused = a.prog_hdr != nullptr;
   const double *rsrc = (SUB && fused) ? sv.rhs_s - sv.first : (fused ? a.tbuf : rhs);
+  if (SUB && (tk.flags & (16 | 32))) {
+    // shared-memory front: a leaf gathers its rhs rows only; an internal node adds
+    // its children's updates through the resident table
+    const int *ft = sv.ftab + tk.goff;
+    const bool leaf = tk.flags & 16;
+    for (int t = lane; t < tk.f; t += 32) {
+      double v = t < tk.ns ? rsrc[tk.first + t] : 0.0;
+      if (!leaf) {
+        const int e = ft[t];
+        const int y = (short)(e & 0xffff), z = (short)(e >> 16);
+        v = (v + (y >= 0 ? sv.cbs[y] : 0.0)) + (z >= 0 ? sv.cbs[z] : 0.0);
+      }
+      w.v[t] = v;
+    }
+  } else
   for (int b0 = lane; b0 < tk.f; b0 += 256) {
     int4 gg[8];
 #pragma unroll
@@ -783,12 +901,28 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
                                               const SubView &sv, WarpCtx &w, unsigned long long (*mbar)[2]) {
   const int lane = w.lane;
   long long t0 = pclock<PROF>();
+  if (SUB && (tk.flags & 32)) {
+    // shared-memory front: own y, own-subtree x (xs) or top x (staged in zs)
+    const unsigned short *bt = sv.btab + tk.cboff - tk.ns;
+    const double *ys = sv.ys - sv.first + tk.first;
+    for (int t = lane; t < tk.f; t += 32) {
+      double v;
+      if (t < tk.ns) v = ys[t];
+      else {
+        const unsigned code = bt[t];
+        v = (code & 0x8000u) ? sv.zs[code & 0x7fffu] : sv.xs[code];
+      }
+      w.v[t] = v;
+    }
+    __syncwarp();
+  }
   const int *bp = a.bpos + tk.goff;
   if (tk.flags & 4) {  // front table arrived through the ring
     mbar_wait(&mbar[w.wl][w.jc & 1], (unsigned)(w.jc >> 1) & 1u);
     bp = reinterpret_cast<const int *>(w.slot0 + (w.jc & 1) * w.slotsz);
   }
   const double *y = (SUB ? sv.ys - sv.first : a.ybuf) + tk.first;
+  if (!(SUB && (tk.flags & 32)))
   for (int b0 = lane; b0 < tk.f; b0 += 256) {
     int ii[8];
 #pragma unroll
@@ -1009,6 +1143,16 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   sv.cbs = sv.xs + a.sub_len;
   sv.rhs_s = sv.cbs + a.sub_cb;
   sv.zs = sv.rhs_s + a.sub_len;
+  sv.ftab = nullptr;
+  sv.btab = nullptr;
+  if (a.tab_ints) {  // this CTA's subtree front tables, resident for the whole launch
+    int *tb = reinterpret_cast<int *>((reinterpret_cast<uintptr_t>(sv.zs + a.kpad) + 15) & ~(uintptr_t)15);
+    const int o = a.tab_ptr[crank], nt = a.tab_ptr[crank + 1] - o;
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) tb[i] = a.tab[o + i];
+    sv.ftab = tb;
+    sv.btab = reinterpret_cast<const unsigned short *>(tb + a.tab_nf[crank]);
+    __syncthreads();
+  }
   sv.first = a.sub_info[4 * crank + 0];
   sv.len = a.sub_info[4 * crank + 1];
   sv.cbfirst = a.sub_info[4 * crank + 2];
@@ -1016,7 +1160,8 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     // copy this warp's task list and level bounds into shared memory (static for
     // the whole sweep: no global round trip per level or task afterwards)
     const int gid = crank * a.warps + wl;
-    const uintptr_t base = (reinterpret_cast<uintptr_t>(sv.zs + a.kpad) + 15) & ~(uintptr_t)15;
+    const uintptr_t base =
+        (reinterpret_cast<uintptr_t>(sv.zs + a.kpad) + 15 + (size_t)a.tab_ints * 4) & ~(uintptr_t)15;
     char *area = reinterpret_cast<char *>(base) + (size_t)wl * a.tstride;
     int *bnd = reinterpret_cast<int *>(area);
     SweepTask *tl = reinterpret_cast<SweepTask *>(area + ((a.nl + 1 + 3) / 4) * 16);
@@ -1120,6 +1265,10 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       if (PROF) tl_mark(w, 4);
       ++L;
       tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;  // x_T visible
+      if (a.tab_ints) {  // stage x_T in shared memory for the subtree backward tables
+        for (int i = threadIdx.x; i < a.ntT; i += blockDim.x) sv.zs[i] = x[a.ztab[2 * i].x];
+        __syncthreads();
+      }
       sweep_trace(a, step);
     } else {
       for (int t = 0; t < a.ntop; ++t, ++L) {
@@ -1518,6 +1667,7 @@ void SweepStageDeleter::operator()(SweepStage *p) const { delete p; }
 SweepStagePtr sweep_stage_new() { return SweepStagePtr(new SweepStage()); }
 
 static constexpr int kCluster = 16, kWarps = 16;
+static constexpr int kSmemMax = 227 * 1024 - 1536;  // opt-in maximum minus the kernel's static shared memory
 
 // gathered values of a program: vals[b][id] (b = slab if any coupling is per-slab)
 static int gather_values(const CplProgram &pg, const SweepCoupling *cpl, int ncpl, int nrhs, DevBuf &buf,
@@ -1546,13 +1696,9 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   const NDDevice &dev = *fac.dev;
   const NDPlan &p = *dev.plan;
   const int cluster = kCluster, warps = kWarps;
-  // per warp: gather buffer (max front, rounded to 16 doubles) + two TMA slots
-  int64_t maxb = 2;
-  for (int sn = 0; sn < p.nsn; ++sn) maxb = std::max({maxb, p.bsz_f[sn], p.bsz_b[sn]});
-  const int slot = (int)((maxb + 15) / 16 * 16);
-  const int vstride = (int)(((std::max(dev.max_front, 1) + 15) / 16) * 16 + 2 * slot);
-  const int64_t smem_doubles = 224 * 1024 / 8;
-  const NDSweepPlan &sp = dev.get_sweep_plan(cluster, warps, smem_doubles - (int64_t)warps * vstride, s);
+  const int slot = sweep_slot(p);
+  const NDSweepPlan &sp = dev.get_sweep_plan(cluster, warps, kSmemMax / 8, s);
+  const int vstride = sp.vstride;
   const int64_t n = p.n;
   st.fac = &fac;
   st.sp = &sp;
@@ -1593,6 +1739,12 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   a.g3p = sp.g3p.as<int4>();
   a.bpos = sp.bpos.as<int>();
   a.bpos4 = sp.bpos4.as<int>();
+  if (sp.tab_ints) {
+    a.tab = sp.tab.as<int>();
+    a.tab_ptr = sp.tab_ptr.as<int>();
+    a.tab_nf = sp.tab_nf.as<int>();
+    a.tab_ints = sp.tab_ints;
+  }
   a.nlevels = p.nlevels;
   a.nw = cluster * warps;
   a.n = n;
@@ -1644,9 +1796,9 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   a.vstride = vstride;
   a.null_work = env_int2("STMHD_SWEEP_NULL", 0);
   a.post_hdr = nullptr;  // set by sweep_stage_set_post for this launch
-  st.smem = ((size_t)warps * a.vstride + 3 * a.sub_len + a.sub_cb + a.kpad + 2) * sizeof(double) +
-            (size_t)warps * a.tstride;
-  require(st.smem <= 224 * 1024, "nd sweep: subtree vectors or fronts too large for shared memory");
+  st.smem = ((size_t)warps * a.vstride + 3 * a.sub_len + a.sub_cb + a.kpad + 4) * sizeof(double) +
+            (size_t)a.tab_ints * 4 + (size_t)warps * a.tstride;
+  require(st.smem <= (size_t)kSmemMax, "nd sweep: subtree vectors or fronts too large for shared memory");
   // consumers wait on their producers' flags (set at launch)
   a.nwait = next;
   for (int e = 0; e < next; ++e) {
