@@ -594,6 +594,25 @@ __global__ void __launch_bounds__(512, 1) nd_solve_kernel(SolveArgs a) {
   }
 }
 
+// One CTA per right-hand side: every right-hand side is an independent tree solve,
+// so levels only need __syncthreads (the grid-wide version pays a 2.3 us software
+// barrier per level).  Used when there are enough right-hand sides to fill the GPU.
+__global__ void __launch_bounds__(512, 1) nd_solve_cta_kernel(SolveArgs a) {
+  extern __shared__ double vbuf[];
+  const int b = blockIdx.x;
+  const int w = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  double *v = vbuf + w * a.vstride;
+  const double *rhs = a.rhs + (int64_t)b * a.ld_rhs;
+  for (int l = 0; l < a.nlevels; ++l) {
+    for (int i = a.fwd_ptr[l] + w; i < a.fwd_ptr[l + 1]; i += nwarp) warp_forward(a, rhs, a.fwd_items[i], b, v);
+    __syncthreads();
+  }
+  for (int l = a.nlevels - 1; l >= 0; --l) {
+    for (int i = a.bwd_ptr[l] + w; i < a.bwd_ptr[l + 1]; i += nwarp) warp_backward(a, a.bwd_items[i], b, v);
+    __syncthreads();
+  }
+}
+
 // Scratch for batched solves, grown on demand (per process; one stream at a time).
 static double *solve_scratch(size_t doubles) {
   static DevBuf buf;
@@ -644,6 +663,21 @@ void NDFactor::solve(const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x,
     attr = true;
   }
   void *args[] = {&a};
+  static const int cta_min = [] {
+    const char *e = getenv("STMHD_SOLVE_CTA_MIN");
+    return e ? atoi(e) : 8;
+  }();
+  if (nrhs >= cta_min) {  // independent right-hand sides: one CTA each, no grid barrier
+    static bool attr2 = false;
+    if (!attr2) {
+      STMHD_CUDA_CHECK(cudaFuncSetAttribute(nd_solve_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            220 * 1024));
+      attr2 = true;
+    }
+    nd_solve_cta_kernel<<<nrhs, threads, smem, s>>>(a);
+    STMHD_LAUNCH_CHECK();
+    return;
+  }
   STMHD_CUDA_CHECK(cudaLaunchCooperativeKernel((void *)nd_solve_kernel, dim3(num_sms()), dim3(threads), args, smem, s));
   count_launch();
 }

@@ -1762,7 +1762,6 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
     require(ext[e] && ext[e]->sp && ext[e]->nrhs == nrhs, "sweep: external stage not prepared for these slabs");
     st.ext_pos[e] = &ext[e]->sp->pos_h;
   }
-  st.post_prog = nullptr;
   if (ncpl > 0) {
     const std::vector<int> *ext_pos[2] = {nullptr, nullptr};
     for (int e = 0; e < next; ++e) ext_pos[e] = st.ext_pos[e];
@@ -2005,7 +2004,12 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   int nat = 1;
-  if (nst > 1) {  // the stages wait on each other: all clusters must be co-resident
+  // the stages wait on each other: all clusters must be co-resident (cooperative
+  // launch; STMHD_PIPE_COOP=0 drops the attribute for profilers that cannot replay
+  // cooperative cluster launches -- 48 CTAs on 148 SMs are co-resident in practice and
+  // a consumer traps after 4 s instead of hanging)
+  static const int coop_env = env_int2("STMHD_PIPE_COOP", 1);
+  if (nst > 1 && coop_env) {
     at[1].id = cudaLaunchAttributeCooperative;
     at[1].val.cooperative = 1;
     nat = 2;
