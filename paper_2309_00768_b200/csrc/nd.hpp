@@ -180,6 +180,7 @@ struct NDFactor {
   // dense inverse of the top Schur complement per batch entry (nd_sweep.cu), built
   // lazily for the sweep plan that uses it: [nbatch][n_T][kpad] doubles
   mutable DevBuf ktop;
+  mutable DevBuf scratch, bar;  // batched-solve scratch and grid-barrier words (per factor)
   mutable const void *ktop_plan = nullptr;
   mutable uint64_t ktop_gen = ~0ull;
   void factor(const double *values, int64_t value_stride, cudaStream_t s);

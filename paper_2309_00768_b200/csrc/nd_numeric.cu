@@ -613,24 +613,14 @@ __global__ void __launch_bounds__(512, 1) nd_solve_cta_kernel(SolveArgs a) {
   }
 }
 
-// Scratch for batched solves, grown on demand (per process; one stream at a time).
-static double *solve_scratch(size_t doubles) {
-  static DevBuf buf;
-  if (buf.bytes < doubles * sizeof(double)) {
-    STMHD_CUDA_CHECK(cudaDeviceSynchronize());
-    buf.alloc(doubles * sizeof(double) * 5 / 4 + 1024);
-  }
-  return buf.as<double>();
-}
 
 void NDFactor::solve(const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,
                      cudaStream_t s) const {
   const NDPlan &p = *dev->plan;
   require(nbatch == 1 || nrhs <= nbatch, "lu solve: more right-hand sides than factors");
-  static DevBuf bar;
   if (!bar.ptr) {
-    bar.alloc(2 * sizeof(unsigned));
-    STMHD_CUDA_CHECK(cudaMemset(bar.ptr, 0, 2 * sizeof(unsigned)));
+    bar.alloc_async(2 * sizeof(unsigned), s);
+    STMHD_CUDA_CHECK(cudaMemsetAsync(bar.ptr, 0, 2 * sizeof(unsigned), s));
   }
   SolveArgs a{};
   a.fwd_items = dev->fwd_items.as<SolveItem>();
@@ -647,7 +637,10 @@ void NDFactor::solve(const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x,
   a.x = x;
   a.ld_x = ld_x;
   a.nrhs = nrhs;
-  double *scr = solve_scratch((size_t)nrhs * (p.n + p.cbv_size));
+  // per-factor scratch from the stream-ordered pool (factors may solve on different streams)
+  const size_t need = (size_t)nrhs * (p.n + p.cbv_size) * sizeof(double);
+  if (scratch.bytes < need) scratch.alloc_async(need, s);
+  double *scr = scratch.as<double>();
   a.ybuf = scr;
   a.n = p.n;
   a.cbv = scr + (int64_t)nrhs * p.n;

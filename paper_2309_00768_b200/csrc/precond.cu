@@ -386,11 +386,22 @@ void PC::coupling_u(const double *z, int64_t lz, double beta, const double *xs, 
 // path up to the summation order of the coupled right-hand sides.
 void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
   const double *r_u = r, *r_p = r + o_p, *r_j = r + o_j, *r_a = r + o_a;
-  // batched (slab-parallel) pre-steps: wave right-hand side and the pressure block
-  d->lu_ma->solve(r_a, slab, ta1.as<double>(), n_a, nt, s);
-  apply_potential(ta1.as<double>(), n_a, ta2.as<double>(), n_a, s);
-  pressure_schur_inverse(r_p, slab, x + o_p, slab, s);
+  // batched (slab-parallel) pre-steps; the pressure chain runs on a second stream,
+  // overlapped with the wave right-hand side, and joins before the velocity stage
+  // process-wide side stream and events (never destroyed: pooled buffers allocated on
+  // the side stream may be freed on it after this preconditioner is gone)
+  static cudaStream_t side = nullptr;
+  static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (!side) {
+    STMHD_CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    STMHD_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    STMHD_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  }
+  STMHD_CUDA_CHECK(cudaEventRecord(ev_fork, s));
+  STMHD_CUDA_CHECK(cudaStreamWaitEvent(side, ev_fork, 0));
+  pressure_schur_inverse(r_p, slab, x + o_p, slab, side);
   {  // tu1 = r_u - B^T x_p
+    cudaStream_t s = side;
     SpmvArgs a;
     a.nrows = n_u;
     a.nslab = nt;
@@ -403,6 +414,9 @@ void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
     a.nterms = 1;
     spmv(a, s, 8);
   }
+  STMHD_CUDA_CHECK(cudaEventRecord(ev_join, side));
+  d->lu_ma->solve(r_a, slab, ta1.as<double>(), n_a, nt, s);
+  apply_potential(ta1.as<double>(), n_a, ta2.as<double>(), n_a, s);
   if (!st_wave) {
     st_wave = sweep_stage_new();
     st_mj = sweep_stage_new();
@@ -432,6 +446,7 @@ void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
   cu.lag = 1;
   cu.coef = 1.0;
   SweepStage *ju[1] = {st_mj.get()};
+  STMHD_CUDA_CHECK(cudaStreamWaitEvent(s, ev_join, 0));  // tu1 (pressure chain) ready
   sweep_stage_prepare(*st_vel, *fu, tu1.as<double>(), n_u, x, slab, nt, &cu, 1, ju, 1, s, tag);
   // after slab k of the M_j stage: rhs_u(k) += -Z_j x_j(k) - Z_a x_A(k)
   SweepCoupling cz[2];
