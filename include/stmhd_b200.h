@@ -137,6 +137,13 @@ int stmhd_lu_factor(stmhd_lu lu, void *stream, const double *values, int64_t val
    (nbatch==1 ? 0 : b).  Vectors: rhs[b*ld + i]. */
 int stmhd_lu_solve(stmhd_lu lu, void *stream, const double *rhs, int64_t ld_rhs, double *x,
                    int64_t ld_x, int nrhs);
+/* sequential sweep over nrhs slabs (factor b for slab b, or 0 if nbatch == 1):
+     x_b = A_b^{-1} (rhs_b + c_coef * C x_{b-1})       (C may be NULL: independent solves)
+   C in CSR (device arrays).  Reference: solve_potential / solve_velocity,
+   precond.py:122-131,173-180; oracle/c5.py C5.solve. */
+int stmhd_lu_sweep(stmhd_lu lu, void *stream, const double *rhs, int64_t ld_rhs, double *x,
+                   int64_t ld_x, int nrhs, const int32_t *c_rowptr, const int32_t *c_col,
+                   const double *c_val, double c_coef);
 /* storage diagnostics: [0] factor doubles per matrix, [1] supernodes, [2] levels,
    [3] max front, [4] symbolic nnz(L+U) per matrix */
 int stmhd_lu_info(stmhd_lu lu, int64_t *info5);
@@ -145,6 +152,23 @@ int stmhd_lu_info(stmhd_lu lu, int64_t *info5);
    workspace doubles, [6] CB-vector doubles, [7] forward work items */
 int stmhd_nd_plan_info(int64_t n, const int32_t *rowptr, const int32_t *col, const int32_t *gx,
                        const int32_t *gy, int leaf_max, int64_t *info8);
+
+/* ---- configuration-5 scalar advection-diffusion block (oracle/c5.py) ----
+   values[k*nnz + e] = base[e] + sum over the entry's element contributions cinfo
+   ({element, local row i, local col j, orientation o}, ranges cptr) of
+   sum_c grad12[o][j][c] * sum_m mloc9[i][m] * u[k][node_m][c]
+   (the P1 advection term int psi_i (u_k . grad psi_j), reference fem.py:430-462 with a
+   P1 vector velocity).  Device arrays except mloc9 / grad12 (host, 9 / 12 doubles). */
+int stmhd_c5_values(void *stream, int64_t nnz, int nt, const double *base, const int32_t *cptr,
+                    const int32_t *cinfo, const int32_t *elem, const double *u, int64_t n_nodes,
+                    const double *mloc9, const double *grad12, double *values);
+/* block-bidiagonal batched SpMV: y_k = F_k x_k + c_coef * C x_{k-1} (F per slab with
+   value stride val_stride, C shared, may be NULL).  oracle/c5.py C5.apply;
+   the space-time Jacobian's structure (spacetime.py:131-153). */
+int stmhd_bidiag_spmv(void *stream, int64_t n, int nt, const int32_t *rowptr, const int32_t *col,
+                      const double *vals, int64_t val_stride, const int32_t *c_rowptr,
+                      const int32_t *c_col, const double *c_val, double c_coef, const double *x,
+                      double *y);
 
 #ifdef __cplusplus
 }

@@ -34,3 +34,157 @@ def c5_velocity_fields(coords: np.ndarray, nt: int, seed: int = 0) -> np.ndarray
         out[k, :, 0] = ux / scale
         out[k, :, 1] = uy / scale
     return out
+
+
+def c5_host_tables(n: int, dt: float = 1e-2, eps: float = 1e-3) -> dict:
+    """Host side of the configuration-5 operator: the fixed pattern (element couplings,
+    Dirichlet rows and columns reduced to the diagonal as bc_identity leaves them), the constant
+    part M/dt + eps K per entry, every entry's element contributions
+    {element, local row, local col, orientation} for the device advection assembly, the
+    P1 element mass / gradient tensors, and C = bc_zero(M/dt)."""
+    import scipy.sparse as sp
+
+    from . import fem
+
+    mesh = fem.Mesh(-1.0, 1.0, -1.0, 1.0, n, n)
+    p1 = fem.Space(mesh, 1)
+    nn = p1.n_nodes
+    T = fem.element_tensors(1, 1, mesh.hx, mesh.hy)
+    bc = np.unique(np.concatenate([p1.side_nodes["top"], p1.side_nodes["bottom"]]))
+    isbc = np.zeros(nn, dtype=bool)
+    isbc[bc] = True
+    el = p1.elem
+    ne = len(el)
+    rows = np.repeat(el[:, :, None], 3, axis=2).ravel()
+    cols = np.repeat(el[:, None, :], 3, axis=1).ravel()
+    keys = np.unique(rows * nn + cols)
+    # bc_identity clears the rows AND columns of Dirichlet nodes, then sets the diagonal
+    keys = keys[(~isbc[keys // nn] & ~isbc[keys % nn]) | (keys // nn == keys % nn)]
+    keys = np.union1d(keys, bc * nn + bc)
+    prow, pcol = keys // nn, keys % nn
+    nnz = len(keys)
+    o = np.arange(ne) & 1
+    li = np.tile(np.repeat(np.arange(3), 3), ne)
+    lj = np.tile(np.tile(np.arange(3), 3), ne)
+    eid = np.repeat(np.arange(ne), 9)
+    keep = ~isbc[rows] & ~isbc[cols]
+    ent = np.searchsorted(keys, rows * nn + cols)
+    base = np.zeros(nnz)
+    loc = (np.asarray(T["M1"])[None, :, :] / dt + eps * np.asarray(T["K1"])[o]).reshape(-1)
+    np.add.at(base, ent[keep], loc[keep])
+    base[np.searchsorted(keys, bc * nn + bc)] = 1.0
+    order = np.argsort(ent[keep], kind="stable")
+    ce = ent[keep][order]
+    cinfo = np.column_stack([eid[keep][order], li[keep][order], lj[keep][order], o[eid[keep][order]]])
+    m = fem._assemble(p1, p1, [T["M1"], T["M1"]]).tocsr()
+    keepc = sp.diags((~isbc).astype(float))
+    cmat = (keepc @ (m / dt) @ keepc).tocsr()
+    cmat.eliminate_zeros()
+    cmat.sort_indices()
+    return dict(p1=p1, bc=bc, nnz=nnz, rowptr=np.searchsorted(prow, np.arange(nn + 1)).astype(np.int32),
+                col=pcol.astype(np.int32), base=base, cptr=np.searchsorted(ce, np.arange(nnz + 1)).astype(np.int32),
+                cinfo=cinfo.astype(np.int32),
+                mloc=np.ascontiguousarray(np.asarray(T["M1"], dtype=np.float64).reshape(-1)),
+                grad=np.ascontiguousarray(np.asarray(T["G1"], dtype=np.float64).reshape(-1)), coupling=cmat)
+
+
+class C5Operator:
+    """Configuration-5 scalar advection-diffusion space-time block on the device
+    (SURVEY 8(d)); the same interface as the CPU restatement ``oracle/c5.py C5``.
+
+    Per slab F_k = M/dt + eps K + W(u_k) on a P1 space of the n x n mesh of [-1,1]^2
+    (W: reference fem.py:430-462, ``lin_a`` with a P1 vector velocity), Dirichlet
+    rows/columns of the top/bottom nodes replaced by the identity (fem.py:593-600); sub-diagonal -C with
+    C = bc_zero(M/dt) (fem.py:603-610).  ``apply`` is the block-bidiagonal batched
+    SpMV, ``solve`` the exact inverse by sequential block forward substitution
+    (reference solve_potential, precond.py:173-180) on the cluster sweep, with one
+    nested-dissection LU per slab."""
+
+    def __init__(self, n: int, nt: int, ufields=None, seed: int = 0, dt: float = 1e-2, eps: float = 1e-3,
+                 leaf: int = 32):
+        import torch
+
+        from . import _lib
+        from .linalg import DEV, _LUHandle
+
+        self.n_cells, self.nt, self.dt, self.eps = n, nt, dt, eps
+        h = c5_host_tables(n, dt, eps)
+        p1 = h["p1"]
+        self.p1, self.n, self.bc, self.nnz = p1, p1.n_nodes, h["bc"], h["nnz"]
+        self.rowptr, self.col, self.coupling = h["rowptr"], h["col"], h["coupling"]
+        self._mloc, self._grad = h["mloc"], h["grad"]
+        base, cptr, cinfo, el, cmat = h["base"], h["cptr"], h["cinfo"], p1.elem, h["coupling"]
+        tens = lambda a, dt_=torch.int32: torch.as_tensor(np.ascontiguousarray(a), dtype=dt_, device=DEV)
+        self._d = dict(rowptr=tens(self.rowptr), col=tens(self.col), base=tens(base, torch.float64),
+                       cptr=tens(cptr), cinfo=tens(cinfo.astype(np.int32)), elem=tens(el.astype(np.int32)),
+                       c_rowptr=tens(cmat.indptr.astype(np.int32)), c_col=tens(cmat.indices.astype(np.int32)),
+                       c_val=tens(cmat.data, torch.float64))
+        if ufields is None:
+            ufields = c5_velocity_fields(p1.coords, nt, seed)
+        self.u = torch.as_tensor(np.ascontiguousarray(ufields, dtype=np.float64), device=DEV)
+        self.values = torch.empty(nt * self.nnz, dtype=torch.float64, device=DEV)
+        self._lib = _lib.load()
+        self._lu = None
+        self._leaf = leaf
+        self._grid = (p1.gi, p1.gj)
+        self._handle_cls = _LUHandle
+        self.assemble()
+
+    def assemble(self):
+        """Every slab's F_k values on the device (stmhd_c5_values)."""
+        from . import _lib
+
+        d = self._d
+        _lib.check(self._lib.stmhd_c5_values(_lib.stream_ptr(), self.nnz, self.nt, _lib.ptr(d["base"]),
+                                             _lib.ptr(d["cptr"]), _lib.ptr(d["cinfo"]), _lib.ptr(d["elem"]),
+                                             _lib.ptr(self.u), self.n, _lib.ptr(self._mloc), _lib.ptr(self._grad),
+                                             _lib.ptr(self.values)))
+
+    def matrix(self, k: int):
+        """F_k as scipy CSR (tests / inspection)."""
+        import scipy.sparse as sp
+
+        v = self.values[k * self.nnz:(k + 1) * self.nnz].cpu().numpy()
+        return sp.csr_matrix((v, self.col, self.rowptr), shape=(self.n, self.n))
+
+    def apply(self, x, out=None):
+        """y_k = F_k x_k - C x_{k-1} (oracle C5.apply)."""
+        import torch
+
+        from . import _lib
+        from .linalg import as_device
+
+        x = as_device(x).reshape(-1).contiguous()
+        out = torch.empty_like(x) if out is None else out
+        d = self._d
+        _lib.check(self._lib.stmhd_bidiag_spmv(_lib.stream_ptr(), self.n, self.nt, _lib.ptr(d["rowptr"]),
+                                               _lib.ptr(d["col"]), _lib.ptr(self.values), self.nnz,
+                                               _lib.ptr(d["c_rowptr"]), _lib.ptr(d["c_col"]), _lib.ptr(d["c_val"]),
+                                               -1.0, _lib.ptr(x), _lib.ptr(out)))
+        return out
+
+    def factor(self):
+        """One nested-dissection LU per slab (batched, shared symbolic structure)."""
+        import scipy.sparse as sp
+
+        if self._lu is None:
+            pat = sp.csr_matrix((np.ones(self.nnz), self.col, self.rowptr), shape=(self.n, self.n))
+            self._lu = self._handle_cls(pat, self.nt, self._grid[0], self._grid[1], self._leaf)
+        self._lu.factor(self.values, self.nnz)
+
+    def solve(self, r, out=None):
+        """x_k = F_k^{-1}(r_k + C x_{k-1}) sequentially (oracle C5.solve)."""
+        import torch
+
+        from . import _lib
+        from .linalg import as_device
+
+        if self._lu is None:
+            self.factor()
+        r = as_device(r).reshape(-1).contiguous()
+        out = torch.empty_like(r) if out is None else out
+        d = self._d
+        _lib.check(self._lib.stmhd_lu_sweep(self._lu.h, _lib.stream_ptr(), _lib.ptr(r), self.n, _lib.ptr(out),
+                                            self.n, self.nt, _lib.ptr(d["c_rowptr"]), _lib.ptr(d["c_col"]),
+                                            _lib.ptr(d["c_val"]), 1.0))
+        return out

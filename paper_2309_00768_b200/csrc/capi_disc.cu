@@ -2,22 +2,12 @@
 // preconditioner and Krylov kernels (see include/stmhd_b200.h).
 #include <cstring>
 
+#include "capi_common.hpp"
+
 #include "pc.hpp"
 
 using namespace stmhd;
 
-#define CAPI_BEGIN try {
-#define CAPI_END                                   \
-  return STMHD_OK;                                 \
-  }                                                \
-  catch (const stmhd::Error &e) {                  \
-    stmhd::set_last_error(e.what(), e.block);      \
-    return e.status;                               \
-  }                                                \
-  catch (const std::exception &e) {                \
-    stmhd::set_last_error(e.what());               \
-    return STMHD_CONFIG;                           \
-  }
 
 int64_t stmhd_disc_s::I(const char *k) const {
   auto it = ints.find(k);

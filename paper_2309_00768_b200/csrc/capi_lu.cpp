@@ -2,6 +2,8 @@
 // (drop-in for reference LUFactor, pkg/src/stmhd/linalg.py:71-96).
 #include <cstring>
 
+#include "capi_common.hpp"
+
 #include "nd.hpp"
 
 #include <atomic>
@@ -25,18 +27,6 @@ struct stmhd_lu_s {
   NDFactor fac;
 };
 
-#define CAPI_BEGIN try {
-#define CAPI_END                                   \
-  return STMHD_OK;                                 \
-  }                                                \
-  catch (const stmhd::Error &e) {                  \
-    stmhd::set_last_error(e.what(), e.block);      \
-    return e.status;                               \
-  }                                                \
-  catch (const std::exception &e) {                \
-    stmhd::set_last_error(e.what());               \
-    return STMHD_CONFIG;                           \
-  }
 
 extern "C" {
 
@@ -94,6 +84,26 @@ int stmhd_lu_solve(stmhd_lu lu, void *stream, const double *rhs, int64_t ld_rhs,
   require(lu->fac.factors.ptr, "stmhd_lu_solve: not factored");
   lu->fac.solve(rhs, ld_rhs, x, ld_x, nrhs, (cudaStream_t)stream);
   STMHD_LAUNCH_CHECK();
+  CAPI_END
+}
+
+int stmhd_lu_sweep(stmhd_lu lu, void *stream, const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x,
+                   int nrhs, const int32_t *c_rowptr, const int32_t *c_col, const double *c_val, double c_coef) {
+  CAPI_BEGIN
+  require(lu && rhs && x && nrhs >= 1, "stmhd_lu_sweep: bad arguments");
+  require(lu->fac.factors.ptr, "stmhd_lu_sweep: not factored");
+  require(lu->fac.nbatch == 1 || lu->fac.nbatch >= nrhs, "stmhd_lu_sweep: more slabs than factors");
+  SweepCoupling c;
+  int ncpl = 0;
+  if (c_rowptr) {
+    c.rowptr = c_rowptr;
+    c.col = c_col;
+    c.val = c_val;
+    c.lag = 1;
+    c.coef = c_coef;
+    ncpl = 1;
+  }
+  lu->fac.sweep(rhs, ld_rhs, x, ld_x, nrhs, ncpl ? &c : nullptr, ncpl, (cudaStream_t)stream);
   CAPI_END
 }
 

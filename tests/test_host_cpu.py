@@ -174,3 +174,34 @@ def test_overhead_ratio_arithmetic_and_errors():
         compute_overhead_ratios(st, frozen)
     with pytest.raises(ConfigurationError):
         compute_overhead_ratios(seq, st)
+
+
+def test_c5_host_tables_match_reference(golden):
+    """The configuration-5 tables the device assembly consumes, contracted on the host
+    in numpy, reproduce the reference's F_k (golden, make_golden.py c5_case) and its
+    coupling bc_zero(M/dt) -- pattern exactly, values to 1e-12."""
+    from conftest import csr_from
+    from paper_2309_00768_b200.c5 import c5_host_tables
+
+    g = golden("c5_tiny")
+    h = c5_host_tables(8)
+    nn = h["p1"].n_nodes
+    el = h["p1"].elem
+    mloc = h["mloc"].reshape(3, 3)
+    grad = h["grad"].reshape(2, 3, 2)
+    for k in range(g["ufields"].shape[0]):
+        u = g["ufields"][k]
+        vals = h["base"].copy()
+        for e in range(h["nnz"]):
+            for j in range(h["cptr"][e], h["cptr"][e + 1]):
+                elem, i, jj, o = h["cinfo"][j]
+                s = mloc[i] @ u[el[elem]]  # sum_m M[i][m] u[node_m][c]
+                vals[e] += grad[o, jj] @ s
+        mine = sp.csr_matrix((vals, h["col"], h["rowptr"]), shape=(nn, nn))
+        ref = csr_from(g, f"F{k}")
+        np.testing.assert_array_equal(mine.indptr, ref.indptr)
+        np.testing.assert_array_equal(mine.indices, ref.indices)
+        assert np.max(np.abs(mine.data - ref.data)) <= 1e-12 * np.max(np.abs(ref.data))
+    ref_c = csr_from(g, "coupling")
+    assert abs(h["coupling"] - ref_c).max() <= 1e-12 * abs(ref_c).max()
+    np.testing.assert_array_equal(np.sort(h["bc"]), np.sort(g["bc"]))
