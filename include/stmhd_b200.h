@@ -84,6 +84,11 @@ int stmhd_assemble(stmhd_disc d, void *stream, const double *state, const double
 /* ---- K2: space-time Jacobian matvec y = J x (spacetime.py:131-153) ---- */
 int stmhd_jac_apply(stmhd_disc d, void *stream, const double *slab_values, const double *x,
                     double *y);
+/* the same J.v from the sliced-ELL copy of the slab values (stspmv.cu): size per slab
+   (-1 on error), relayout once per assembly, apply */
+int64_t stmhd_jac_sell_size(stmhd_disc d, void *stream);
+int stmhd_jac_relayout(stmhd_disc d, void *stream, const double *slab_values, double *sell);
+int stmhd_jac_apply_sell(stmhd_disc d, void *stream, const double *sell, const double *x, double *y);
 
 /* ---- K3-K6: preconditioner (precond.py:67-301) ----
    variant: 0 TRIANGULAR, 1 SIMPLIFIED, 2 FULL (precond.py:40-43).
@@ -169,6 +174,28 @@ int stmhd_bidiag_spmv(void *stream, int64_t n, int nt, const int32_t *rowptr, co
                       const double *vals, int64_t val_stride, const int32_t *c_rowptr,
                       const int32_t *c_col, const double *c_val, double c_coef, const double *x,
                       double *y);
+
+/* ---- sliced-ELL space-time SpMV plan (stspmv.cu) ----
+   y_k = alpha * A_k x_k + c_coef * C x_{k + rel}  for k in [0, nt), x and y with slab
+   stride n.  A: per-slab values (stride val_stride) on the CSR pattern (rowptr, col);
+   C: shared values on (c_rowptr, c_col) (may be NULL), its columns shifted by
+   c_col_shift into slab-relative form (-n: C couples slab k-1; negative relative
+   columns are skipped at k = 0).  The space-time Jacobian (spacetime.py:131-153) and
+   configuration 5's F_k / -C bidiagonal (oracle/c5.py C5.apply).  Index arrays and
+   c_val are HOST memory (copied); values and vectors device memory. */
+typedef struct stmhd_spmv_s *stmhd_spmv;
+int stmhd_spmv_create(int64_t n, const int32_t *rowptr, const int32_t *col, const int32_t *c_rowptr,
+                      const int32_t *c_col, const double *c_val, int32_t c_col_shift, void *stream,
+                      stmhd_spmv *out);
+int stmhd_spmv_destroy(stmhd_spmv plan);
+/* per-slab length of the sliced-ELL value array (rows sorted by length in windows of
+   128 and cut into slices of 32, entries column-major per slice, padded) */
+int64_t stmhd_spmv_sell_size(stmhd_spmv plan);
+/* sell[k*sell_size + e] <- vals[k*val_stride + csr index of e] for k < nt (once per assembly) */
+int stmhd_spmv_relayout(stmhd_spmv plan, void *stream, int nt, const double *vals, int64_t val_stride,
+                        double *sell);
+int stmhd_spmv_apply(stmhd_spmv plan, void *stream, int nt, const double *sell, double alpha, double c_coef,
+                     const double *x, double *y);
 
 #ifdef __cplusplus
 }

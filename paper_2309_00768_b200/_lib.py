@@ -53,6 +53,14 @@ _SIGS = {
     "stmhd_c5_values": (c_int, [P, c_i64, c_int, P, P, P, P, P, c_i64, P, P, P]),
     "stmhd_bidiag_spmv": (c_int, [P, c_i64, c_int, P, P, P, c_i64, P, P, P, c_dbl, P, P]),
     "stmhd_nd_plan_info": (c_int, [c_i64, P, P, P, P, c_int, P]),
+    "stmhd_spmv_create": (c_int, [c_i64, P, P, P, P, P, C.c_int32, P, C.POINTER(c_vp)]),
+    "stmhd_spmv_destroy": (c_int, [c_vp]),
+    "stmhd_spmv_sell_size": (c_i64, [c_vp]),
+    "stmhd_spmv_relayout": (c_int, [c_vp, P, c_int, P, c_i64, P]),
+    "stmhd_spmv_apply": (c_int, [c_vp, P, c_int, P, c_dbl, c_dbl, P, P]),
+    "stmhd_jac_sell_size": (c_i64, [c_vp, P]),
+    "stmhd_jac_relayout": (c_int, [c_vp, P, P, P]),
+    "stmhd_jac_apply_sell": (c_int, [c_vp, P, P, P, P]),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -134,6 +134,7 @@ class C5Operator:
         """Every slab's F_k values on the device (stmhd_c5_values)."""
         from . import _lib
 
+        self._sell = None  # the sliced-ELL copy follows the values
         d = self._d
         _lib.check(self._lib.stmhd_c5_values(_lib.stream_ptr(), self.nnz, self.nt, _lib.ptr(d["base"]),
                                              _lib.ptr(d["cptr"]), _lib.ptr(d["cinfo"]), _lib.ptr(d["elem"]),
@@ -156,12 +157,44 @@ class C5Operator:
 
         x = as_device(x).reshape(-1).contiguous()
         out = torch.empty_like(x) if out is None else out
-        d = self._d
-        _lib.check(self._lib.stmhd_bidiag_spmv(_lib.stream_ptr(), self.n, self.nt, _lib.ptr(d["rowptr"]),
-                                               _lib.ptr(d["col"]), _lib.ptr(self.values), self.nnz,
-                                               _lib.ptr(d["c_rowptr"]), _lib.ptr(d["c_col"]), _lib.ptr(d["c_val"]),
-                                               -1.0, _lib.ptr(x), _lib.ptr(out)))
+        _lib.check(self._lib.stmhd_spmv_apply(self._spmv_plan(), _lib.stream_ptr(), self.nt, _lib.ptr(self._sell),
+                                              1.0, -1.0, _lib.ptr(x), _lib.ptr(out)))
         return out
+
+    def _spmv_plan(self):
+        """Row-block plan of the slab-looped SpMV (stmhd_spmv_create), built once."""
+        import ctypes
+
+        from . import _lib
+
+        if getattr(self, "_plan", None) is None:
+            h = ctypes.c_void_p()
+            rp = np.ascontiguousarray(self.rowptr, dtype=np.int32)
+            cl = np.ascontiguousarray(self.col, dtype=np.int32)
+            crp = np.ascontiguousarray(self.coupling.indptr, dtype=np.int32)
+            ccl = np.ascontiguousarray(self.coupling.indices, dtype=np.int32)
+            cvl = np.ascontiguousarray(self.coupling.data, dtype=np.float64)
+            _lib.check(self._lib.stmhd_spmv_create(self.n, rp.ctypes.data, cl.ctypes.data, crp.ctypes.data,
+                                                   ccl.ctypes.data, cvl.ctypes.data, -self.n, _lib.stream_ptr(),
+                                                   ctypes.byref(h)))
+            self._plan = h.value
+            self._sell = None
+        if self._sell is None:
+            import torch
+
+            n = self._lib.stmhd_spmv_sell_size(self._plan)
+            self._sell = torch.empty(self.nt * n, dtype=torch.float64, device=self.values.device)
+            _lib.check(self._lib.stmhd_spmv_relayout(self._plan, _lib.stream_ptr(), self.nt, _lib.ptr(self.values),
+                                                     self.nnz, _lib.ptr(self._sell)))
+        return self._plan
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan is not None:
+            try:
+                self._lib.stmhd_spmv_destroy(plan)
+            except Exception:
+                pass
 
     def factor(self):
         """One nested-dissection LU per slab (batched, shared symbolic structure)."""

@@ -186,6 +186,48 @@ int stmhd_jac_apply(stmhd_disc d, void *stream, const double *js, const double *
   CAPI_END
 }
 
+// J.v in the sliced-ELL layout (stspmv.cu): per-slab merged rows [f_u|z_j|z_a ; y|f_a]
+// + the shared couplings (B^T, B, M_j, K_jA, -M/dt with slab-relative columns reaching
+// into slab k-1); plan built once from the host patterns.
+static const StSpmvPlan &jv_plan(stmhd_disc d, cudaStream_t s) {
+  if (!d->jv_plan) {
+    auto p = std::make_unique<StSpmvPlan>();
+    p->build((int)d->slab(), d->H("js_rowptr").as<int>(), d->H("js_col").as<int>(), d->H("jc_rowptr").as<int>(),
+             d->H("jc_col").as<int>(), d->H("jc_val").as<double>(), 0, s);
+    d->jv_plan = std::move(p);
+  }
+  return *d->jv_plan;
+}
+
+int64_t stmhd_jac_sell_size(stmhd_disc d, void *stream) {
+  try {
+    if (!d || !d->finalized) return -1;
+    return jv_plan(d, (cudaStream_t)stream).sell_a;
+  } catch (const Error &e) {
+    set_last_error(e.what(), e.block);
+    return -1;
+  }
+}
+
+int stmhd_jac_relayout(stmhd_disc d, void *stream, const double *js, double *sell) {
+  CAPI_BEGIN
+  require(d && d->finalized && js && sell, "stmhd_jac_relayout: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  jv_plan(d, s).relayout((int)d->I("nt"), js, d->I("nnz_js"), sell, s);
+  CAPI_END
+}
+
+int stmhd_jac_apply_sell(stmhd_disc d, void *stream, const double *sell, const double *x, double *y) {
+  CAPI_BEGIN
+  require(d && d->finalized && sell && x && y, "stmhd_jac_apply_sell: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t slab = d->slab();
+  jv_plan(d, s).apply((int)d->I("nt"), sell, 1.0, 1.0, x, slab, y, slab, s);
+  const int o_p = (int)d->I("n_u"), pin = (int)d->I("p_pin");
+  dense_row(d->D<double>("p_mean_row"), (int)d->I("n_p"), x + o_p, slab, y + o_p + pin, slab, (int)d->I("nt"), 1.0, s);
+  CAPI_END
+}
+
 int stmhd_pc_create(stmhd_disc d, void *stream, const double *js, const double *fp, const double *alf, int variant,
                     stmhd_pc *out) {
   CAPI_BEGIN

@@ -6,6 +6,7 @@
 #include <unordered_map>
 
 #include "nd.hpp"
+#include "stspmv.hpp"
 
 struct stmhd_disc_s;
 
@@ -70,6 +71,7 @@ struct stmhd_disc_s {
   std::unique_ptr<stmhd::NDDevice> dev_fu, dev_ca, dev_fa, dev_fp, dev_mj, dev_ma, dev_mp, dev_kp;
   std::unique_ptr<stmhd::NDFactor> lu_mj, lu_ma, lu_mp, lu_kp;
   stmhd::DevBuf clamped;  // nt*slab clamped state workspace
+  std::unique_ptr<stmhd::StSpmvPlan> jv_plan;  // J.v row blocks (built at the first apply)
 
   int64_t I(const char *k) const;
   double R(const char *k) const;

@@ -289,7 +289,8 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
         }
     const int nT = (int)tpos.size();
     std::vector<std::array<int, 4>> zc(nT, {-1, -1, -1, -1});
-    bool ok = nT > 0 && nT <= 4096;
+    // K (nT^2 per slab) may not outgrow the factor itself (batched per-slab factors)
+    bool ok = nT > 0 && nT <= 4096 && (int64_t)nT * nT <= p.factor_size;
     for (int r : roots) {  // subtree roots' updates land on top unknowns
       for (int a = 0; a < p.nb[r] && ok; ++a) {
         const int tgt = bpos[p.idx_off[r] + p.ns[r] + a];
@@ -1659,6 +1660,7 @@ struct SweepStage {
   // gathered coupling values are reused while (tag, program) are unchanged (tag 0:
   // always regather)
   int64_t vals_tag = 0, post_tag = 0;
+  int warps = 0;  // warps per CTA (0: not chosen yet)
   const std::vector<int> *ext_pos[2] = {nullptr, nullptr};
   const CplProgram *vals_prog = nullptr, *post_prog = nullptr;
 };
@@ -1695,8 +1697,19 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
                          int next, cudaStream_t s, int64_t vals_tag) {
   const NDDevice &dev = *fac.dev;
   const NDPlan &p = *dev.plan;
-  const int cluster = kCluster, warps = kWarps;
+  const int cluster = kCluster;
   const int slot = sweep_slot(p);
+  // warps per CTA: 16, halved while the plan's shared memory does not fit (large
+  // slabs such as configuration 5); the choice sticks to the stage
+  auto smem_of = [&](const NDSweepPlan &c, int w) {
+    const size_t tstr = ((c.nl + 1 + 3) / 4) * 16 + (size_t)c.max_wtasks * sizeof(SweepTask);
+    return ((size_t)w * c.vstride + 3 * c.sub_len + c.sub_cb + c.kpad + 4) * sizeof(double) + (size_t)c.tab_ints * 4 +
+           (size_t)w * tstr;
+  };
+  int warps = st.warps ? st.warps : kWarps;
+  while (!st.warps && warps > 4 && smem_of(dev.get_sweep_plan(cluster, warps, kSmemMax / 8, s), warps) > (size_t)kSmemMax)
+    warps /= 2;
+  st.warps = warps;
   const NDSweepPlan &sp = dev.get_sweep_plan(cluster, warps, kSmemMax / 8, s);
   const int vstride = sp.vstride;
   const int64_t n = p.n;
@@ -1946,7 +1959,9 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
       st.a.flag_out = nullptr;
     }
     smem = std::max(smem, st.smem);
+    require(st.warps == stg[0]->warps, "sweep: stages of one launch need the same warps per CTA");
   }
+  const int warps = stg[0]->warps;
   for (int i = 0; i < nst; ++i) {
     SweepStage &st = *stg[i];
     for (int e = 0; e < st.a.nwait; ++e) {
@@ -1987,15 +2002,15 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
   DevBuf pr;
   DevBuf tlb;
   if (prof_on) {
-    pr.alloc((size_t)kCluster * kWarps * 8 * sizeof(unsigned long long));
+    pr.alloc((size_t)kCluster * warps * 8 * sizeof(unsigned long long));
     m.st[ts].prof = pr.as<unsigned long long>();
-    tlb.alloc((size_t)kWarps * 128 * sizeof(unsigned long long));
+    tlb.alloc((size_t)warps * 128 * sizeof(unsigned long long));
     STMHD_CUDA_CHECK(cudaMemsetAsync(tlb.ptr, 0, tlb.bytes, s));
     m.st[ts].tline = tlb.as<unsigned long long>();
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kCluster * nst);
-  cfg.blockDim = dim3(kWarps * 32);
+  cfg.blockDim = dim3(warps * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
@@ -2047,7 +2062,7 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
             (long long)a.sub_cb);
   }
   if (prof_on) {
-    const int nwp = kCluster * kWarps;
+    const int nwp = kCluster * warps;
     std::vector<unsigned long long> h((size_t)nwp * 8);
     STMHD_CUDA_CHECK(cudaMemcpyAsync(h.data(), pr.ptr, h.size() * 8, cudaMemcpyDeviceToHost, s));
     STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -2065,12 +2080,12 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
             mean[4] / nrhs0, mx[4] / nrhs0, mean[5] / nrhs0, mx[5] / nrhs0, mean[6] * us, mean[7] * us);
     // timeline of slab 1, CTA 0: per warp, events (1 level start fwd, 2 gathered, 3 chunk, 4 level done fwd,
     // 5 level start bwd, 6 level done bwd) in us from the first event
-    std::vector<unsigned long long> tv((size_t)kWarps * 128);
+    std::vector<unsigned long long> tv((size_t)warps * 128);
     STMHD_CUDA_CHECK(cudaMemcpy(tv.data(), tlb.ptr, tv.size() * 8, cudaMemcpyDeviceToHost));
     unsigned long long t0 = ~0ull;
     for (auto v : tv)
       if (v) t0 = std::min(t0, v & ((1ull << 56) - 1));
-    for (int wv = 0; wv < kWarps; ++wv) {
+    for (int wv = 0; wv < warps; ++wv) {
       fprintf(stderr, "[tl] w%02d:", wv);
       for (int i = 0; i < 128; ++i) {
         const unsigned long long v = tv[(size_t)wv * 128 + i];

@@ -181,6 +181,7 @@ class Discretization:
         big = sp.hstack([prev, cur]).tocsr()
         rp, ci, va = csr_arrays(big)
         up("jc_rowptr", rp), up("jc_col", ci.astype(np.int64) - L.slab_size), up("jc_val", va)
+        self.jc_nnz = len(ci)
         # preconditioner CSRs (field-local coordinates)
         for key, mat in (("mu_dt", self.mass_u_dt_bc), ("ma_dt", self.mass_a_dt_bc),
                          ("mp_dt", (self.mass_p / self.dt).tocsr()), ("divt", self.div_t_bc),

@@ -80,11 +80,28 @@ class SpaceTimeJacobian:
         self.size = n_steps * disc.layout.slab_size
         self.block_multiplies = 0
         self._slabs = None
+        self._sell = None
+
+    def _sell_values(self):
+        """Sliced-ELL copy of the slab values (stmhd_jac_relayout), made at the first
+        apply; ``values`` is not modified after assembly (the reference builds fresh
+        matrices, spacetime.py:167-175)."""
+        if self._sell is None:
+            lib = _lib.load()
+            _bind_nt(self.disc, self.n_steps)
+            n = lib.stmhd_jac_sell_size(self.disc.handle, _lib.stream_ptr())
+            if n < 0:
+                _lib.check(1)
+            self._sell = torch.empty((self.n_steps, n), dtype=torch.float64, device=self.values.device)
+            _lib.check(lib.stmhd_jac_relayout(self.disc.handle, _lib.stream_ptr(), _lib.ptr(self.values),
+                                              _lib.ptr(self._sell)))
+        return self._sell
 
     def _into(self, v: torch.Tensor, out: torch.Tensor):
+        sell = self._sell_values()
         _bind_nt(self.disc, self.n_steps)
-        _lib.check(_lib.load().stmhd_jac_apply(self.disc.handle, _lib.stream_ptr(), _lib.ptr(self.values),
-                                               _lib.ptr(v), _lib.ptr(out)))
+        _lib.check(_lib.load().stmhd_jac_apply_sell(self.disc.handle, _lib.stream_ptr(), _lib.ptr(sell),
+                                                    _lib.ptr(v), _lib.ptr(out)))
         self.block_multiplies += 8 * self.n_steps + 2 * (self.n_steps - 1)
         return out
 
