@@ -7,6 +7,9 @@
 // exact per-orientation tensors (see fem.py in this package); rows and CSR
 // entries gather their element contributions in a fixed order, so the
 // assembly is deterministic (no atomics).
+#include <cstdlib>
+#include <cstring>
+
 #include "disc.hpp"
 
 namespace stmhd {
@@ -315,6 +318,443 @@ __global__ void __launch_bounds__(256) values_kernel(AsmArgs a, ValArgs v) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Element-matrix assembly per patch (P2/P1; tables: asm_patches.py).
+//
+// Per (patch, slab): phase A evaluates the element matrices of every element the
+// patch's entries touch into shared memory.  Every entry is affine in the element
+// state (u, A, j), so E = W s with per-orientation linear maps W built on the host
+// (discretisation constants folded in): one lane per element, W rows as warp-uniform
+// broadcast loads, a compact loop (no instruction-cache pressure).  Phase B writes
+// each owned CSR entry of the merged Jacobian pattern and of F_p as the sum of its
+// element contributions (16-bit shared-memory offsets).  Same algebra as
+// values_kernel, element-wise instead of entry-wise.
+struct PatchArgs {
+  int nt, npatch, nnv;
+  int o_j, o_a;
+  int64_t slab;
+  double idt, mu, ceta;
+  const double *sc;  // clamped state
+  const int *elem_v, *elem_1;
+  const int4 *desc;  // {round offset, rounds, slot offset, n0 | n1 << 16}
+  const int *slots, *out;
+  const uint4 *codes;  // 8 x uint16 per table entry
+  const double2 *w;    // element linear map W1 (asm_patches.element_linear_maps)
+  const double *g1, *mx;  // reference-element G1[o][n][d], MX[il][n]
+  double *js, *fp;
+  int64_t js_stride, fp_stride;
+};
+
+constexpr int kPatchESZ = 270, kPatchRound = 256, kPatchMaxC = 6;
+
+__global__ void __launch_bounds__(256, 2) values_patch_kernel(const __grid_constant__ PatchArgs P) {
+  extern __shared__ double E[];
+  const int pt = blockIdx.x;
+  const int4 dsc = P.desc[pt];
+  const int n0 = dsc.w & 0xffff, n1 = dsc.w >> 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int ntab = dsc.y * kPatchRound;
+  const int *outp = P.out + (int64_t)dsc.x * kPatchRound;
+  const uint4 *codep = P.codes + (int64_t)dsc.x * kPatchRound;
+  for (int k = blockIdx.y; k < P.nt; k += gridDim.y) {
+    const double *s = P.sc + (int64_t)k * P.slab;
+    // phase A: E = W s per element (lane = element; the warps of one orientation
+    // split the 270 outputs; W rows are warp-uniform broadcast loads)
+    {
+      const int o = warp & 1, nwo = nwarps >> 1, wo = warp >> 1;
+      const int no = o ? n1 : n0, sbase = o ? n0 : 0;
+      const double2 *W1 = P.w + o * (162 * 7);
+      for (int c0 = 0; c0 < no; c0 += 32) {
+        const int loc = c0 + lane;
+        const bool ok = loc < no;
+        const int sl = sbase + (ok ? loc : 0);
+        const int e = P.slots[dsc.z + sl];
+        double st[13], av[3], jv[3];
+#pragma unroll
+        for (int m = 0; m < 6; ++m) {
+          const int g = P.elem_v[e * 6 + m];
+          st[m] = s[g];
+          st[6 + m] = s[P.nnv + g];
+        }
+        st[12] = 1.0;
+#pragma unroll
+        for (int n = 0; n < 3; ++n) {
+          const int g = P.elem_1[e * 3 + n];
+          av[n] = s[P.o_a + g];
+          jv[n] = s[P.o_j + g];
+        }
+        double *Es = E + sl * kPatchESZ;
+        // FU, FA, FP: affine in u (W1 rows)
+        for (int v = wo; v < 162; v += nwo) {
+          const double2 *w = W1 + v * 7;
+          double acc = 0.0;
+#pragma unroll
+          for (int t = 0; t < 6; ++t) {
+            const double2 c = __ldg(w + t);
+            acc = fma(c.x, st[2 * t], acc);
+            acc = fma(c.y, st[2 * t + 1], acc);
+          }
+          acc = fma(__ldg(w + 6).x, st[12], acc);
+          if (ok) Es[v < 144 ? v : 252 + (v - 144)] = acc;
+        }
+        // Z_j, Z_A, Y: grad A and the j moments first, in the reference's order (keeps
+        // exact cancellations, e.g. d_x A = 0 on a Harris sheet), then one product each
+        double ga[2], jm[6];
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          ga[d] = 0.0;
+#pragma unroll
+          for (int n = 0; n < 3; ++n) ga[d] += av[n] * __ldg(&P.g1[(o * 3 + n) * 2 + d]);
+        }
+#pragma unroll
+        for (int il = 0; il < 6; ++il) {
+          jm[il] = 0.0;
+#pragma unroll
+          for (int n = 0; n < 3; ++n) jm[il] += jv[n] * __ldg(&P.mx[il * 3 + n]);
+        }
+        for (int v = wo; v < 108; v += nwo) {
+          const int q = v % 36;
+          double val;
+          if (v < 36) {  // ZJ[d][il][jl] = ga_d MX[il][jl]
+            val = (q < 18 ? ga[0] : ga[1]) * __ldg(&P.mx[q % 18]);
+          } else if (v < 72) {  // ZA[d][il][jl] = jm(il) G1[jl][d]
+            const int d = q / 18, il = (q / 3) % 6, jl = q % 3;
+            double j_il = jm[0];
+#pragma unroll
+            for (int i = 1; i < 6; ++i)
+              if (il == i) j_il = jm[i];
+            val = j_il * __ldg(&P.g1[(o * 3 + jl) * 2 + d]);
+          } else {  // Y[c][il][jl] = ga_c MX[jl][il]
+            const int c = q / 18, il = (q / 6) % 3, jl = q % 6;
+            val = ga[c] * __ldg(&P.mx[jl * 3 + il]);
+          }
+          if (ok) Es[144 + v] = val;
+        }
+      }
+    }
+    __syncthreads();
+    // phase B: owned entries; 8 codes per entry in one 16-byte word; 4 entries per
+    // thread in flight (table loads are L2 round trips)
+    for (int i0 = threadIdx.x; i0 < ntab; i0 += 4 * blockDim.x) {
+      int w[4];
+      uint4 cw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * blockDim.x;
+        w[u] = i < ntab ? __ldg(outp + i) : -1;
+        cw[u] = i < ntab ? __ldg(codep + i) : make_uint4(~0u, ~0u, ~0u, ~0u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (w[u] < 0) continue;
+        double v = 0.0;
+        if (w[u] & (1 << 29)) {
+          v = 1.0;
+        } else {
+          const unsigned c[8] = {cw[u].x & 0xffffu, cw[u].x >> 16, cw[u].y & 0xffffu, cw[u].y >> 16,
+                                 cw[u].z & 0xffffu, cw[u].z >> 16, cw[u].w & 0xffffu, cw[u].w >> 16};
+#pragma unroll
+          for (int j = 0; j < kPatchMaxC; ++j)
+            if (c[j] != 0xffffu) v += E[c[j]];
+        }
+        const int idx = w[u] & ((1 << 29) - 1);
+        if (w[u] & (1 << 30)) P.fp[(int64_t)k * P.fp_stride + idx] = v;
+        else P.js[(int64_t)k * P.js_stride + idx] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+static void values_patch(stmhd_disc_s *d, const AsmArgs &a, cudaStream_t s, double *js, double *fp) {
+  PatchArgs P{};
+  P.nt = a.nt;
+  P.npatch = (int)d->I("pa_npatch");
+  P.nnv = a.nnv;
+  P.o_j = a.n_u + a.n_p;
+  P.o_a = P.o_j + a.n_j;
+  P.slab = a.slab;
+  P.idt = 1.0 / a.dt;
+  P.mu = a.mu;
+  P.ceta = a.eta / a.mu0;
+  P.sc = a.sc;
+  P.elem_v = a.elem_v;
+  P.elem_1 = a.elem_1;
+  P.desc = d->D<int4>("pa_desc");
+  P.slots = d->D<int>("pa_slots");
+  P.out = d->D<int>("pa_out");
+  P.codes = d->D<uint4>("pa_codes");
+  P.w = d->D<double2>("pa_w");
+  {
+    constexpr TOff O = toff(6, 3);
+    P.g1 = d->D<double>("tensors") + O.G1;
+    P.mx = d->D<double>("tensors") + O.MX;
+  }
+  // outputs the caller did not ask for go to a scratch slab-sized sink? No: both are
+  // required together (the plan interleaves js and F_p entries)
+  P.js = js;
+  P.fp = fp;
+  P.js_stride = d->I("nnz_js");
+  P.fp_stride = d->I("nnz_fp");
+  const size_t smem = (size_t)d->I("pa_max_slots") * kPatchESZ * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    STMHD_CUDA_CHECK(cudaFuncSetAttribute(values_patch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          113 * 1024));
+    attr = true;
+  }
+  require(smem <= 113 * 1024, "patch assembly: element matrices exceed shared memory");
+  values_patch_kernel<<<dim3(P.npatch, a.nt), 256, smem, s>>>(P);
+  STMHD_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// Residual per patch (P2/P1; tables: asm_patches.build_residual_plan).  Phase A: the
+// element residual vector RU[d][il] | RP | RJ | RA of every element the patch's rows
+// touch (reference _slab_galerkin, spacetime.py:42-62, term by term as
+// residual_kernel); phase B: each owned row is the sum of its node's element entries
+// plus the row constant (-flux, e_load, -bc value; Dirichlet rows add the raw state).
+struct ResConst {
+  double TV[2][6][6][6][2];
+  double MV[6][6], KV[2][6][6];
+  double MX[6][3], G1[2][3][2], M1[3][3], K1[2][3][3];
+  double BD[2][3][6][2];  // -int q_m d_c phi_n
+};
+
+struct ResArgs {
+  ResConst c;
+  int nt, nnv, o_p, o_j, o_a;
+  int64_t slab;
+  double idt, mu, ceta, imu0;
+  const double *sc, *state, *ic_u, *ic_a, *add;
+  const int *elem_v, *elem_p, *elem_1;
+  const int4 *desc;
+  const int *slots, *out;
+  const uint4 *codes;
+  double *res;
+};
+
+constexpr int kResSZ = 21;
+
+// RU[d][il] for il in [R0, R0+3): mass/dt + mu K + pressure + (u.grad)u + Lorentz
+template <int O, int R0>
+__device__ __forceinline__ void res_part_u(const ResArgs &P, const double *s, const double *pu, const double *pa,
+                                           int e, double *E) {
+  const ResConst &C = P.c;
+  double u[2][6], up[2][6];
+#pragma unroll
+  for (int m = 0; m < 6; ++m) {
+    const int g = P.elem_v[e * 6 + m];
+    u[0][m] = s[g];
+    u[1][m] = s[P.nnv + g];
+    up[0][m] = pu[g];
+    up[1][m] = pu[P.nnv + g];
+  }
+  double pv[3], av[3], jv[3];
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    pv[n] = s[P.o_p + P.elem_p[e * 3 + n]];
+    const int g = P.elem_1[e * 3 + n];
+    av[n] = s[P.o_a + g];
+    jv[n] = s[P.o_j + g];
+  }
+  (void)pa;
+  double ga[2];
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    ga[d] = 0.0;
+#pragma unroll
+    for (int n = 0; n < 3; ++n) ga[d] += av[n] * C.G1[O][n][d];
+  }
+#pragma unroll
+  for (int il = R0; il < R0 + 3; ++il) {
+    double w[6];
+#pragma unroll
+    for (int n = 0; n < 6; ++n) {
+      double t = 0.0;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int m = 0; m < 6; ++m) t = fma(u[c][m], C.TV[O][il][m][n][c], t);
+      w[n] = t;
+    }
+    double jm = 0.0;
+#pragma unroll
+    for (int n = 0; n < 3; ++n) jm += jv[n] * C.MX[il][n];
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      double mass = 0.0, visc = 0.0, pres = 0.0, adv = 0.0;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        mass += C.MV[il][j] * (u[d][j] - up[d][j]);
+        visc += C.KV[O][il][j] * u[d][j];
+        adv += w[j] * u[d][j];
+      }
+#pragma unroll
+      for (int n = 0; n < 3; ++n) pres += C.BD[O][n][il][d] * pv[n];
+      E[d * 6 + il] = mass * P.idt + P.mu * visc + pres + adv + ga[d] * jm;
+    }
+  }
+}
+
+// RP (divergence), RJ (current definition), RA (induction)
+template <int O>
+__device__ __forceinline__ void res_part_s(const ResArgs &P, const double *s, const double *pa, int e, double *E) {
+  const ResConst &C = P.c;
+  double u[2][6];
+#pragma unroll
+  for (int m = 0; m < 6; ++m) {
+    const int g = P.elem_v[e * 6 + m];
+    u[0][m] = s[g];
+    u[1][m] = s[P.nnv + g];
+  }
+  double av[3], apv[3], jv[3];
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    const int g = P.elem_1[e * 3 + n];
+    av[n] = s[P.o_a + g];
+    apv[n] = pa[g];
+    jv[n] = s[P.o_j + g];
+  }
+  double gx = 0.0, gy = 0.0;
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    gx += av[n] * C.G1[O][n][0];
+    gy += av[n] * C.G1[O][n][1];
+  }
+#pragma unroll
+  for (int ml = 0; ml < 3; ++ml) {
+    double rp = 0.0;
+#pragma unroll
+    for (int n = 0; n < 6; ++n)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) rp += C.BD[O][ml][n][c] * u[c][n];
+    double mj = 0.0, kj = 0.0, mass = 0.0, diff = 0.0;
+#pragma unroll
+    for (int n = 0; n < 3; ++n) {
+      mj += C.M1[ml][n] * jv[n];
+      kj += C.K1[O][ml][n] * av[n];
+      mass += C.M1[ml][n] * (av[n] - apv[n]);
+      diff += C.K1[O][ml][n] * av[n];
+    }
+    double mx = 0.0, my = 0.0;
+#pragma unroll
+    for (int n = 0; n < 6; ++n) {
+      mx += C.MX[n][ml] * u[0][n];
+      my += C.MX[n][ml] * u[1][n];
+    }
+    E[12 + ml] = rp;
+    E[15 + ml] = mj + kj * P.imu0;
+    E[18 + ml] = mass * P.idt + P.ceta * diff + (gx * mx + gy * my);
+  }
+}
+
+template <int O>
+__device__ __noinline__ void res_part(const ResArgs &P, int part, const double *s, const double *pu,
+                                      const double *pa, int e, double *E) {
+  if (part == 0) res_part_u<O, 0>(P, s, pu, pa, e, E);
+  else if (part == 1) res_part_u<O, 3>(P, s, pu, pa, e, E);
+  else res_part_s<O>(P, s, pa, e, E);
+}
+
+__global__ void __launch_bounds__(256) residual_patch_kernel(const __grid_constant__ ResArgs P) {
+  extern __shared__ double E[];
+  const int pt = blockIdx.x, k = blockIdx.y;
+  const int4 dsc = P.desc[pt];
+  const int n0 = dsc.w & 0xffff, n1 = dsc.w >> 16;
+  const int ch0 = (n0 + 31) / 32, nch = ch0 + (n1 + 31) / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const double *s = P.sc + (int64_t)k * P.slab;
+  const double *pu = k ? P.sc + (int64_t)(k - 1) * P.slab : P.ic_u;
+  const double *pa = k ? P.sc + (int64_t)(k - 1) * P.slab + P.o_a : P.ic_a;
+  for (int t = warp; t < 3 * nch; t += nwarps) {
+    const int part = t % 3, ch = t / 3;
+    const int o = ch < ch0 ? 0 : 1;
+    const int loc = o == 0 ? ch * 32 + lane : (ch - ch0) * 32 + lane;
+    if (loc >= (o == 0 ? n0 : n1)) continue;
+    const int sl = o == 0 ? loc : n0 + loc;
+    const int e = P.slots[dsc.z + sl];
+    if (o == 0) res_part<0>(P, part, s, pu, pa, e, E + sl * kResSZ);
+    else res_part<1>(P, part, s, pu, pa, e, E + sl * kResSZ);
+  }
+  __syncthreads();
+  const int ntab = dsc.y * kPatchRound;
+  const int *outp = P.out + (int64_t)dsc.x * kPatchRound;
+  const uint4 *codep = P.codes + (int64_t)dsc.x * kPatchRound;
+  const double *raw = P.state + (int64_t)k * P.slab;
+  for (int i0 = threadIdx.x; i0 < ntab; i0 += 4 * blockDim.x) {
+    int w[4];
+    uint4 cw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      w[u] = i < ntab ? __ldg(outp + i) : -1;
+      cw[u] = i < ntab ? __ldg(codep + i) : make_uint4(~0u, ~0u, ~0u, ~0u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (w[u] < 0) continue;
+      const int r = w[u] & ((1 << 29) - 1);
+      double v = P.add[r];
+      if (w[u] & (1 << 29)) {
+        v = raw[r] + v;
+      } else {
+        const unsigned c[8] = {cw[u].x & 0xffffu, cw[u].x >> 16, cw[u].y & 0xffffu, cw[u].y >> 16,
+                               cw[u].z & 0xffffu, cw[u].z >> 16, cw[u].w & 0xffffu, cw[u].w >> 16};
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < kPatchMaxC; ++j)
+          if (c[j] != 0xffffu) acc += E[c[j]];
+        v = acc + v;
+      }
+      P.res[(int64_t)k * P.slab + r] = v;
+    }
+  }
+}
+
+static void residual_patch(stmhd_disc_s *d, const AsmArgs &a, cudaStream_t s) {
+  ResArgs P{};
+  const HostArray &T = d->H("tensors");
+  constexpr TOff O = toff(6, 3);
+  require(T.count >= O.total, "patch residual: tensor blob too small");
+  const double *t = T.as<double>();
+  std::memcpy(P.c.MV, t + O.MV, sizeof(P.c.MV));
+  std::memcpy(P.c.KV, t + O.KV, sizeof(P.c.KV));
+  std::memcpy(P.c.TV, t + O.TV, sizeof(P.c.TV));
+  std::memcpy(P.c.MX, t + O.MX, sizeof(P.c.MX));
+  std::memcpy(P.c.G1, t + O.G1, sizeof(P.c.G1));
+  std::memcpy(P.c.M1, t + O.M1, sizeof(P.c.M1));
+  std::memcpy(P.c.K1, t + O.K1, sizeof(P.c.K1));
+  std::memcpy(P.c.BD, t + O.BD, sizeof(P.c.BD));
+  P.nt = a.nt;
+  P.nnv = a.nnv;
+  P.o_p = a.n_u;
+  P.o_j = a.n_u + a.n_p;
+  P.o_a = P.o_j + a.n_j;
+  P.slab = a.slab;
+  P.idt = 1.0 / a.dt;
+  P.mu = a.mu;
+  P.ceta = a.eta / a.mu0;
+  P.imu0 = 1.0 / a.mu0;
+  P.sc = a.sc;
+  P.state = a.state;
+  P.ic_u = a.ic_u;
+  P.ic_a = a.ic_a;
+  P.add = d->D<double>("pr_add");
+  P.elem_v = a.elem_v;
+  P.elem_p = a.elem_p;
+  P.elem_1 = a.elem_1;
+  P.desc = d->D<int4>("pr_desc");
+  P.slots = d->D<int>("pr_slots");
+  P.out = d->D<int>("pr_out");
+  P.codes = d->D<uint4>("pr_codes");
+  P.res = a.res;
+  const size_t smem = (size_t)d->I("pr_max_slots") * kResSZ * sizeof(double);
+  require(smem <= 48 * 1024, "patch residual: element vectors exceed shared memory");
+  residual_patch_kernel<<<dim3((unsigned)d->I("pr_npatch"), a.nt), 256, smem, s>>>(P);
+  STMHD_LAUNCH_CHECK();
+}
+
 static AsmArgs make_args(const stmhd_disc_s *d) {
   AsmArgs a{};
   a.nt = (int)d->I("nt");
@@ -372,14 +812,26 @@ static void assemble_t(stmhd_disc_s *d, cudaStream_t s, const double *state, con
     STMHD_CUDA_CHECK(cudaFuncSetAttribute(values_kernel<NV, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
     attr = true;
   }
+  static const bool patch_env = [] {
+    const char *e = getenv("STMHD_PATCH_ASM");
+    return !e || atoi(e) != 0;
+  }();
   if (res) {
-    residual_kernel<NV, NP><<<dim3(cdiv(a.slab, 256), a.nt), 256, smem, s>>>(a);
-    STMHD_LAUNCH_CHECK();
+    if (NV == 6 && NP == 3 && patch_env && d->dev.count("pr_desc")) {
+      residual_patch(d, a, s);
+    } else {
+      residual_kernel<NV, NP><<<dim3(cdiv(a.slab, 256), a.nt), 256, smem, s>>>(a);
+      STMHD_LAUNCH_CHECK();
+    }
     pin_row_kernel<<<a.nt, 256, 0, s>>>(state, d->D<double>("p_mean_row"), a.n_p, a.slab, a.n_u, a.p_pin,
                                          d->R("p_mean_target"), res);
     STMHD_LAUNCH_CHECK();
   }
   const int ychunks = std::max(1, std::min(a.nt, 8));
+  if (NV == 6 && NP == 3 && js && fp && patch_env && d->dev.count("pa_desc")) {
+    values_patch(d, a, s, js, fp);
+    js = fp = nullptr;
+  }
   if (js) {
     ValArgs v{};
     v.nnz = (int)d->I("nnz_js");

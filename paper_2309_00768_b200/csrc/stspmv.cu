@@ -9,6 +9,7 @@
 // front to back while that slab's x stays L1/L2 resident.  Four independent
 // accumulators keep four value loads and four x gathers in flight per thread.
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
 #include <numeric>
 
@@ -18,7 +19,7 @@
 namespace stmhd {
 
 struct SellArgs {
-  int nslices;
+  int nslices, nt;
   const int4 *slice;
   const int2 *lane;  // {row, lenA | lenB << 16}
   const int *col_a, *col_b;
@@ -32,38 +33,74 @@ struct SellArgs {
   int64_t ys;
 };
 
+// S slabs per thread share every column (and coupling) load: per batch of 4 entries
+// a thread has 4 column loads and 4*S value loads + 4*S x gathers in flight.
+template <int S, int B>
 __global__ void __launch_bounds__(256) sell_spmv_kernel(SellArgs a) {
   const int sidx = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (sidx >= a.nslices) return;
-  const int k = blockIdx.y;
+  const int k0 = blockIdx.y * S;
+  const int ns = min(S, a.nt - k0);
   const int4 sl = a.slice[sidx];
   const int2 li = a.lane[sidx * 32 + lane];
   const int lenA = li.y & 0xffff, lenB = li.y >> 16;
-  const double *va = a.sell + (int64_t)k * a.sell_a + (int64_t)sl.z * 32 + lane;
+  const double *va = a.sell + (int64_t)k0 * a.sell_a + (int64_t)sl.z * 32 + lane;
   const int *ca = a.col_a + (int64_t)sl.z * 32 + lane;
-  const double *xk = a.x + (int64_t)k * a.xs;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int j = 0;
-  for (; j + 4 <= sl.x; j += 4) {
-    const int c0 = ca[(j + 0) * 32], c1 = ca[(j + 1) * 32], c2 = ca[(j + 2) * 32], c3 = ca[(j + 3) * 32];
-    const double v0 = va[(j + 0) * 32], v1 = va[(j + 1) * 32], v2 = va[(j + 2) * 32], v3 = va[(j + 3) * 32];
-    if (j + 0 < lenA) s0 = fma(v0, xk[c0], s0);
-    if (j + 1 < lenA) s1 = fma(v1, xk[c1], s1);
-    if (j + 2 < lenA) s2 = fma(v2, xk[c2], s2);
-    if (j + 3 < lenA) s3 = fma(v3, xk[c3], s3);
+  double sa[S][2];
+#pragma unroll
+  for (int q = 0; q < S; ++q) sa[q][0] = sa[q][1] = 0.0;
+  // slabs past the end re-read the last slab (valid addresses, results dropped), so
+  // every load of a batch is issued back to back without branches
+  const double *vq[S];
+  const double *xq[S];
+#pragma unroll
+  for (int q = 0; q < S; ++q) {
+    const int kq = min(q, ns - 1);
+    vq[q] = va + (int64_t)kq * a.sell_a;
+    xq[q] = a.x + (int64_t)(k0 + kq) * a.xs;
   }
-  for (; j < sl.x; ++j)
-    if (j < lenA) s0 = fma(va[j * 32], xk[ca[j * 32]], s0);
-  double sb = 0.0;
+  for (int j = 0; j < sl.x; j += B) {
+    int c[B];
+    bool on[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      on[i] = j + i < lenA;
+      c[i] = on[i] ? ca[(j + i) * 32] : 0;
+    }
+    double v[S][B], xv[S][B];
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        v[q][i] = on[i] ? vq[q][(j + i) * 32] : 0.0;
+        xv[q][i] = on[i] ? xq[q][c[i]] : 0.0;
+      }
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+#pragma unroll
+      for (int i = 0; i < B; ++i) sa[q][i & 1] = fma(v[q][i], xv[q][i], sa[q][i & 1]);
+  }
+  double sb[S];
+#pragma unroll
+  for (int q = 0; q < S; ++q) sb[q] = 0.0;
   if (sl.y) {
     const int *cb = a.col_b + (int64_t)sl.w * 32 + lane;
     const double *vb = a.val_b + (int64_t)sl.w * 32 + lane;
-    for (int q = 0; q < lenB; ++q) {
-      const int64_t xi = (int64_t)k * a.xs + cb[q * 32];
-      if (xi >= 0) sb = fma(vb[q * 32], a.x[xi], sb);
+    for (int j = 0; j < lenB; ++j) {
+      const int c = cb[j * 32];
+      const double bv = vb[j * 32];
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const int64_t xi = (int64_t)(k0 + min(q, ns - 1)) * a.xs + c;
+        if (xi >= 0) sb[q] = fma(bv, a.x[xi], sb[q]);
+      }
     }
   }
-  if (li.x >= 0) a.y[(int64_t)k * a.ys + li.x] = a.alpha_a * ((s0 + s1) + (s2 + s3)) + a.alpha_b * sb;
+  if (li.x >= 0) {
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+      if (q < ns) a.y[(int64_t)(k0 + q) * a.ys + li.x] = a.alpha_a * (sa[q][0] + sa[q][1]) + a.alpha_b * sb[q];
+  }
 }
 
 __global__ void sell_relayout_kernel(const int *src, int64_t n, int nt, const double *csr, int64_t stride,
@@ -164,7 +201,21 @@ void StSpmvPlan::apply(int nt, const double *sell, double alpha_a, double alpha_
   a.xs = xs;
   a.y = y;
   a.ys = ys;
-  sell_spmv_kernel<<<dim3(cdiv(nslices, 8), nt), 256, 0, s>>>(a);
+  a.nt = nt;
+  // slabs per thread x entries per batch (STMHD_SELL_SB = 10*S + B for experiments)
+  static const int sb = [] {
+    const char *e = getenv("STMHD_SELL_SB");
+    return e ? atoi(e) : 0;
+  }();
+  const int S = sb ? sb / 10 : 2, B = sb ? sb % 10 : 4;  // measured best for J.v and C5 (r01)
+  const dim3 blk(256);
+  auto grid = [&](int s_) { return dim3(cdiv(nslices, 8), cdiv(nt, s_)); };
+  if (S == 1 && B == 8) sell_spmv_kernel<1, 8><<<grid(1), blk, 0, s>>>(a);
+  else if (S == 1) sell_spmv_kernel<1, 4><<<grid(1), blk, 0, s>>>(a);
+  else if (S == 2 && B == 8) sell_spmv_kernel<2, 8><<<grid(2), blk, 0, s>>>(a);
+  else if (S == 2) sell_spmv_kernel<2, 4><<<grid(2), blk, 0, s>>>(a);
+  else if (S == 4 && B == 2) sell_spmv_kernel<4, 2><<<grid(4), blk, 0, s>>>(a);
+  else sell_spmv_kernel<4, 4><<<grid(4), blk, 0, s>>>(a);
   STMHD_LAUNCH_CHECK();
 }
 

@@ -182,6 +182,21 @@ class Discretization:
         rp, ci, va = csr_arrays(big)
         up("jc_rowptr", rp), up("jc_col", ci.astype(np.int64) - L.slab_size), up("jc_val", va)
         self.jc_nnz = len(ci)
+        # element-matrix patch plan of the Jacobian assembly (P2/P1)
+        from .asm_patches import build_patch_plan, build_residual_plan
+
+        pp = build_patch_plan(self)
+        if pp is not None:
+            up("pa_desc", pp["desc"]), up("pa_slots", pp["slots"]), up("pa_out", pp["out"])
+            up("pa_codes", pp["codes"]), up("pa_w", pp["w"])
+            for k, v in (("pa_npatch", pp["npatch"]), ("pa_max_slots", pp["max_slots"])):
+                _lib.check(lib.stmhd_disc_set_int(h, k.encode(), int(v)))
+        rp_ = build_residual_plan(self)
+        if rp_ is not None:
+            up("pr_desc", rp_["desc"]), up("pr_slots", rp_["slots"]), up("pr_out", rp_["out"])
+            up("pr_codes", rp_["codes"]), up("pr_add", rp_["add"])
+            for k, v in (("pr_npatch", rp_["npatch"]), ("pr_max_slots", rp_["max_slots"])):
+                _lib.check(lib.stmhd_disc_set_int(h, k.encode(), int(v)))
         # preconditioner CSRs (field-local coordinates)
         for key, mat in (("mu_dt", self.mass_u_dt_bc), ("ma_dt", self.mass_a_dt_bc),
                          ("mp_dt", (self.mass_p / self.dt).tocsr()), ("divt", self.div_t_bc),
