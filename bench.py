@@ -322,7 +322,22 @@ def run_ours(args, rank, world):
 
     per_iter = {"J_apply_ms": tmeas(lambda: jac._into(v, out), 50),
                 "P_apply_ms": tmeas(lambda: pc._into(v, out), 5),
-                "assembly_ms": tmeas(lambda: p.assemble_jacobian(st0, disc), 5)}
+                "assembly_ms": tmeas(lambda: p.assemble_jacobian(st0, disc), 5),
+                "residual_ms": tmeas(lambda: p.residual(st0, disc), 5)}
+    # the other north-star kernels against the same peak (SURVEY 8(d) algorithmic bytes)
+    P_ = disc.pattern
+    jv_bytes = nt * (8 * P_.nnz + 16 * L.slab_size) + 12 * disc.jc_nnz + 8 * L.n_p + 4 * P_.nnz
+    asm_bytes = nt * 8 * (2 * L.slab_size + P_.nnz + P_.fp_nnz)
+    asm_ms = per_iter["assembly_ms"] + per_iter["residual_ms"]
+    kernel_rooflines = {
+        "J_apply (sell_spmv_kernel)": {"algorithmic_bytes": jv_bytes, "ms": per_iter["J_apply_ms"],
+                                       "GBps": jv_bytes / per_iter["J_apply_ms"] / 1e6,
+                                       "frac": jv_bytes / per_iter["J_apply_ms"] / 1e6 / peak},
+        "assembly (residual_patch + values_patch)": {"algorithmic_bytes": asm_bytes, "ms": asm_ms,
+                                                     "GBps": asm_bytes / asm_ms / 1e6,
+                                                     "frac": asm_bytes / asm_ms / 1e6 / peak},
+        "note": "C2 operators are partly L2-resident (168 MB); tools/bench_spmv.py and tools/asm_probe.py "
+                "give the C3/C5 figures"}
 
     line = {
         "metric": "FGMRES iterations/s (C2 Newton solve, P_T preconditioner, FP64)",
@@ -337,6 +352,7 @@ def run_ours(args, rank, world):
         "relative_residual": stats_last.residual_norms[-1] / stats_last.residual_norms[0],
         "phase_s_per_solve": {k: v / args.steps for k, v in breakdown.items()},
         "per_call_ms": per_iter,
+        "kernel_rooflines": kernel_rooflines,
         "e2e": {"value": e2e_value, "unit": "FGMRES it/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "roofline": {"kernel": "nd_sweep_kernel (F_u time sweep, solve_velocity)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

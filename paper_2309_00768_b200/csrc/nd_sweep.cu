@@ -290,7 +290,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     const int nT = (int)tpos.size();
     std::vector<std::array<int, 4>> zc(nT, {-1, -1, -1, -1});
     // K (nT^2 per slab) may not outgrow the factor itself (batched per-slab factors)
-    bool ok = nT > 0 && nT <= 4096 && (int64_t)nT * nT <= p.factor_size;
+    bool ok = nT > 0 && nT <= 4096 && (int64_t)nT * nT * (ncta > 16 ? 8 : 1) <= p.factor_size;
     for (int r : roots) {  // subtree roots' updates land on top unknowns
       for (int a = 0; a < p.nb[r] && ok; ++a) {
         const int tgt = bpos[p.idx_off[r] + p.ns[r] + a];
@@ -624,12 +624,30 @@ struct SweepArgs {
   int vstride;  // doubles per warp: gather buffer + 2 TMA slots
   int slot;     // doubles per TMA slot (largest chunk block)
   int null_work;  // diagnostics: skip all task work (barrier/loop floor)
+  unsigned *gbar;  // grid mode (one CTA per SM, cooperative launch): software grid barrier word
   unsigned long long *trace;
   unsigned long long *prof;  // PROF instantiation: 6 counters per warp
   unsigned long long *tline; // PROF instantiation: per-warp event timeline of slab 1, CTA 0 (128 per warp)
 };
 
-__device__ __forceinline__ void sweep_barrier() {
+__device__ __forceinline__ void sweep_barrier(const SweepArgs &a) {
+  if (a.gbar) {
+    // grid barrier over the launch's CTAs (cooperative-groups arrival scheme: every
+    // CTA adds 1, CTA 0 adds 2^31 - (n - 1), so the top bit flips once all arrived)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+      __threadfence();
+      const unsigned old = atomicAdd(a.gbar, nb);
+      unsigned cur;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(a.gbar) : "memory");
+      } while (((old ^ cur) & 0x80000000u) == 0);
+      __threadfence();
+    }
+    __syncthreads();
+    return;
+  }
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
@@ -657,7 +675,7 @@ __device__ __forceinline__ void st_release_gpu(int *p, int v) {
 }
 
 __device__ __forceinline__ void sweep_trace(const SweepArgs &a, int &step) {
-  if (a.trace && threadIdx.x == 0 && cluster_rank() == 0) {
+  if (a.trace && threadIdx.x == 0 && (a.gbar ? blockIdx.x == 0 : cluster_rank() == 0)) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[step] = t;
@@ -1116,8 +1134,9 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   __shared__ __align__(8) unsigned long long mbar[16][2];
   __shared__ SweepArgs sa;
   __shared__ const double *s_src[8];  // coupling sources of the current slab (by source id)
-  const unsigned cid = cluster_index();
-  const int crank = (int)cluster_rank();
+  const bool grid = m.st[0].gbar != nullptr;  // grid mode: one stage, CTA rank = blockIdx.x
+  const unsigned cid = grid ? 0u : cluster_index();
+  const int crank = grid ? (int)blockIdx.x : (int)cluster_rank();
   if (threadIdx.x == 0) {
     if (cid == 0) sa = m.st[0];
     else if (cid == 1) sa = m.st[1];
@@ -1239,7 +1258,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
     }
     if (a.nsub || a.prog_hdr) {  // subtree roots' updates and coupled top rows visible
-      tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+      tb = pclock<PROF>(); sweep_barrier(a); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step);
     }
     if (a.dense) {
@@ -1265,7 +1284,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       for (int ti = w.bnd[L]; ti < t1; ++ti) dense_task<PROF>(a, w.tl[ti], sv.zs, x, k, w, mbar);
       if (PROF) tl_mark(w, 4);
       ++L;
-      tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;  // x_T visible
+      tb = pclock<PROF>(); sweep_barrier(a); if (PROF) w.acc[3] += pclock<PROF>() - tb;  // x_T visible
       if (a.tab_ints) {  // stage x_T in shared memory for the subtree backward tables
         for (int i = threadIdx.x; i < a.ntT; i += blockDim.x) sv.zs[i] = x[a.ztab[2 * i].x];
         __syncthreads();
@@ -1275,7 +1294,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       for (int t = 0; t < a.ntop; ++t, ++L) {
         const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
         for (int ti = w.bnd[L]; ti < t1; ++ti) forward_task<false, PROF>(a, w.tl[ti], F, rhs, sv, w, mbar);
-        tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+        tb = pclock<PROF>(); sweep_barrier(a); if (PROF) w.acc[3] += pclock<PROF>() - tb;
         sweep_trace(a, step);
       }
       for (int t = a.ntop - 1; t >= 0; --t, ++L) {
@@ -1283,7 +1302,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
         for (int ti = w.bnd[L]; ti < t1; ++ti) backward_task<false, PROF>(a, w.tl[ti], F, x, sv, w, mbar);
         if (t > 0 || a.nsub || k + 1 < a.nslab) {
           tb = pclock<PROF>();
-          sweep_barrier();
+          sweep_barrier(a);
           if (PROF) w.acc[3] += pclock<PROF>() - tb;
         }
         sweep_trace(a, step);
@@ -1299,7 +1318,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     if (a.post_hdr && !a.null_work) {
       // post-slab program: rows of another stage's right-hand side from this stage's
       // x_k (all CTAs' parts: cluster barrier) and external sources at slab k
-      sweep_barrier();
+      sweep_barrier(a);
       if (threadIdx.x == 0) {
         s_src[3] = a.ext_xp[0] ? a.ext_xp[0] + (int64_t)k * a.ext_n[0] : a.zero;
         s_src[4] = a.ext_xp[1] ? a.ext_xp[1] + (int64_t)k * a.ext_n[1] : a.zero;
@@ -1316,7 +1335,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       if (threadIdx.x == 0) st_release_gpu(a.flag_out + (int64_t)k * a.ncta + crank, a.epoch);
     }
     if (a.nsub && k + 1 < a.nslab) {  // x_k visible to every CTA's next coupling
-      tb = pclock<PROF>(); sweep_barrier(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+      tb = pclock<PROF>(); sweep_barrier(a); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step);
     }
   }
@@ -1661,6 +1680,8 @@ struct SweepStage {
   // always regather)
   int64_t vals_tag = 0, post_tag = 0;
   int warps = 0;  // warps per CTA (0: not chosen yet)
+  int ncta = 0;   // CTAs of the sweep: kCluster (one cluster) or one per SM (grid mode)
+  DevBuf gbar;    // grid-mode barrier word
   const std::vector<int> *ext_pos[2] = {nullptr, nullptr};
   const CplProgram *vals_prog = nullptr, *post_prog = nullptr;
 };
@@ -1694,10 +1715,13 @@ static int gather_values(const CplProgram &pg, const SweepCoupling *cpl, int ncp
 
 void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
                          int64_t ld_x, int nrhs, const SweepCoupling *cpl, int ncpl, SweepStage *const *ext,
-                         int next, cudaStream_t s, int64_t vals_tag) {
+                         int next, cudaStream_t s, int64_t vals_tag, int ncta) {
   const NDDevice &dev = *fac.dev;
   const NDPlan &p = *dev.plan;
-  const int cluster = kCluster;
+  if (ncta <= 0) ncta = kCluster;
+  if (st.ncta != ncta) st.warps = 0;  // re-choose the warps for a new CTA count
+  st.ncta = ncta;
+  const int cluster = ncta;
   const int slot = sweep_slot(p);
   // warps per CTA: 16, halved while the plan's shared memory does not fit (large
   // slabs such as configuration 5); the choice sticks to the stage
@@ -1706,9 +1730,19 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
     return ((size_t)w * c.vstride + 3 * c.sub_len + c.sub_cb + c.kpad + 4) * sizeof(double) + (size_t)c.tab_ints * 4 +
            (size_t)w * tstr;
   };
-  int warps = st.warps ? st.warps : kWarps;
-  while (!st.warps && warps > 4 && smem_of(dev.get_sweep_plan(cluster, warps, kSmemMax / 8, s), warps) > (size_t)kSmemMax)
-    warps /= 2;
+  // prefer the most warps whose plan keeps the CTA-local subtree phase (fewer
+  // cluster/grid barriers per slab), else the most warps whose flat plan fits
+  int warps = st.warps;
+  if (!warps) {
+    int flat = 0;
+    for (int w = kWarps; w >= 4 && !warps; w /= 2) {
+      const NDSweepPlan &c = dev.get_sweep_plan(cluster, w, kSmemMax / 8, s);
+      if (smem_of(c, w) > (size_t)kSmemMax) continue;
+      if (c.nsub > 0 || ncta == kCluster) warps = w;  // cluster mode: first fit (stages of a
+      else if (!flat) flat = w;                        // pipelined launch agree on 16)
+    }
+    if (!warps) warps = flat ? flat : 4;
+  }
   st.warps = warps;
   const NDSweepPlan &sp = dev.get_sweep_plan(cluster, warps, kSmemMax / 8, s);
   const int vstride = sp.vstride;
@@ -1808,6 +1842,14 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   a.vstride = vstride;
   a.null_work = env_int2("STMHD_SWEEP_NULL", 0);
   a.post_hdr = nullptr;  // set by sweep_stage_set_post for this launch
+  a.gbar = nullptr;
+  if (ncta != kCluster) {  // grid mode
+    if (!st.gbar.ptr) {
+      st.gbar.alloc(sizeof(unsigned));
+      STMHD_CUDA_CHECK(cudaMemsetAsync(st.gbar.ptr, 0, sizeof(unsigned), s));
+    }
+    a.gbar = st.gbar.as<unsigned>();
+  }
   st.smem = ((size_t)warps * a.vstride + 3 * a.sub_len + a.sub_cb + a.kpad + 4) * sizeof(double) +
             (size_t)a.tab_ints * 4 + (size_t)warps * a.tstride;
   require(st.smem <= (size_t)kSmemMax, "nd sweep: subtree vectors or fronts too large for shared memory");
@@ -1962,6 +2004,8 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
     require(st.warps == stg[0]->warps, "sweep: stages of one launch need the same warps per CTA");
   }
   const int warps = stg[0]->warps;
+  const bool grid = stg[0]->a.gbar != nullptr;
+  require(!grid || nst == 1, "sweep: grid mode runs one stage per launch");
   for (int i = 0; i < nst; ++i) {
     SweepStage &st = *stg[i];
     for (int e = 0; e < st.a.nwait; ++e) {
@@ -2002,14 +2046,14 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
   DevBuf pr;
   DevBuf tlb;
   if (prof_on) {
-    pr.alloc((size_t)kCluster * warps * 8 * sizeof(unsigned long long));
+    pr.alloc((size_t)stg[0]->ncta * warps * 8 * sizeof(unsigned long long));
     m.st[ts].prof = pr.as<unsigned long long>();
     tlb.alloc((size_t)warps * 128 * sizeof(unsigned long long));
     STMHD_CUDA_CHECK(cudaMemsetAsync(tlb.ptr, 0, tlb.bytes, s));
     m.st[ts].tline = tlb.as<unsigned long long>();
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kCluster * nst);
+  cfg.gridDim = dim3(grid ? stg[0]->ncta : kCluster * nst);
   cfg.blockDim = dim3(warps * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -2019,12 +2063,16 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   int nat = 1;
+  if (grid) {  // no cluster; all CTAs co-resident (cooperative) for the grid barrier
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+  }
   // the stages wait on each other: all clusters must be co-resident (cooperative
   // launch; STMHD_PIPE_COOP=0 drops the attribute for profilers that cannot replay
   // cooperative cluster launches -- 48 CTAs on 148 SMs are co-resident in practice and
   // a consumer traps after 4 s instead of hanging)
   static const int coop_env = env_int2("STMHD_PIPE_COOP", 1);
-  if (nst > 1 && coop_env) {
+  if (nst > 1 && coop_env && !grid) {
     at[1].id = cudaLaunchAttributeCooperative;
     at[1].val.cooperative = 1;
     nat = 2;
@@ -2062,7 +2110,7 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
             (long long)a.sub_cb);
   }
   if (prof_on) {
-    const int nwp = kCluster * warps;
+    const int nwp = stg[0]->ncta * warps;
     std::vector<unsigned long long> h((size_t)nwp * 8);
     STMHD_CUDA_CHECK(cudaMemcpyAsync(h.data(), pr.ptr, h.size() * 8, cudaMemcpyDeviceToHost, s));
     STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -2105,7 +2153,14 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   static std::map<const NDDevice *, SweepStagePtr> stages;
   SweepStagePtr &sp = stages[fac.dev];
   if (!sp) sp = sweep_stage_new();
-  sweep_stage_prepare(*sp, fac, rhs, ld_rhs, x, ld_x, nrhs, cpl, ncpl, nullptr, 0, s, 0);
+  // grid mode (one CTA per SM, software grid barrier) when a slab's factor is large
+  // enough that 16 SMs cannot stream it (configuration 5: 75 MB per slab); the
+  // cluster mode keeps the cheaper hardware barrier for the MHD blocks
+  static const int grid_env = env_int2("STMHD_SWEEP_GRID", -1);
+  const double fbytes = 8.0 * (double)fac.dev->plan->factor_size;
+  const bool grid = grid_env == 1 || (grid_env < 0 && fbytes > 32e6);
+  sweep_stage_prepare(*sp, fac, rhs, ld_rhs, x, ld_x, nrhs, cpl, ncpl, nullptr, 0, s, 0,
+                      grid ? num_sms() : kCluster);
   SweepStage *one = sp.get();
   sweep_stages_launch(&one, 1, s);
 }

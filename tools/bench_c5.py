@@ -49,6 +49,10 @@ def main():
     solve_ms = e0.elapsed_time(e1) / args.apply
     # SpMV algorithmic bytes: per-slab values, x and y once, shared indices and coupling
     c = op.coupling
+    # round trip F (F^{-1} x) = x on the full operator (size-independent parity check)
+    op.solve(x, y)
+    z = op.apply(y)
+    round_trip = float(torch.linalg.norm(z - x) / torch.linalg.norm(x))
     spmv_bytes = (8 * args.nt * op.nnz + 2 * 8 * args.nt * op.n + 4 * op.nnz + 4 * (op.n + 1)
                   + 12 * c.nnz + 4 * (op.n + 1))
     peak = 6543.4
@@ -61,6 +65,7 @@ def main():
         "apply_inverse_ms": solve_ms, "apply_inverse_per_slab_us": 1e3 * solve_ms / args.nt,
         "factor_doubles_per_slab": info["factor_doubles"], "factor_GB": 8e-9 * info["factor_doubles"] * args.nt,
         "setup_s": {"host_tables_and_assembly": t_build, "factorisation": t_factor},
+        "round_trip_rel": round_trip,
         "timed": f"{args.spmv} SpMVs, {args.apply} exact-inverse applications (CUDA events)"}))
 
 
