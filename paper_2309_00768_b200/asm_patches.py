@@ -52,7 +52,7 @@ def _slot_offset(kd, d, c, il, jl):
     return off
 
 
-def build_patch_plan(disc, px: int = 4, py: int = 4):
+def build_patch_plan(disc, px: int = 6, py: int = 5):
     """Tables for values_patch_kernel, or None when the element pair is not P2/P1."""
     if disc.vel.nloc != 6 or disc.prs.nloc != 3:
         return None

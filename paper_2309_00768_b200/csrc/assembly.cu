@@ -323,119 +323,146 @@ __global__ void __launch_bounds__(256) values_kernel(AsmArgs a, ValArgs v) {
 //
 // Per (patch, slab): phase A evaluates the element matrices of every element the
 // patch's entries touch into shared memory.  Every entry is affine in the element
-// state (u, A, j), so E = W s with per-orientation linear maps W built on the host
-// (discretisation constants folded in): one lane per element, W rows as warp-uniform
-// broadcast loads, a compact loop (no instruction-cache pressure).  Phase B writes
-// each owned CSR entry of the merged Jacobian pattern and of F_p as the sum of its
-// element contributions (16-bit shared-memory offsets).  Same algebra as
+// state (u, A, j), so E = W s with per-orientation linear maps built on the host
+// (discretisation constants folded in).  A0: one lane per element stages its state
+// row (u, 1, grad A, j moments) in shared memory; A1: one thread per output row of
+// the maps holds its W row in registers and walks the elements of its orientation
+// (state rows are broadcast loads, stores are contiguous): no global loads in the
+// FMA loop.  Z_j, Z_A, Y are single products of grad A / the j moments, formed in the
+// reference's order (exact cancellations, e.g. d_x A = 0 on a Harris sheet, stay
+// exact).  Phase B writes each owned CSR entry of the merged Jacobian pattern and of
+// F_p as the sum of its element contributions (16-bit shared-memory offsets).  A CTA
+// walks a run of slabs so the W rows are loaded once per run.  Same algebra as
 // values_kernel, element-wise instead of entry-wise.
 struct PatchArgs {
-  int nt, npatch, nnv;
+  int nt, npatch, nnv, kchunk;
   int o_j, o_a;
   int64_t slab;
-  double idt, mu, ceta;
   const double *sc;  // clamped state
   const int *elem_v, *elem_1;
   const int4 *desc;  // {round offset, rounds, slot offset, n0 | n1 << 16}
   const int *slots, *out;
   const uint4 *codes;  // 8 x uint16 per table entry
-  const double2 *w;    // element linear map W1 (asm_patches.element_linear_maps)
+  const double *w;     // W1 [o][162][14] (asm_patches.element_linear_maps)
   const double *g1, *mx;  // reference-element G1[o][n][d], MX[il][n]
+  int phases;             // bit 0: element matrices, bit 1: entries (diagnostics: STMHD_PATCH_PHASES)
   double *js, *fp;
   int64_t js_stride, fp_stride;
 };
 
-constexpr int kPatchESZ = 270, kPatchRound = 256, kPatchMaxC = 6;
+constexpr int kPatchESZ = 270, kPatchRound = 256, kPatchMaxC = 6, kPatchThreads = 576;
+constexpr int kPatchSSZ = 24;  // state row: u (12), 1, pad, grad A (2), j moments (6), pad (2)
+constexpr int kPatchItems = 2 * 162 + 2 * 108;
 
-__global__ void __launch_bounds__(256, 2) values_patch_kernel(const __grid_constant__ PatchArgs P) {
-  extern __shared__ double E[];
+__global__ void __launch_bounds__(kPatchThreads, 1) values_patch_kernel(const __grid_constant__ PatchArgs P) {
+  extern __shared__ __align__(16) double E[];
   const int pt = blockIdx.x;
   const int4 dsc = P.desc[pt];
-  const int n0 = dsc.w & 0xffff, n1 = dsc.w >> 16;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int n0 = dsc.w & 0xffff, n1 = dsc.w >> 16, nsl = n0 + n1;
+  double *S = E + (size_t)nsl * kPatchESZ;  // state rows
   const int ntab = dsc.y * kPatchRound;
   const int *outp = P.out + (int64_t)dsc.x * kPatchRound;
   const uint4 *codep = P.codes + (int64_t)dsc.x * kPatchRound;
-  for (int k = blockIdx.y; k < P.nt; k += gridDim.y) {
+  // this thread's output rows (items): t and t + blockDim (W1 rows first, then Z/Y)
+  int it_o[1], it_q[1], it_src[1];
+  double it_c[1];
+  double wr[13];
+#pragma unroll
+  for (int r = 0; r < 1; ++r) {
+    const int it = threadIdx.x + r * kPatchThreads;
+    it_o[r] = -1;
+    it_q[r] = it_src[r] = 0;
+    it_c[r] = 0.0;
+    if (it < 324) {
+      const int o = it / 162, v = it % 162;
+      it_o[r] = o;
+      it_q[r] = v < 144 ? v : v + 108;
+#pragma unroll
+      for (int t = 0; t < 13; ++t) wr[t] = P.w[(o * 162 + v) * 14 + t];
+    } else if (it < kPatchItems) {
+      const int z = it - 324, o = z / 108, v = z % 108, q = v % 36;
+      it_o[r] = o;
+      it_q[r] = 144 + v;
+      if (v < 36) {  // ZJ[d][il][jl] = ga_d MX[il][jl]
+        it_src[r] = 14 + q / 18;
+        it_c[r] = P.mx[q % 18];
+      } else if (v < 72) {  // ZA[d][il][jl] = jm(il) G1[o][jl][d]
+        const int d = q / 18, il = (q / 3) % 6, jl = q % 3;
+        it_src[r] = 16 + il;
+        it_c[r] = P.g1[(o * 3 + jl) * 2 + d];
+      } else {  // Y[c][il][jl] = ga_c MX[jl][il]
+        const int c = q / 18, il = (q / 6) % 3, jl = q % 6;
+        it_src[r] = 14 + c;
+        it_c[r] = P.mx[jl * 3 + il];
+      }
+    }
+  }
+  const int k0 = blockIdx.y * P.kchunk, k1 = min(P.nt, k0 + P.kchunk);
+  for (int k = k0; k < k1; ++k) {
     const double *s = P.sc + (int64_t)k * P.slab;
-    // phase A: E = W s per element (lane = element; the warps of one orientation
-    // split the 270 outputs; W rows are warp-uniform broadcast loads)
-    {
-      const int o = warp & 1, nwo = nwarps >> 1, wo = warp >> 1;
-      const int no = o ? n1 : n0, sbase = o ? n0 : 0;
-      const double2 *W1 = P.w + o * (162 * 7);
-      for (int c0 = 0; c0 < no; c0 += 32) {
-        const int loc = c0 + lane;
-        const bool ok = loc < no;
-        const int sl = sbase + (ok ? loc : 0);
-        const int e = P.slots[dsc.z + sl];
-        double st[13], av[3], jv[3];
+    if (P.phases & 1) {
+      // A0: state rows
+      for (int sl = threadIdx.x; sl < nsl; sl += blockDim.x) {
+        const int e = P.slots[dsc.z + sl], o = e & 1;
+        double *row = S + sl * kPatchSSZ;
 #pragma unroll
         for (int m = 0; m < 6; ++m) {
           const int g = P.elem_v[e * 6 + m];
-          st[m] = s[g];
-          st[6 + m] = s[P.nnv + g];
+          row[m] = s[g];
+          row[6 + m] = s[P.nnv + g];
         }
-        st[12] = 1.0;
+        row[12] = 1.0;
+        row[13] = 0.0;
+        double av[3], jv[3];
 #pragma unroll
         for (int n = 0; n < 3; ++n) {
           const int g = P.elem_1[e * 3 + n];
           av[n] = s[P.o_a + g];
           jv[n] = s[P.o_j + g];
         }
-        double *Es = E + sl * kPatchESZ;
-        // FU, FA, FP: affine in u (W1 rows)
-        for (int v = wo; v < 162; v += nwo) {
-          const double2 *w = W1 + v * 7;
-          double acc = 0.0;
-#pragma unroll
-          for (int t = 0; t < 6; ++t) {
-            const double2 c = __ldg(w + t);
-            acc = fma(c.x, st[2 * t], acc);
-            acc = fma(c.y, st[2 * t + 1], acc);
-          }
-          acc = fma(__ldg(w + 6).x, st[12], acc);
-          if (ok) Es[v < 144 ? v : 252 + (v - 144)] = acc;
-        }
-        // Z_j, Z_A, Y: grad A and the j moments first, in the reference's order (keeps
-        // exact cancellations, e.g. d_x A = 0 on a Harris sheet), then one product each
-        double ga[2], jm[6];
 #pragma unroll
         for (int d = 0; d < 2; ++d) {
-          ga[d] = 0.0;
+          double ga = 0.0;
 #pragma unroll
-          for (int n = 0; n < 3; ++n) ga[d] += av[n] * __ldg(&P.g1[(o * 3 + n) * 2 + d]);
+          for (int n = 0; n < 3; ++n) ga += av[n] * P.g1[(o * 3 + n) * 2 + d];
+          row[14 + d] = ga;
         }
 #pragma unroll
         for (int il = 0; il < 6; ++il) {
-          jm[il] = 0.0;
+          double jm = 0.0;
 #pragma unroll
-          for (int n = 0; n < 3; ++n) jm[il] += jv[n] * __ldg(&P.mx[il * 3 + n]);
+          for (int n = 0; n < 3; ++n) jm += jv[n] * P.mx[il * 3 + n];
+          row[16 + il] = jm;
         }
-        for (int v = wo; v < 108; v += nwo) {
-          const int q = v % 36;
-          double val;
-          if (v < 36) {  // ZJ[d][il][jl] = ga_d MX[il][jl]
-            val = (q < 18 ? ga[0] : ga[1]) * __ldg(&P.mx[q % 18]);
-          } else if (v < 72) {  // ZA[d][il][jl] = jm(il) G1[jl][d]
-            const int d = q / 18, il = (q / 3) % 6, jl = q % 3;
-            double j_il = jm[0];
+      }
+      __syncthreads();
+      // A1: output rows x elements of their orientation
 #pragma unroll
-            for (int i = 1; i < 6; ++i)
-              if (il == i) j_il = jm[i];
-            val = j_il * __ldg(&P.g1[(o * 3 + jl) * 2 + d]);
-          } else {  // Y[c][il][jl] = ga_c MX[jl][il]
-            const int c = q / 18, il = (q / 6) % 3, jl = q % 6;
-            val = ga[c] * __ldg(&P.mx[jl * 3 + il]);
+      for (int r = 0; r < 1; ++r) {
+        const int o = it_o[r];
+        if (o < 0) continue;
+        const int sb = o ? n0 : 0, se = o ? nsl : n0;
+        if (it_q[r] < 144 || it_q[r] >= 252) {
+          for (int sl = sb; sl < se; ++sl) {
+            const double2 *row = reinterpret_cast<const double2 *>(S + sl * kPatchSSZ);
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int t = 0; t < 6; ++t) {
+              const double2 x = row[t];
+              a0 = fma(wr[2 * t], x.x, a0);
+              a1 = fma(wr[2 * t + 1], x.y, a1);
+            }
+            E[sl * kPatchESZ + it_q[r]] = fma(wr[12], 1.0, a0 + a1);
           }
-          if (ok) Es[144 + v] = val;
+        } else {
+          for (int sl = sb; sl < se; ++sl) E[sl * kPatchESZ + it_q[r]] = S[sl * kPatchSSZ + it_src[r]] * it_c[r];
         }
       }
     }
     __syncthreads();
     // phase B: owned entries; 8 codes per entry in one 16-byte word; 4 entries per
     // thread in flight (table loads are L2 round trips)
-    for (int i0 = threadIdx.x; i0 < ntab; i0 += 4 * blockDim.x) {
+    for (int i0 = threadIdx.x; i0 < ((P.phases & 2) ? ntab : 0); i0 += 4 * blockDim.x) {
       int w[4];
       uint4 cw[4];
 #pragma unroll
@@ -474,9 +501,6 @@ static void values_patch(stmhd_disc_s *d, const AsmArgs &a, cudaStream_t s, doub
   P.o_j = a.n_u + a.n_p;
   P.o_a = P.o_j + a.n_j;
   P.slab = a.slab;
-  P.idt = 1.0 / a.dt;
-  P.mu = a.mu;
-  P.ceta = a.eta / a.mu0;
   P.sc = a.sc;
   P.elem_v = a.elem_v;
   P.elem_1 = a.elem_1;
@@ -484,27 +508,34 @@ static void values_patch(stmhd_disc_s *d, const AsmArgs &a, cudaStream_t s, doub
   P.slots = d->D<int>("pa_slots");
   P.out = d->D<int>("pa_out");
   P.codes = d->D<uint4>("pa_codes");
-  P.w = d->D<double2>("pa_w");
+  P.w = d->D<double>("pa_w");
   {
     constexpr TOff O = toff(6, 3);
     P.g1 = d->D<double>("tensors") + O.G1;
     P.mx = d->D<double>("tensors") + O.MX;
   }
-  // outputs the caller did not ask for go to a scratch slab-sized sink? No: both are
-  // required together (the plan interleaves js and F_p entries)
   P.js = js;
   P.fp = fp;
+  {
+    static const int ph = [] {
+      const char *e = getenv("STMHD_PATCH_PHASES");
+      return e ? atoi(e) : 3;
+    }();
+    P.phases = ph;
+  }
   P.js_stride = d->I("nnz_js");
   P.fp_stride = d->I("nnz_fp");
-  const size_t smem = (size_t)d->I("pa_max_slots") * kPatchESZ * sizeof(double);
+  const size_t smem = (size_t)d->I("pa_max_slots") * (kPatchESZ + kPatchSSZ) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     STMHD_CUDA_CHECK(cudaFuncSetAttribute(values_patch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          113 * 1024));
+                                          225 * 1024));
     attr = true;
   }
-  require(smem <= 113 * 1024, "patch assembly: element matrices exceed shared memory");
-  values_patch_kernel<<<dim3(P.npatch, a.nt), 256, smem, s>>>(P);
+  require(smem <= 225 * 1024, "patch assembly: element matrices exceed shared memory");
+  // slab runs per CTA: W rows loaded once per run, >= ~2 waves of one CTA per SM
+  P.kchunk = std::max(1, std::min(8, (int)((int64_t)P.npatch * a.nt / (2 * num_sms()))));
+  values_patch_kernel<<<dim3(P.npatch, cdiv(a.nt, P.kchunk)), kPatchThreads, smem, s>>>(P);
   STMHD_LAUNCH_CHECK();
 }
 

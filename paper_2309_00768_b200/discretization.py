@@ -11,6 +11,7 @@ blocks M_j, M_A^bc, M_p, K_p^pin on the device (problems.py:225-228).
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import scipy.sparse as sp
@@ -185,7 +186,8 @@ class Discretization:
         # element-matrix patch plan of the Jacobian assembly (P2/P1)
         from .asm_patches import build_patch_plan, build_residual_plan
 
-        pp = build_patch_plan(self)
+        ps = os.environ.get("STMHD_PATCH", "6x5").split("x")  # cells per patch (r01 sweep: 6x5 best)
+        pp = build_patch_plan(self, int(ps[0]), int(ps[1]))
         if pp is not None:
             up("pa_desc", pp["desc"]), up("pa_slots", pp["slots"]), up("pa_out", pp["out"])
             up("pa_codes", pp["codes"]), up("pa_w", pp["w"])
