@@ -59,13 +59,18 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(SellArgs a) {
     vq[q] = va + (int64_t)kq * a.sell_a;
     xq[q] = a.x + (int64_t)(k0 + kq) * a.xs;
   }
+  // column indices run one batch ahead of the value loads and x gathers, so the
+  // col -> x dependency does not serialise two memory latencies per batch
+  int c[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) c[i] = i < lenA ? ca[i * 32] : 0;
   for (int j = 0; j < sl.x; j += B) {
-    int c[B];
     bool on[B];
+    int cn[B];
 #pragma unroll
     for (int i = 0; i < B; ++i) {
       on[i] = j + i < lenA;
-      c[i] = on[i] ? ca[(j + i) * 32] : 0;
+      cn[i] = (j + B + i < lenA) ? ca[(j + B + i) * 32] : 0;
     }
     double v[S][B], xv[S][B];
 #pragma unroll
@@ -79,6 +84,8 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(SellArgs a) {
     for (int q = 0; q < S; ++q)
 #pragma unroll
       for (int i = 0; i < B; ++i) sa[q][i & 1] = fma(v[q][i], xv[q][i], sa[q][i & 1]);
+#pragma unroll
+    for (int i = 0; i < B; ++i) c[i] = cn[i];
   }
   double sb[S];
 #pragma unroll
@@ -207,7 +214,8 @@ void StSpmvPlan::apply(int nt, const double *sell, double alpha_a, double alpha_
     const char *e = getenv("STMHD_SELL_SB");
     return e ? atoi(e) : 0;
   }();
-  const int S = sb ? sb / 10 : 2, B = sb ? sb % 10 : 4;  // measured best for J.v and C5 (r01)
+  // measured (r01): J.v (rows ~45 entries) 2 slabs x 4, C5 (rows ~14) 4 slabs x 4
+  const int S = sb ? sb / 10 : (nnz_a >= (int64_t)16 * nrows ? 2 : 4), B = sb ? sb % 10 : 4;
   const dim3 blk(256);
   auto grid = [&](int s_) { return dim3(cdiv(nslices, 8), cdiv(nt, s_)); };
   if (S == 1 && B == 8) sell_spmv_kernel<1, 8><<<grid(1), blk, 0, s>>>(a);
