@@ -238,7 +238,9 @@ SweepStagePtr sweep_stage_new();
 // same tag (a preconditioner's lifetime), so their gathered copy is reused.
 void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
                          int64_t ld_x, int nrhs, const SweepCoupling *cpl, int ncpl, SweepStage *const *ext,
-                         int next, cudaStream_t s, int64_t vals_tag = 0, int ncta = 0);
+                         int next, cudaStream_t s, int64_t vals_tag = 0, int ncta = 0, bool grid = false,
+                         int warps_force = 0);
+int sweep_stage_warps(const SweepStage &st);
 // After every slab k, add sum_c coef_c C_c src_c(k) to target's right-hand side of
 // slab k (before publishing slab k).  Sources: this stage's x_k (ext < 0) or its
 // external stages.  Call after both stages are prepared, before the launch.
@@ -246,8 +248,8 @@ void sweep_stage_set_post(SweepStage &st, SweepStage &target, const SweepCouplin
                           int64_t vals_tag = 0);
 // Run prepared stages in ONE launch, one 16-CTA cluster each, pipelined slab by slab
 // (a consumer waits on per-slab release flags of its producers); then permute out.
-// A stage prepared with ncta != 16 runs alone in grid mode (ncta CTAs, cooperative
-// launch, software grid barrier).
+// Stages prepared with grid = true (or ncta != 16) form a grid-family launch: no
+// clusters, cooperative launch, stage i on its own ncta CTAs with a software barrier.
 void sweep_stages_launch(SweepStage *const *st, int nst, cudaStream_t s);
 
 // Cluster-resident sweep in nested-dissection order (nd_sweep.cu).

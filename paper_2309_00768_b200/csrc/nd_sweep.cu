@@ -618,6 +618,7 @@ struct SweepArgs {
   const double *ext_xp[2];
   int64_t ext_n[2];
   const int *flag_in[2];  // per producer: [slab][cta] = epoch once slab written
+  int ext_ncta[2];        // per producer: its CTA count
   int nwait;
   int *flag_out;          // this stage's flags (null: not consumed)
   int epoch;
@@ -630,13 +631,14 @@ struct SweepArgs {
   unsigned long long *tline; // PROF instantiation: per-warp event timeline of slab 1, CTA 0 (128 per warp)
 };
 
-__device__ __forceinline__ void sweep_barrier(const SweepArgs &a) {
+__device__ __forceinline__ void sweep_barrier(const SweepArgs &a, int crank) {
   if (a.gbar) {
-    // grid barrier over the launch's CTAs (cooperative-groups arrival scheme: every
-    // CTA adds 1, CTA 0 adds 2^31 - (n - 1), so the top bit flips once all arrived)
+    // software barrier over the stage's a.ncta CTAs (cooperative-groups arrival
+    // scheme: every CTA adds 1, rank 0 adds 2^31 - (n - 1), so the top bit flips once
+    // all arrived)
     __syncthreads();
     if (threadIdx.x == 0) {
-      const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+      const unsigned nb = crank == 0 ? 0x80000000u - (unsigned)(a.ncta - 1) : 1u;
       __threadfence();
       const unsigned old = atomicAdd(a.gbar, nb);
       unsigned cur;
@@ -674,8 +676,8 @@ __device__ __forceinline__ void st_release_gpu(int *p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ void sweep_trace(const SweepArgs &a, int &step) {
-  if (a.trace && threadIdx.x == 0 && (a.gbar ? blockIdx.x == 0 : cluster_rank() == 0)) {
+__device__ __forceinline__ void sweep_trace(const SweepArgs &a, int &step, int crank) {
+  if (a.trace && threadIdx.x == 0 && crank == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[step] = t;
@@ -1126,6 +1128,7 @@ __device__ __forceinline__ void run_program(const int4 hd, const int2 *items, co
 // Up to three sweeps of one pipelined launch, one cluster each (cluster i runs st[i]).
 struct SweepMulti {
   SweepArgs st[3];
+  int first[4];  // grid-family launch: stage i owns CTAs [first[i], first[i+1])
 };
 
 template <bool PROF>
@@ -1134,9 +1137,19 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   __shared__ __align__(8) unsigned long long mbar[16][2];
   __shared__ SweepArgs sa;
   __shared__ const double *s_src[8];  // coupling sources of the current slab (by source id)
-  const bool grid = m.st[0].gbar != nullptr;  // grid mode: one stage, CTA rank = blockIdx.x
-  const unsigned cid = grid ? 0u : cluster_index();
-  const int crank = grid ? (int)blockIdx.x : (int)cluster_rank();
+  // grid-family launch (no clusters, software barriers): stages own CTA ranges;
+  // cluster launch: stage = cluster index, rank = rank in the cluster
+  const bool grid = m.st[0].gbar != nullptr;
+  unsigned cid;
+  int crank;
+  if (grid) {
+    const int b = (int)blockIdx.x;
+    cid = b >= m.first[2] ? 2u : (b >= m.first[1] ? 1u : 0u);
+    crank = b - m.first[cid];
+  } else {
+    cid = cluster_index();
+    crank = (int)cluster_rank();
+  }
   if (threadIdx.x == 0) {
     if (cid == 0) sa = m.st[0];
     else if (cid == 1) sa = m.st[1];
@@ -1209,7 +1222,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   __syncwarp();
   const int64_t n = a.n;
   int step = 0;
-  sweep_trace(a, step);
+  sweep_trace(a, step, crank);
   for (int k = 0; k < a.nslab; ++k) {
     const double *rhs = a.rhsp + (int64_t)k * n;
     double *x = a.xp + (int64_t)k * n;
@@ -1227,9 +1240,10 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
         s_src[5] = s_src[6] = s_src[7] = a.zero;  // 5: own x_k (post-slab program only)
       }
       // pipelined launch: wait until every CTA of each producer has published slab k
-      if ((int)threadIdx.x < a.nwait * a.ncta) {
-        const int e = threadIdx.x / a.ncta, c = threadIdx.x % a.ncta;
-        const int *f = a.flag_in[e] + (int64_t)k * a.ncta + c;
+      for (int t = threadIdx.x; t < (a.nwait > 0 ? a.ext_ncta[0] : 0) + (a.nwait > 1 ? a.ext_ncta[1] : 0);
+           t += blockDim.x) {
+        const int e = t < a.ext_ncta[0] ? 0 : 1, c = e ? t - a.ext_ncta[0] : t;
+        const int *f = a.flag_in[e] + (int64_t)k * a.ext_ncta[e] + c;
         unsigned long long t0, t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
         while (ld_acquire_gpu(f) != a.epoch) {
@@ -1241,7 +1255,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       const double *vk = a.prog_vals + (a.prog_per_slab ? (int64_t)k * a.prog_nent : 0);
       run_program<0>(a.prog_hdr[crank], a.prog_items, a.prog_ecol, vk, rhs, nullptr, sv, a.tbuf, s_src);
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
-      sweep_trace(a, step);
+      sweep_trace(a, step, crank);
     }
     const double *F = a.factors + (int64_t)k * a.fstride;
     // phase levels of this warp's list: subtree forward (CTA-local), top forward,
@@ -1258,8 +1272,8 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
     }
     if (a.nsub || a.prog_hdr) {  // subtree roots' updates and coupled top rows visible
-      tb = pclock<PROF>(); sweep_barrier(a); if (PROF) w.acc[3] += pclock<PROF>() - tb;
-      sweep_trace(a, step);
+      tb = pclock<PROF>(); sweep_barrier(a, crank); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+      sweep_trace(a, step, crank);
     }
     if (a.dense) {
       // z_T = coupled rhs of the top unknowns + the subtree roots' updates (all CTAs
@@ -1278,34 +1292,34 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
         sv.zs[i] = z;
       }
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
-      sweep_trace(a, step);
+      sweep_trace(a, step, crank);
       const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
       if (PROF) tl_mark(w, 1);
       for (int ti = w.bnd[L]; ti < t1; ++ti) dense_task<PROF>(a, w.tl[ti], sv.zs, x, k, w, mbar);
       if (PROF) tl_mark(w, 4);
       ++L;
-      tb = pclock<PROF>(); sweep_barrier(a); if (PROF) w.acc[3] += pclock<PROF>() - tb;  // x_T visible
+      tb = pclock<PROF>(); sweep_barrier(a, crank); if (PROF) w.acc[3] += pclock<PROF>() - tb;  // x_T visible
       if (a.tab_ints) {  // stage x_T in shared memory for the subtree backward tables
         for (int i = threadIdx.x; i < a.ntT; i += blockDim.x) sv.zs[i] = x[a.ztab[2 * i].x];
         __syncthreads();
       }
-      sweep_trace(a, step);
+      sweep_trace(a, step, crank);
     } else {
       for (int t = 0; t < a.ntop; ++t, ++L) {
         const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
         for (int ti = w.bnd[L]; ti < t1; ++ti) forward_task<false, PROF>(a, w.tl[ti], F, rhs, sv, w, mbar);
-        tb = pclock<PROF>(); sweep_barrier(a); if (PROF) w.acc[3] += pclock<PROF>() - tb;
-        sweep_trace(a, step);
+        tb = pclock<PROF>(); sweep_barrier(a, crank); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+        sweep_trace(a, step, crank);
       }
       for (int t = a.ntop - 1; t >= 0; --t, ++L) {
         const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
         for (int ti = w.bnd[L]; ti < t1; ++ti) backward_task<false, PROF>(a, w.tl[ti], F, x, sv, w, mbar);
         if (t > 0 || a.nsub || k + 1 < a.nslab) {
           tb = pclock<PROF>();
-          sweep_barrier(a);
+          sweep_barrier(a, crank);
           if (PROF) w.acc[3] += pclock<PROF>() - tb;
         }
-        sweep_trace(a, step);
+        sweep_trace(a, step, crank);
       }
     }
     for (int h = a.nsub - 1; h >= 0; --h, ++L) {
@@ -1318,7 +1332,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     if (a.post_hdr && !a.null_work) {
       // post-slab program: rows of another stage's right-hand side from this stage's
       // x_k (all CTAs' parts: cluster barrier) and external sources at slab k
-      sweep_barrier(a);
+      sweep_barrier(a, crank);
       if (threadIdx.x == 0) {
         s_src[3] = a.ext_xp[0] ? a.ext_xp[0] + (int64_t)k * a.ext_n[0] : a.zero;
         s_src[4] = a.ext_xp[1] ? a.ext_xp[1] + (int64_t)k * a.ext_n[1] : a.zero;
@@ -1335,8 +1349,8 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       if (threadIdx.x == 0) st_release_gpu(a.flag_out + (int64_t)k * a.ncta + crank, a.epoch);
     }
     if (a.nsub && k + 1 < a.nslab) {  // x_k visible to every CTA's next coupling
-      tb = pclock<PROF>(); sweep_barrier(a); if (PROF) w.acc[3] += pclock<PROF>() - tb;
-      sweep_trace(a, step);
+      tb = pclock<PROF>(); sweep_barrier(a, crank); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+      sweep_trace(a, step, crank);
     }
   }
   if (PROF && lane == 0)
@@ -1687,6 +1701,7 @@ struct SweepStage {
 };
 
 void SweepStageDeleter::operator()(SweepStage *p) const { delete p; }
+int sweep_stage_warps(const SweepStage &st) { return st.warps; }
 SweepStagePtr sweep_stage_new() { return SweepStagePtr(new SweepStage()); }
 
 static constexpr int kCluster = 16, kWarps = 16;
@@ -1715,10 +1730,11 @@ static int gather_values(const CplProgram &pg, const SweepCoupling *cpl, int ncp
 
 void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
                          int64_t ld_x, int nrhs, const SweepCoupling *cpl, int ncpl, SweepStage *const *ext,
-                         int next, cudaStream_t s, int64_t vals_tag, int ncta) {
+                         int next, cudaStream_t s, int64_t vals_tag, int ncta, bool grid, int warps_force) {
   const NDDevice &dev = *fac.dev;
   const NDPlan &p = *dev.plan;
   if (ncta <= 0) ncta = kCluster;
+  grid = grid || ncta != kCluster;
   if (st.ncta != ncta) st.warps = 0;  // re-choose the warps for a new CTA count
   st.ncta = ncta;
   const int cluster = ncta;
@@ -1732,6 +1748,7 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   };
   // prefer the most warps whose plan keeps the CTA-local subtree phase (fewer
   // cluster/grid barriers per slab), else the most warps whose flat plan fits
+  if (warps_force > 0) st.warps = warps_force;
   int warps = st.warps;
   if (!warps) {
     int flat = 0;
@@ -1843,7 +1860,7 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   a.null_work = env_int2("STMHD_SWEEP_NULL", 0);
   a.post_hdr = nullptr;  // set by sweep_stage_set_post for this launch
   a.gbar = nullptr;
-  if (ncta != kCluster) {  // grid mode
+  if (grid) {  // grid-family launch: software barrier
     if (!st.gbar.ptr) {
       st.gbar.alloc(sizeof(unsigned));
       STMHD_CUDA_CHECK(cudaMemsetAsync(st.gbar.ptr, 0, sizeof(unsigned), s));
@@ -1859,6 +1876,7 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
     a.flag_in[e] = nullptr;
     a.ext_xp[e] = ext[e]->a.xp;
     a.ext_n[e] = ext[e]->a.n;
+    a.ext_ncta[e] = ext[e]->ncta;
   }
   st.a.flag_out = nullptr;
 }
@@ -1990,7 +2008,7 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
     SweepStage &st = *stg[i];
     st.a.epoch = epoch;
     if (nst > 1) {  // every stage publishes per-slab flags
-      const int64_t need = (int64_t)st.nrhs * kCluster;
+      const int64_t need = (int64_t)st.nrhs * st.ncta;
       if (st.flags_slabs < need) {
         st.flags.alloc_async(need * sizeof(int), s);
         STMHD_CUDA_CHECK(cudaMemsetAsync(st.flags.ptr, 0, need * sizeof(int), s));
@@ -2005,7 +2023,12 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
   }
   const int warps = stg[0]->warps;
   const bool grid = stg[0]->a.gbar != nullptr;
-  require(!grid || nst == 1, "sweep: grid mode runs one stage per launch");
+  int first[4] = {0, 0, 0, 0};
+  for (int i = 0; i < nst; ++i) {
+    require((stg[i]->a.gbar != nullptr) == grid, "sweep: all stages of a launch in grid or cluster mode");
+    require(grid || stg[i]->ncta == kCluster, "sweep: cluster launches take 16-CTA stages");
+    first[i + 1] = first[i] + stg[i]->ncta;
+  }
   for (int i = 0; i < nst; ++i) {
     SweepStage &st = *stg[i];
     for (int e = 0; e < st.a.nwait; ++e) {
@@ -2046,14 +2069,15 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
   DevBuf pr;
   DevBuf tlb;
   if (prof_on) {
-    pr.alloc((size_t)stg[0]->ncta * warps * 8 * sizeof(unsigned long long));
+    pr.alloc((size_t)stg[ts]->ncta * warps * 8 * sizeof(unsigned long long));
     m.st[ts].prof = pr.as<unsigned long long>();
     tlb.alloc((size_t)warps * 128 * sizeof(unsigned long long));
     STMHD_CUDA_CHECK(cudaMemsetAsync(tlb.ptr, 0, tlb.bytes, s));
     m.st[ts].tline = tlb.as<unsigned long long>();
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid ? stg[0]->ncta : kCluster * nst);
+  cfg.gridDim = dim3(grid ? first[nst] : kCluster * nst);
+  for (int i = 0; i < 4; ++i) m.first[i] = i <= nst ? first[i] : first[nst];
   cfg.blockDim = dim3(warps * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -2110,7 +2134,7 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
             (long long)a.sub_cb);
   }
   if (prof_on) {
-    const int nwp = stg[0]->ncta * warps;
+    const int nwp = stg[ts]->ncta * warps;
     std::vector<unsigned long long> h((size_t)nwp * 8);
     STMHD_CUDA_CHECK(cudaMemcpyAsync(h.data(), pr.ptr, h.size() * 8, cudaMemcpyDeviceToHost, s));
     STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -2160,7 +2184,7 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   const double fbytes = 8.0 * (double)fac.dev->plan->factor_size;
   const bool grid = grid_env == 1 || (grid_env < 0 && fbytes > 32e6);
   sweep_stage_prepare(*sp, fac, rhs, ld_rhs, x, ld_x, nrhs, cpl, ncpl, nullptr, 0, s, 0,
-                      grid ? num_sms() : kCluster);
+                      grid ? num_sms() : kCluster, grid);
   SweepStage *one = sp.get();
   sweep_stages_launch(&one, 1, s);
 }

@@ -428,7 +428,21 @@ void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
   static int64_t next_tag = 0;
   if (!vals_tag) vals_tag = ++next_tag;
   const int64_t tag = vals_tag;
-  sweep_stage_prepare(*st_wave, *ca, ta2.as<double>(), n_a, x + o_a, slab, nt, cw, 2, nullptr, 0, s, tag);
+  // large velocity factors (64^2 meshes: 45 MB per slab) stream faster from most of
+  // the GPU: grid-family launch with the wave and M_j sweeps on 16 CTAs each and the
+  // velocity sweep on the remaining SMs (software barriers); smaller ones keep the
+  // three-cluster launch (hardware cluster barrier, dense top)
+  static const int grid_env = [] {
+    const char *e = getenv("STMHD_PC_GRID");
+    return e ? atoi(e) : -1;
+  }();
+  const bool grid = grid_env == 1 || (grid_env < 0 && 8.0 * (double)fu->dev->plan->factor_size > 24e6 &&
+                                      num_sms() >= 64);
+  const int nc_fu = grid ? num_sms() - 32 : 16;
+  // grid-family launches need one warp count for all stages: the velocity stage's
+  // choice (the others have slack) is remembered after the first preparation
+  const int wf = grid ? pipe_warps : 0;
+  sweep_stage_prepare(*st_wave, *ca, ta2.as<double>(), n_a, x + o_a, slab, nt, cw, 2, nullptr, 0, s, tag, 16, grid, wf);
   SweepCoupling cj;  // -K_jA x_A
   DCsr mix = d->csr("mixja");
   cj.rowptr = mix.rowptr;
@@ -437,7 +451,7 @@ void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
   cj.ext = 0;
   cj.coef = -1.0;
   SweepStage *wj[1] = {st_wave.get()};
-  sweep_stage_prepare(*st_mj, *d->lu_mj, r_j, slab, x + o_j, slab, nt, &cj, 1, wj, 1, s, tag);
+  sweep_stage_prepare(*st_mj, *d->lu_mj, r_j, slab, x + o_j, slab, nt, &cj, 1, wj, 1, s, tag, 16, grid, wf);
   SweepCoupling cu;  // + M_u/dt x_u(k-1); waits on the M_j stage (which adds the Z terms)
   DCsr m = d->csr("mu_dt");
   cu.rowptr = m.rowptr;
@@ -447,7 +461,18 @@ void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
   cu.coef = 1.0;
   SweepStage *ju[1] = {st_mj.get()};
   STMHD_CUDA_CHECK(cudaStreamWaitEvent(s, ev_join, 0));  // tu1 (pressure chain) ready
-  sweep_stage_prepare(*st_vel, *fu, tu1.as<double>(), n_u, x, slab, nt, &cu, 1, ju, 1, s, tag);
+  sweep_stage_prepare(*st_vel, *fu, tu1.as<double>(), n_u, x, slab, nt, &cu, 1, ju, 1, s, tag, nc_fu, grid, wf);
+  if (grid && !pipe_warps) {
+    pipe_warps = sweep_stage_warps(*st_vel);
+    if (sweep_stage_warps(*st_wave) != pipe_warps || sweep_stage_warps(*st_mj) != pipe_warps) {
+      sweep_stage_prepare(*st_wave, *ca, ta2.as<double>(), n_a, x + o_a, slab, nt, cw, 2, nullptr, 0, s, tag, 16, grid,
+                          pipe_warps);
+      sweep_stage_prepare(*st_mj, *d->lu_mj, r_j, slab, x + o_j, slab, nt, &cj, 1, wj, 1, s, tag, 16, grid,
+                          pipe_warps);
+      sweep_stage_prepare(*st_vel, *fu, tu1.as<double>(), n_u, x, slab, nt, &cu, 1, ju, 1, s, tag, nc_fu, grid,
+                          pipe_warps);
+    }
+  }
   // after slab k of the M_j stage: rhs_u(k) += -Z_j x_j(k) - Z_a x_A(k)
   SweepCoupling cz[2];
   cz[0].rowptr = d->D<int>("js_seg0");  // z_j segment of the u rows, slab columns o_j + j

@@ -1,0 +1,54 @@
+"""Grid-mode sweeps (one CTA per SM / grid-family pipelined launch with software
+barriers, nd_sweep.cu) give the same P_T^{-1} and C5 inverse as the cluster mode:
+a child process forces the grid modes (STMHD_SWEEP_GRID=1, STMHD_PC_GRID=1) and its
+results are compared with this process's cluster-mode results."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2309_00768_b200 as p
+from paper_2309_00768_b200 import c5
+d = p.discretize_config("C1")
+st = p.initial_state(d)
+st.vec.data += 1e-3 * torch.randn(st.vec.data.shape, dtype=torch.float64, device="cuda",
+                                  generator=torch.Generator(device="cuda").manual_seed(0))
+jac = p.assemble_jacobian(st, d)
+pc = p.SpaceTimePreconditioner(jac, d, st)
+r = torch.randn(jac.size, dtype=torch.float64, device="cuda", generator=torch.Generator(device="cuda").manual_seed(1))
+z = pc.apply_inverse(r)
+n, nt = 16, 6
+u = c5.c5_velocity_fields(c5.c5_host_tables(n)["p1"].coords, nt, seed=3)
+op = c5.C5Operator(n, nt, ufields=u)
+x = np.random.default_rng(4).standard_normal(nt * op.n)
+s = op.solve(x)
+np.savez(sys.argv[2], z=z.cpu().numpy(), s=s.cpu().numpy())
+"""
+
+
+def _run(tmp_path, env_extra, name):
+    env = dict(os.environ, **env_extra)
+    out = str(tmp_path / name)
+    subprocess.run([sys.executable, "-c", CHILD, ROOT, out], env=env, check=True, timeout=600)
+    return np.load(out)
+
+
+def test_grid_modes_match_cluster_mode(tmp_path):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    a = _run(tmp_path, {"STMHD_SWEEP_GRID": "0", "STMHD_PC_GRID": "0"}, "cluster.npz")
+    b = _run(tmp_path, {"STMHD_SWEEP_GRID": "1", "STMHD_PC_GRID": "1"}, "grid.npz")
+    for k in ("z", "s"):
+        err = np.linalg.norm(a[k] - b[k]) / np.linalg.norm(a[k])
+        assert err < 1e-10, (k, err)
