@@ -346,6 +346,7 @@ struct PatchArgs {
   const double *w;     // W1 [o][162][14] (asm_patches.element_linear_maps)
   const double *g1, *mx;  // reference-element G1[o][n][d], MX[il][n]
   int phases;             // bit 0: element matrices, bit 1: entries (diagnostics: STMHD_PATCH_PHASES)
+  int pipe;               // double-buffered software pipeline over the slab run
   double *js, *fp;
   int64_t js_stride, fp_stride;
 };
@@ -355,111 +356,132 @@ constexpr int kPatchSSZ = 24;  // state row: u (12), 1, pad, grad A (2), j momen
 constexpr int kPatchItems = 2 * 162 + 2 * 108;
 
 __global__ void __launch_bounds__(kPatchThreads, 1) values_patch_kernel(const __grid_constant__ PatchArgs P) {
-  extern __shared__ __align__(16) double E[];
+  extern __shared__ __align__(16) double smem_e[];
   const int pt = blockIdx.x;
   const int4 dsc = P.desc[pt];
   const int n0 = dsc.w & 0xffff, n1 = dsc.w >> 16, nsl = n0 + n1;
-  double *S = E + (size_t)nsl * kPatchESZ;  // state rows
+  // two buffers of element matrices, then two of state rows
+  // pipelined: two buffers of element matrices, then two of state rows; sequential:
+  // one of each (the buffer pointers alias)
+  const int nb = P.pipe ? 2 : 1;
+  double *const E0 = smem_e, *const E1 = smem_e + (size_t)(nb - 1) * nsl * kPatchESZ;
+  double *const S0 = smem_e + (size_t)nb * nsl * kPatchESZ, *const S1 = S0 + (size_t)(nb - 1) * nsl * kPatchSSZ;
   const int ntab = dsc.y * kPatchRound;
   const int *outp = P.out + (int64_t)dsc.x * kPatchRound;
   const uint4 *codep = P.codes + (int64_t)dsc.x * kPatchRound;
-  // this thread's output rows (items): t and t + blockDim (W1 rows first, then Z/Y)
-  int it_o[1], it_q[1], it_src[1];
-  double it_c[1];
-  double wr[13];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  // FU/FA/FP rows: E_o = S_o W1_o^T on the FP64 tensor cores (mma m8n8k4): 2 x 21
+  // n-tiles of 8 output rows over the warps, the B fragments (W1) in registers
+  constexpr int kNT = 21, kMaxTW = 3;
+  double bf[kMaxTW][4];
 #pragma unroll
-  for (int r = 0; r < 1; ++r) {
-    const int it = threadIdx.x + r * kPatchThreads;
-    it_o[r] = -1;
-    it_q[r] = it_src[r] = 0;
-    it_c[r] = 0.0;
-    if (it < 324) {
-      const int o = it / 162, v = it % 162;
-      it_o[r] = o;
-      it_q[r] = v < 144 ? v : v + 108;
+  for (int i = 0; i < kMaxTW; ++i) {
+    const int t = warp + i * nwarps;
+    const int o = t / kNT, n = (t % kNT) * 8 + (lane >> 2);
 #pragma unroll
-      for (int t = 0; t < 13; ++t) wr[t] = P.w[(o * 162 + v) * 14 + t];
-    } else if (it < kPatchItems) {
-      const int z = it - 324, o = z / 108, v = z % 108, q = v % 36;
-      it_o[r] = o;
-      it_q[r] = 144 + v;
-      if (v < 36) {  // ZJ[d][il][jl] = ga_d MX[il][jl]
-        it_src[r] = 14 + q / 18;
-        it_c[r] = P.mx[q % 18];
-      } else if (v < 72) {  // ZA[d][il][jl] = jm(il) G1[o][jl][d]
-        const int d = q / 18, il = (q / 3) % 6, jl = q % 3;
-        it_src[r] = 16 + il;
-        it_c[r] = P.g1[(o * 3 + jl) * 2 + d];
-      } else {  // Y[c][il][jl] = ga_c MX[jl][il]
-        const int c = q / 18, il = (q / 6) % 3, jl = q % 6;
-        it_src[r] = 14 + c;
-        it_c[r] = P.mx[jl * 3 + il];
-      }
+    for (int ks = 0; ks < 4; ++ks) {
+      const int kk = ks * 4 + (lane & 3);
+      bf[i][ks] = (t < 2 * kNT && n < 162 && kk < 14) ? P.w[(o * 162 + n) * 14 + kk] : 0.0;
     }
   }
+  // Z_j, Z_A, Y rows: one product each (threads 0..215)
+  int z_o = -1, z_q = 0, z_src = 0;
+  double z_c = 0.0;
+  if ((int)threadIdx.x < 216) {
+    const int z = threadIdx.x, o = z / 108, v = z % 108, q = v % 36;
+    z_o = o;
+    z_q = 144 + v;
+    if (v < 36) {  // ZJ[d][il][jl] = ga_d MX[il][jl]
+      z_src = 14 + q / 18;
+      z_c = P.mx[q % 18];
+    } else if (v < 72) {  // ZA[d][il][jl] = jm(il) G1[o][jl][d]
+      const int d = q / 18, il = (q / 3) % 6, jl = q % 3;
+      z_src = 16 + il;
+      z_c = P.g1[(o * 3 + jl) * 2 + d];
+    } else {  // Y[c][il][jl] = ga_c MX[jl][il]
+      const int c = q / 18, il = (q / 6) % 3, jl = q % 6;
+      z_src = 14 + c;
+      z_c = P.mx[jl * 3 + il];
+    }
+  }
+  // software pipeline over the CTA's slab run, double-buffered state rows S and
+  // element matrices E: iteration k writes the entries of slab k (B) from E[k&1] while
+  // the tensor cores form E[(k+1)&1] (A1) and A0 stages the state rows of slab k+2;
+  // the three are independent, so warps interleave them between two barriers
   const int k0 = blockIdx.y * P.kchunk, k1 = min(P.nt, k0 + P.kchunk);
-  for (int k = k0; k < k1; ++k) {
+  auto stage_A0 = [&](int k) {
+    if (!(P.phases & 1) || k >= k1) return;
     const double *s = P.sc + (int64_t)k * P.slab;
-    if (P.phases & 1) {
-      // A0: state rows
-      for (int sl = threadIdx.x; sl < nsl; sl += blockDim.x) {
-        const int e = P.slots[dsc.z + sl], o = e & 1;
-        double *row = S + sl * kPatchSSZ;
+    double *S = (k & 1) ? S1 : S0;
+    for (int sl = threadIdx.x; sl < nsl; sl += blockDim.x) {
+      const int e = P.slots[dsc.z + sl], o = e & 1;
+      double *row = S + sl * kPatchSSZ;
 #pragma unroll
-        for (int m = 0; m < 6; ++m) {
-          const int g = P.elem_v[e * 6 + m];
-          row[m] = s[g];
-          row[6 + m] = s[P.nnv + g];
-        }
-        row[12] = 1.0;
-        row[13] = 0.0;
-        double av[3], jv[3];
-#pragma unroll
-        for (int n = 0; n < 3; ++n) {
-          const int g = P.elem_1[e * 3 + n];
-          av[n] = s[P.o_a + g];
-          jv[n] = s[P.o_j + g];
-        }
-#pragma unroll
-        for (int d = 0; d < 2; ++d) {
-          double ga = 0.0;
-#pragma unroll
-          for (int n = 0; n < 3; ++n) ga += av[n] * P.g1[(o * 3 + n) * 2 + d];
-          row[14 + d] = ga;
-        }
-#pragma unroll
-        for (int il = 0; il < 6; ++il) {
-          double jm = 0.0;
-#pragma unroll
-          for (int n = 0; n < 3; ++n) jm += jv[n] * P.mx[il * 3 + n];
-          row[16 + il] = jm;
-        }
+      for (int m = 0; m < 6; ++m) {
+        const int g = P.elem_v[e * 6 + m];
+        row[m] = s[g];
+        row[6 + m] = s[P.nnv + g];
       }
-      __syncthreads();
-      // A1: output rows x elements of their orientation
+      row[12] = 1.0;
+      row[13] = 0.0;
+      double av[3], jv[3];
 #pragma unroll
-      for (int r = 0; r < 1; ++r) {
-        const int o = it_o[r];
-        if (o < 0) continue;
-        const int sb = o ? n0 : 0, se = o ? nsl : n0;
-        if (it_q[r] < 144 || it_q[r] >= 252) {
-          for (int sl = sb; sl < se; ++sl) {
-            const double2 *row = reinterpret_cast<const double2 *>(S + sl * kPatchSSZ);
-            double a0 = 0.0, a1 = 0.0;
+      for (int n = 0; n < 3; ++n) {
+        const int g = P.elem_1[e * 3 + n];
+        av[n] = s[P.o_a + g];
+        jv[n] = s[P.o_j + g];
+      }
 #pragma unroll
-            for (int t = 0; t < 6; ++t) {
-              const double2 x = row[t];
-              a0 = fma(wr[2 * t], x.x, a0);
-              a1 = fma(wr[2 * t + 1], x.y, a1);
-            }
-            E[sl * kPatchESZ + it_q[r]] = fma(wr[12], 1.0, a0 + a1);
-          }
-        } else {
-          for (int sl = sb; sl < se; ++sl) E[sl * kPatchESZ + it_q[r]] = S[sl * kPatchSSZ + it_src[r]] * it_c[r];
+      for (int d = 0; d < 2; ++d) {
+        double ga = 0.0;
+#pragma unroll
+        for (int n = 0; n < 3; ++n) ga += av[n] * P.g1[(o * 3 + n) * 2 + d];
+        row[14 + d] = ga;
+      }
+#pragma unroll
+      for (int il = 0; il < 6; ++il) {
+        double jm = 0.0;
+#pragma unroll
+        for (int n = 0; n < 3; ++n) jm += jv[n] * P.mx[il * 3 + n];
+        row[16 + il] = jm;
+      }
+    }
+  };
+  auto stage_A1 = [&](int k) {
+    if (!(P.phases & 1) || k >= k1) return;
+    const double *S = (k & 1) ? S1 : S0;
+    double *E = (k & 1) ? E1 : E0;
+    // A1 (tensor cores): per tile, m-tiles of 8 elements x 4 k-steps
+#pragma unroll
+    for (int i = 0; i < kMaxTW; ++i) {
+      const int t = warp + i * nwarps;
+      if (t >= 2 * kNT) break;
+      const int o = t / kNT, n = (t % kNT) * 8 + (lane & 3) * 2;
+      const int no = o ? n1 : n0, sb = o ? n0 : 0;
+      for (int m0 = 0; m0 < no; m0 += 8) {
+        const int ra = m0 + (lane >> 2);
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const double av = ra < no ? S[(sb + ra) * kPatchSSZ + ks * 4 + (lane & 3)] : 0.0;
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(d0), "+d"(d1)
+                       : "d"(av), "d"(bf[i][ks]));
+        }
+        if (ra < no && n < 162) {
+          const int q = n < 144 ? n : n + 108;
+          *reinterpret_cast<double2 *>(E + (sb + ra) * kPatchESZ + q) = make_double2(d0, d1);
         }
       }
     }
-    __syncthreads();
+    // A1 (scalar): Z_j, Z_A, Y
+    if (z_o >= 0) {
+      const int sb = z_o ? n0 : 0, se = z_o ? nsl : n0;
+      for (int sl = sb; sl < se; ++sl) E[sl * kPatchESZ + z_q] = S[sl * kPatchSSZ + z_src] * z_c;
+    }
+  };
+  auto stage_B = [&](int k) {
+    const double *E = (k & 1) ? E1 : E0;
     // phase B: owned entries; 8 codes per entry in one 16-byte word; 4 entries per
     // thread in flight (table loads are L2 round trips)
     for (int i0 = threadIdx.x; i0 < ((P.phases & 2) ? ntab : 0); i0 += 4 * blockDim.x) {
@@ -489,7 +511,28 @@ __global__ void __launch_bounds__(kPatchThreads, 1) values_patch_kernel(const __
         else P.js[(int64_t)k * P.js_stride + idx] = v;
       }
     }
+  };
+  if (P.pipe) {
+    stage_A0(k0);
     __syncthreads();
+    stage_A1(k0);
+    stage_A0(k0 + 1);
+    __syncthreads();
+    for (int k = k0; k < k1; ++k) {
+      stage_B(k);
+      stage_A1(k + 1);
+      stage_A0(k + 2);
+      __syncthreads();
+    }
+  } else {
+    for (int k = k0; k < k1; ++k) {
+      stage_A0(k);
+      __syncthreads();
+      stage_A1(k);
+      __syncthreads();
+      stage_B(k);
+      __syncthreads();
+    }
   }
 }
 
@@ -525,7 +568,15 @@ static void values_patch(stmhd_disc_s *d, const AsmArgs &a, cudaStream_t s, doub
   }
   P.js_stride = d->I("nnz_js");
   P.fp_stride = d->I("nnz_fp");
-  const size_t smem = (size_t)d->I("pa_max_slots") * (kPatchESZ + kPatchSSZ) * sizeof(double);
+  // double buffers when they fit (small patches), else the sequential phases; r01
+  // measurements at C3: 6x5 sequential 1.65 ms, 4x3 pipelined 2.33 ms
+  const size_t one = (size_t)d->I("pa_max_slots") * (kPatchESZ + kPatchSSZ) * sizeof(double);
+  static const int pipe_env = [] {
+    const char *e = getenv("STMHD_PATCH_PIPE");
+    return e ? atoi(e) : 0;
+  }();
+  P.pipe = (pipe_env && 2 * one <= 225 * 1024) ? 1 : 0;
+  const size_t smem = (P.pipe ? 2 : 1) * one;
   static bool attr = false;
   if (!attr) {
     STMHD_CUDA_CHECK(cudaFuncSetAttribute(values_patch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -534,7 +585,7 @@ static void values_patch(stmhd_disc_s *d, const AsmArgs &a, cudaStream_t s, doub
   }
   require(smem <= 225 * 1024, "patch assembly: element matrices exceed shared memory");
   // slab runs per CTA: W rows loaded once per run, >= ~2 waves of one CTA per SM
-  P.kchunk = std::max(1, std::min(8, (int)((int64_t)P.npatch * a.nt / (2 * num_sms()))));
+  P.kchunk = std::max(1, std::min(16, (int)((int64_t)P.npatch * a.nt / (2 * num_sms()))));
   values_patch_kernel<<<dim3(P.npatch, cdiv(a.nt, P.kchunk)), kPatchThreads, smem, s>>>(P);
   STMHD_LAUNCH_CHECK();
 }
