@@ -290,7 +290,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     const int nT = (int)tpos.size();
     std::vector<std::array<int, 4>> zc(nT, {-1, -1, -1, -1});
     // K (nT^2 per slab) may not outgrow the factor itself (batched per-slab factors)
-    bool ok = nT > 0 && nT <= 4096 && (int64_t)nT * nT * (ncta > 16 ? 8 : 1) <= p.factor_size;
+    bool ok = nT > 0 && nT <= 4096 && (int64_t)nT * nT * (ncta > 48 ? 8 : 1) <= p.factor_size;
     for (int r : roots) {  // subtree roots' updates land on top unknowns
       for (int a = 0; a < p.nb[r] && ok; ++a) {
         const int tgt = bpos[p.idx_off[r] + p.ns[r] + a];

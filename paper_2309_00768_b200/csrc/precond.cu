@@ -438,7 +438,11 @@ void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
   }();
   const bool grid = grid_env == 1 || (grid_env < 0 && 8.0 * (double)fu->dev->plan->factor_size > 24e6 &&
                                       num_sms() >= 64);
-  const int nc_fu = grid ? num_sms() - 32 : 16;
+  static const int fu_ctas_env = [] {
+    const char *e = getenv("STMHD_PC_FU_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  const int nc_fu = grid ? (fu_ctas_env > 0 ? std::min(fu_ctas_env, num_sms() - 32) : num_sms() - 32) : 16;
   // grid-family launches need one warp count for all stages: the velocity stage's
   // choice (the others have slack) is remembered after the first preparation
   const int wf = grid ? pipe_warps : 0;
