@@ -167,6 +167,12 @@ int stmhd_nd_plan_info(int64_t n, const int32_t *rowptr, const int32_t *col, con
 int stmhd_c5_values(void *stream, int64_t nnz, int nt, const double *base, const int32_t *cptr,
                     const int32_t *cinfo, const int32_t *elem, const double *u, int64_t n_nodes,
                     const double *mloc9, const double *grad12, double *values);
+/* configuration-5 advection fields on the device: u[k][node][2] for k < nt from the
+   per-slab modes (host, nt x 8 x {kx, ky, amplitude}, drawn as c5.c5_velocity_fields
+   draws them) at the node coordinates xy (device, n_nodes x 2), rescaled to
+   max |u_k| = 1; the host generator's sums in the same order.  Synchronises. */
+int stmhd_c5_velocity(void *stream, int64_t n_nodes, int nt, const double *xy, const double *modes_host,
+                      double *u);
 /* block-bidiagonal batched SpMV: y_k = F_k x_k + c_coef * C x_{k-1} (F per slab with
    value stride val_stride, C shared, may be NULL).  oracle/c5.py C5.apply;
    the space-time Jacobian's structure (spacetime.py:131-153). */

@@ -51,6 +51,7 @@ _SIGS = {
     "stmhd_lu_info": (c_int, [c_vp, P]),
     "stmhd_lu_sweep": (c_int, [c_vp, P, P, c_i64, P, c_i64, c_int, P, P, P, c_dbl]),
     "stmhd_c5_values": (c_int, [P, c_i64, c_int, P, P, P, P, P, c_i64, P, P, P]),
+    "stmhd_c5_velocity": (c_int, [P, c_i64, c_int, P, P, P]),
     "stmhd_bidiag_spmv": (c_int, [P, c_i64, c_int, P, P, P, c_i64, P, P, P, c_dbl, P, P]),
     "stmhd_nd_plan_info": (c_int, [c_i64, P, P, P, P, c_int, P]),
     "stmhd_spmv_create": (c_int, [c_i64, P, P, P, P, P, C.c_int32, P, C.POINTER(c_vp)]),

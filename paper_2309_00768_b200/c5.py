@@ -14,8 +14,34 @@ from __future__ import annotations
 import numpy as np
 
 
+def c5_modes(nt: int, seed: int = 0) -> np.ndarray:
+    """(nt, 8, 3) per-slab modes {kx, ky, amplitude} in the generator's draw order."""
+    rng = np.random.default_rng(seed)
+    out = np.empty((nt, 8, 3))
+    for k in range(nt):
+        out[k, :, :2] = rng.integers(1, 9, size=(8, 2))
+        out[k, :, 2] = rng.standard_normal(8)
+    return out
+
+
+def c5_velocity_fields_device(coords: np.ndarray, nt: int, seed: int = 0):
+    """The same fields as c5_velocity_fields, evaluated on the device
+    (stmhd_c5_velocity): a (nt, n_nodes, 2) CUDA tensor."""
+    import torch
+
+    from . import _lib
+    from .linalg import DEV
+
+    xy = torch.as_tensor(np.ascontiguousarray(coords, dtype=np.float64), device=DEV)
+    md = np.ascontiguousarray(c5_modes(nt, seed))
+    u = torch.empty((nt, len(coords), 2), dtype=torch.float64, device=DEV)
+    _lib.check(_lib.load().stmhd_c5_velocity(_lib.stream_ptr(), len(coords), nt, _lib.ptr(xy), md.ctypes.data,
+                                             _lib.ptr(u)))
+    return u
+
+
 def c5_velocity_fields(coords: np.ndarray, nt: int, seed: int = 0) -> np.ndarray:
-    """(nt, n_nodes, 2) nodal velocities for the slabs 0..nt-1."""
+    """(nt, n_nodes, 2) nodal velocities for the slabs 0..nt-1 (host reference)."""
     rng = np.random.default_rng(seed)
     x = coords[:, 0] + 1.0
     y = coords[:, 1] + 1.0
@@ -119,9 +145,10 @@ class C5Operator:
                        cptr=tens(cptr), cinfo=tens(cinfo.astype(np.int32)), elem=tens(el.astype(np.int32)),
                        c_rowptr=tens(cmat.indptr.astype(np.int32)), c_col=tens(cmat.indices.astype(np.int32)),
                        c_val=tens(cmat.data, torch.float64))
-        if ufields is None:
-            ufields = c5_velocity_fields(p1.coords, nt, seed)
-        self.u = torch.as_tensor(np.ascontiguousarray(ufields, dtype=np.float64), device=DEV)
+        if ufields is None:  # seeded fields, generated on the device
+            self.u = c5_velocity_fields_device(p1.coords, nt, seed)
+        else:
+            self.u = torch.as_tensor(np.ascontiguousarray(ufields, dtype=np.float64), device=DEV)
         self.values = torch.empty(nt * self.nnz, dtype=torch.float64, device=DEV)
         self._lib = _lib.load()
         self._lu = None

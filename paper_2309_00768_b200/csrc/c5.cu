@@ -48,6 +48,44 @@ __global__ void c5_values_kernel(C5Args a) {
   }
 }
 
+
+// Advection fields of configuration 5: per slab, 8 Fourier modes
+// (kx, ky, amplitude) of the stream function psi = sum a sin(pi kx (x+1)/2) sin(pi ky (y+1)/2),
+// u = (d_y psi, -d_x psi) at the P1 nodes, rescaled to max |u| = 1 -- the same sums,
+// in the same order, as the host generator c5.c5_velocity_fields.
+__global__ void c5_velocity_kernel(const double *xy, int64_t n, const double *modes, double *u,
+                                   unsigned long long *umax) {
+  const int k = blockIdx.y;
+  const double *md = modes + (int64_t)k * 24;
+  const double h = 0.5 * 3.141592653589793;
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = xy[2 * i] + 1.0, y = xy[2 * i + 1] + 1.0;
+    double ux = 0.0, uy = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double kx = md[3 * q], ky = md[3 * q + 1], a = md[3 * q + 2];
+      double sx, cx, sy, cy;
+      sincos(h * kx * x, &sx, &cx);
+      sincos(h * ky * y, &sy, &cy);
+      ux += a * sx * (h * ky) * cy;
+      uy -= a * (h * kx) * cx * sy;
+    }
+    u[((int64_t)k * n + i) * 2] = ux;
+    u[((int64_t)k * n + i) * 2 + 1] = uy;
+    m = fmax(m, sqrt(ux * ux + uy * uy));
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(umax + k, __double_as_longlong(m));  // m >= 0: bit order = value order
+}
+
+__global__ void c5_velocity_scale_kernel(int64_t n, const unsigned long long *umax, double *u) {
+  const int k = blockIdx.y;
+  const double sc = __longlong_as_double(umax[k]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * n; i += (int64_t)gridDim.x * blockDim.x)
+    u[(int64_t)k * 2 * n + i] /= sc;
+}
+
 }  // namespace stmhd
 
 using namespace stmhd;
@@ -74,6 +112,23 @@ int stmhd_c5_values(void *stream, int64_t nnz, int nt, const double *base, const
   c5_values_kernel<<<dim3((unsigned)std::min<int64_t>(cdiv(std::max<int64_t>(nnz, 1), 256), 1024), nt), 256, 0,
                      (cudaStream_t)stream>>>(a);
   STMHD_LAUNCH_CHECK();
+  CAPI_END
+}
+
+int stmhd_c5_velocity(void *stream, int64_t n_nodes, int nt, const double *xy, const double *modes_host,
+                      double *u) {
+  CAPI_BEGIN
+  require(n_nodes >= 1 && nt >= 1 && xy && modes_host && u, "stmhd_c5_velocity: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  DevBuf md((size_t)nt * 24 * sizeof(double)), mx((size_t)nt * sizeof(unsigned long long));
+  STMHD_CUDA_CHECK(cudaMemcpyAsync(md.ptr, modes_host, md.bytes, cudaMemcpyHostToDevice, s));
+  STMHD_CUDA_CHECK(cudaMemsetAsync(mx.ptr, 0, mx.bytes, s));
+  const unsigned gx = (unsigned)std::min<int64_t>(cdiv(n_nodes, 256), 64);
+  c5_velocity_kernel<<<dim3(gx, nt), 256, 0, s>>>(xy, n_nodes, md.as<double>(), u, mx.as<unsigned long long>());
+  STMHD_LAUNCH_CHECK();
+  c5_velocity_scale_kernel<<<dim3(gx, nt), 256, 0, s>>>(n_nodes, mx.as<unsigned long long>(), u);
+  STMHD_LAUNCH_CHECK();
+  STMHD_CUDA_CHECK(cudaStreamSynchronize(s));  // scratch buffers die here
   CAPI_END
 }
 

@@ -50,3 +50,11 @@ def test_c5_matches_oracle_and_round_trips(c5mod):
     s = op.solve(x).cpu().numpy()
     assert relerr(s, ref.solve(x).ravel()) < 1e-10
     assert relerr(op.apply(s).cpu().numpy(), x) < 1e-10  # F (F^{-1} x) = x
+
+
+def test_c5_device_velocity_fields_match_host_generator(c5mod):
+    coords = c5mod.c5_host_tables(24)["p1"].coords
+    host = c5mod.c5_velocity_fields(coords, 5, seed=7)
+    dev = c5mod.c5_velocity_fields_device(coords, 5, seed=7).cpu().numpy()
+    assert np.max(np.abs(dev - host)) < 1e-13
+    assert np.allclose(np.sqrt((dev ** 2).sum(-1)).max(axis=1), 1.0, atol=1e-14)
