@@ -626,6 +626,7 @@ struct SweepArgs {
   int slot;     // doubles per TMA slot (largest chunk block)
   int null_work;  // diagnostics: skip all task work (barrier/loop floor)
   unsigned *gbar;  // grid mode (one CTA per SM, cooperative launch): software grid barrier word
+  int kpref;       // L2 prefetch of the slab's dense-top rows at the slab start
   unsigned long long *trace;
   unsigned long long *prof;  // PROF instantiation: 6 counters per warp
   unsigned long long *tline; // PROF instantiation: per-warp event timeline of slab 1, CTA 0 (128 per warp)
@@ -1226,6 +1227,16 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   for (int k = 0; k < a.nslab; ++k) {
     const double *rhs = a.rhsp + (int64_t)k * n;
     double *x = a.xp + (int64_t)k * n;
+    if (a.dense && a.kpref && lane == 0 && !a.null_work) {
+      // the dense-top K rows of this warp for slab k, into L2 one slab phase ahead of
+      // their use (the ring then streams them from L2)
+      for (int ti = w.bnd[a.nsub]; ti < w.bnd[a.nsub + 1]; ++ti) {
+        const SweepTask &t = w.tl[ti];
+        const double *src = a.ktop + (int64_t)k * a.kstride + t.foff;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"((unsigned)(t.c1 * t.bsz * 8))
+                     : "memory");
+      }
+    }
     if (a.prog_hdr && !a.null_work) {
       // fused coupling (CTA-local): rhs_k + sum_c coef_c C_c src_c for this CTA's items.
       // Sources by id: 0 x_{k-1}, 1 x_{k-1} of the own subtree (shared memory),
@@ -1858,6 +1869,7 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   a.slot = slot;
   a.vstride = vstride;
   a.null_work = env_int2("STMHD_SWEEP_NULL", 0);
+  a.kpref = env_int2("STMHD_SWEEP_KPREF", 0);  // measured: no gain (dense step not HBM-latency bound)
   a.post_hdr = nullptr;  // set by sweep_stage_set_post for this launch
   a.gbar = nullptr;
   if (grid) {  // grid-family launch: software barrier
