@@ -632,21 +632,22 @@ struct SweepArgs {
   unsigned long long *tline; // PROF instantiation: per-warp event timeline of slab 1, CTA 0 (128 per warp)
 };
 
-__device__ __forceinline__ void sweep_barrier(const SweepArgs &a, int crank) {
+__device__ __forceinline__ void sweep_barrier(const SweepArgs &a, int crank, unsigned &gphase) {
   if (a.gbar) {
     // software barrier over the stage's a.ncta CTAs (cooperative-groups arrival
     // scheme: every CTA adds 1, rank 0 adds 2^31 - (n - 1), so the top bit flips once
-    // all arrived)
+    // all arrived).  The arrival is a fire-and-forget release reduction; each CTA
+    // tracks the expected top bit itself (gphase, read once per launch), so only the
+    // polling loads are round trips.
     __syncthreads();
     if (threadIdx.x == 0) {
       const unsigned nb = crank == 0 ? 0x80000000u - (unsigned)(a.ncta - 1) : 1u;
-      __threadfence();
-      const unsigned old = atomicAdd(a.gbar, nb);
+      asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.gbar), "r"(nb) : "memory");
+      gphase ^= 0x80000000u;
       unsigned cur;
       do {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(a.gbar) : "memory");
-      } while (((old ^ cur) & 0x80000000u) == 0);
-      __threadfence();
+      } while ((cur & 0x80000000u) != gphase);
     }
     __syncthreads();
     return;
@@ -1158,6 +1159,11 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   }
   __syncthreads();
   const SweepArgs &a = sa;
+  unsigned gphase = 0;  // grid barrier: top bit of the barrier word after the last completion
+  if (a.gbar && threadIdx.x == 0) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gphase) : "l"(a.gbar) : "memory");
+    gphase &= 0x80000000u;
+  }
   WarpCtx w;
   w.lane = threadIdx.x & 31;
   w.wl = threadIdx.x >> 5;
@@ -1283,7 +1289,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
     }
     if (a.nsub || a.prog_hdr) {  // subtree roots' updates and coupled top rows visible
-      tb = pclock<PROF>(); sweep_barrier(a, crank); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+      tb = pclock<PROF>(); sweep_barrier(a, crank, gphase); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step, crank);
     }
     if (a.dense) {
@@ -1309,7 +1315,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       for (int ti = w.bnd[L]; ti < t1; ++ti) dense_task<PROF>(a, w.tl[ti], sv.zs, x, k, w, mbar);
       if (PROF) tl_mark(w, 4);
       ++L;
-      tb = pclock<PROF>(); sweep_barrier(a, crank); if (PROF) w.acc[3] += pclock<PROF>() - tb;  // x_T visible
+      tb = pclock<PROF>(); sweep_barrier(a, crank, gphase); if (PROF) w.acc[3] += pclock<PROF>() - tb;  // x_T visible
       if (a.tab_ints) {  // stage x_T in shared memory for the subtree backward tables
         for (int i = threadIdx.x; i < a.ntT; i += blockDim.x) sv.zs[i] = x[a.ztab[2 * i].x];
         __syncthreads();
@@ -1319,7 +1325,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       for (int t = 0; t < a.ntop; ++t, ++L) {
         const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
         for (int ti = w.bnd[L]; ti < t1; ++ti) forward_task<false, PROF>(a, w.tl[ti], F, rhs, sv, w, mbar);
-        tb = pclock<PROF>(); sweep_barrier(a, crank); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+        tb = pclock<PROF>(); sweep_barrier(a, crank, gphase); if (PROF) w.acc[3] += pclock<PROF>() - tb;
         sweep_trace(a, step, crank);
       }
       for (int t = a.ntop - 1; t >= 0; --t, ++L) {
@@ -1327,7 +1333,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
         for (int ti = w.bnd[L]; ti < t1; ++ti) backward_task<false, PROF>(a, w.tl[ti], F, x, sv, w, mbar);
         if (t > 0 || a.nsub || k + 1 < a.nslab) {
           tb = pclock<PROF>();
-          sweep_barrier(a, crank);
+          sweep_barrier(a, crank, gphase);
           if (PROF) w.acc[3] += pclock<PROF>() - tb;
         }
         sweep_trace(a, step, crank);
@@ -1343,7 +1349,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     if (a.post_hdr && !a.null_work) {
       // post-slab program: rows of another stage's right-hand side from this stage's
       // x_k (all CTAs' parts: cluster barrier) and external sources at slab k
-      sweep_barrier(a, crank);
+      sweep_barrier(a, crank, gphase);
       if (threadIdx.x == 0) {
         s_src[3] = a.ext_xp[0] ? a.ext_xp[0] + (int64_t)k * a.ext_n[0] : a.zero;
         s_src[4] = a.ext_xp[1] ? a.ext_xp[1] + (int64_t)k * a.ext_n[1] : a.zero;
@@ -1360,7 +1366,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       if (threadIdx.x == 0) st_release_gpu(a.flag_out + (int64_t)k * a.ncta + crank, a.epoch);
     }
     if (a.nsub && k + 1 < a.nslab) {  // x_k visible to every CTA's next coupling
-      tb = pclock<PROF>(); sweep_barrier(a, crank); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+      tb = pclock<PROF>(); sweep_barrier(a, crank, gphase); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step, crank);
     }
   }
