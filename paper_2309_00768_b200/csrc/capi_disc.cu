@@ -127,6 +127,7 @@ int stmhd_disc_finalize(stmhd_disc d, void *stream) {
     *c.f = std::make_unique<NDFactor>();
     (*c.f)->dev = c.dv;
     (*c.f)->nbatch = 1;
+    (*c.f)->dense_ok = true;  // constant, well-conditioned (mass / pinned Laplacian): dense inverse allowed
     (*c.f)->factor(d->D<double>(c.key), 0, s);
     if ((*c.f)->check_status(s)) throw Error(STMHD_SINGULAR, std::string("constant factor ") + c.block + " is singular");
   }

@@ -181,12 +181,20 @@ struct NDFactor {
   // lazily for the sweep plan that uses it: [nbatch][n_T][kpad] doubles
   mutable DevBuf ktop;
   mutable DevBuf scratch, bar;  // batched-solve scratch and grid-barrier words (per factor)
+  // small shared factors (nbatch == 1, n <= 2048): dense A^{-1} (column-major), built
+  // once per factorisation by solving A X = I; batched solves are then one FP64
+  // tensor-core GEMM (dense_solve_gemm, nd_numeric.cu)
+  mutable DevBuf dinv, gemm_ws;
+  mutable uint64_t dinv_gen = ~0ull;
+  bool dense_ok = false;  // set for the discretisation's constant factors only
   mutable const void *ktop_plan = nullptr;
   mutable uint64_t ktop_gen = ~0ull;
   void factor(const double *values, int64_t value_stride, cudaStream_t s);
   // x_b = A_b^{-1} rhs_b (b < nrhs; factor b, or 0 if nbatch == 1).
   void solve(const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,
              cudaStream_t s) const;
+  void solve_nd(const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,
+                cudaStream_t s) const;  // the supernodal substitution path
   // Sequential sweep over slabs k = 0..nrhs-1:
   //   x_k = A_k^{-1}( rhs_k + sum_t coef_t C_t x_(k-lag_t) )
   void sweep(const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,

@@ -614,8 +614,104 @@ __global__ void __launch_bounds__(512, 1) nd_solve_cta_kernel(SolveArgs a) {
 }
 
 
+// C = A B for A (n x n, column-major), B (n x nrhs, ld ldb), split over K in S parts:
+// part s writes ws[s][c][m]; FP64 tensor cores (mma.sync m8n8k4).  CTA tile 32 x 32,
+// 8 warps of one 8-row m-subtile x two 8-column c-subtiles, 8 k-steps of loads in
+// flight per iteration.
+__global__ void __launch_bounds__(256) dense_gemm_kernel(const double *__restrict__ A, int n,
+                                                         const double *__restrict__ B, int64_t ldb, int nrhs,
+                                                         int kchunk, double *__restrict__ ws) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * 32 + (warp >> 1) * 8;
+  const int c0 = blockIdx.y * 32 + (warp & 1) * 16;
+  const int kb = blockIdx.z * kchunk, ke = min(n, kb + kchunk);
+  const int am = m0 + (lane >> 2), kq = lane & 3;
+  const int bc0 = c0 + (lane >> 2), bc1 = c0 + 8 + (lane >> 2);
+  double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int k0 = kb; k0 < ke; k0 += 32) {
+    double a[8], b0[8], b1[8];
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int kk = k0 + ks * 4 + kq;
+      const bool ok = kk < ke;
+      a[ks] = (ok && am < n) ? A[(int64_t)kk * n + am] : 0.0;
+      b0[ks] = (ok && bc0 < nrhs) ? B[(int64_t)bc0 * ldb + kk] : 0.0;
+      b1[ks] = (ok && bc1 < nrhs) ? B[(int64_t)bc1 * ldb + kk] : 0.0;
+    }
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(d[0][0]), "+d"(d[0][1])
+                   : "d"(a[ks]), "d"(b0[ks]));
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(d[1][0]), "+d"(d[1][1])
+                   : "d"(a[ks]), "d"(b1[ks]));
+    }
+  }
+  // D fragment: row m0 + lane/4, columns c + 2*(lane%4) + {0, 1}
+  const int row = m0 + (lane >> 2);
+  double *w = ws + (int64_t)blockIdx.z * nrhs * n;
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int col = c0 + 8 * j + 2 * kq + i;
+      if (row < n && col < nrhs) w[(int64_t)col * n + row] = d[j][i];
+    }
+}
+
+__global__ void dense_gemm_reduce(const double *ws, int n, int nrhs, int nsplit, double *x, int64_t ldx) {
+  const int64_t tot = (int64_t)n * nrhs;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int sp = 0; sp < nsplit; ++sp) v += ws[sp * tot + t];  // fixed order: deterministic
+    x[(t / n) * ldx + t % n] = v;
+  }
+}
+
+__global__ void identity_kernel(double *m, int n) {
+  const int64_t tot = (int64_t)n * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x)
+    m[t] = (t / n == t % n) ? 1.0 : 0.0;
+}
+
 void NDFactor::solve(const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,
                      cudaStream_t s) const {
+  const NDPlan &p = *dev->plan;
+  static const int dense_env = [] {
+    const char *e = getenv("STMHD_DENSE_INV");
+    return e ? atoi(e) : 1;
+  }();
+  if (!(dense_env && dense_ok && nbatch == 1 && p.n <= 2048 && nrhs >= 8)) {
+    solve_nd(rhs, ld_rhs, x, ld_x, nrhs, s);
+    return;
+  }
+  const int n = (int)p.n;
+  if (dinv_gen != gen) {  // A^{-1} = solve(A, I), once per factorisation
+    DevBuf eye((size_t)n * n * sizeof(double));
+    identity_kernel<<<std::min<int64_t>(cdiv((int64_t)n * n, 256), 4096), 256, 0, s>>>(eye.as<double>(), n);
+    STMHD_LAUNCH_CHECK();
+    if (dinv.bytes < eye.bytes) dinv.alloc_async(eye.bytes, s);
+    solve_nd(eye.as<double>(), n, dinv.as<double>(), n, n, s);
+    STMHD_CUDA_CHECK(cudaStreamSynchronize(s));  // eye dies here
+    dinv_gen = gen;
+  }
+  const int mt = (n + 31) / 32, ct = (nrhs + 31) / 32;
+  int nsplit = std::max(1, std::min((2 * num_sms() + mt * ct - 1) / (mt * ct), (n + 127) / 128));
+  const int kchunk = ((n + nsplit - 1) / nsplit + 31) / 32 * 32;
+  nsplit = (n + kchunk - 1) / kchunk;
+  const size_t wsb = (size_t)nsplit * n * nrhs * sizeof(double);
+  if (gemm_ws.bytes < wsb) gemm_ws.alloc_async(wsb, s);
+  dense_gemm_kernel<<<dim3(mt, ct, nsplit), 256, 0, s>>>(dinv.as<double>(), n, rhs, ld_rhs, nrhs, kchunk,
+                                                          gemm_ws.as<double>());
+  STMHD_LAUNCH_CHECK();
+  dense_gemm_reduce<<<std::min<int64_t>(cdiv((int64_t)n * nrhs, 256), 2048), 256, 0, s>>>(gemm_ws.as<double>(), n, nrhs,
+                                                                                        nsplit, x, ld_x);
+  STMHD_LAUNCH_CHECK();
+}
+
+void NDFactor::solve_nd(const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,
+                        cudaStream_t s) const {
   const NDPlan &p = *dev->plan;
   require(nbatch == 1 || nrhs <= nbatch, "lu solve: more right-hand sides than factors");
   if (!bar.ptr) {

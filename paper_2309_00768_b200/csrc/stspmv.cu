@@ -16,6 +16,10 @@
 #include "capi_common.hpp"
 #include "stspmv.hpp"
 
+#ifndef STMHD_SELL_MINB
+#define STMHD_SELL_MINB 4  // CTAs per SM the register budget is sized for
+#endif
+
 namespace stmhd {
 
 struct SellArgs {
@@ -36,7 +40,7 @@ struct SellArgs {
 // S slabs per thread share every column (and coupling) load: per batch of 4 entries
 // a thread has 4 column loads and 4*S value loads + 4*S x gathers in flight.
 template <int S, int B>
-__global__ void __launch_bounds__(256) sell_spmv_kernel(SellArgs a) {
+__global__ void __launch_bounds__(256, STMHD_SELL_MINB) sell_spmv_kernel(SellArgs a) {
   const int sidx = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (sidx >= a.nslices) return;
   const int k0 = blockIdx.y * S;
