@@ -107,6 +107,11 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     return e ? atoi(e) : 1;
   }();
   int D = (sub_env && !flat) ? 1 : 0;  // 1: subtree phase in use
+  // subtrees per sweep: one per CTA in cluster mode; in grid mode (ncta > 16) fewer
+  // subtrees than CTAs keep the top small enough for the dense K (all CTAs stream K
+  // and the coupling; CTAs without a subtree idle through the subtree phases)
+  static const int maxsub_env = env_int2("STMHD_SWEEP_GRID_SUBTREES", 0);
+  const int max_sub = (ncta > 16 && maxsub_env > 0) ? std::min(maxsub_env, ncta) : ncta;
   std::vector<int> frontier;
   if (D) {
     for (int sn = 0; sn < p.nsn; ++sn)
@@ -116,7 +121,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
       for (int i = 0; i < (int)frontier.size(); ++i) {
         const int sn = frontier[i];
         const int nc = p.child_ptr[sn + 1] - p.child_ptr[sn];
-        if (nc == 0 || (int)frontier.size() - 1 + nc > ncta) continue;
+        if (nc == 0 || (int)frontier.size() - 1 + nc > max_sub) continue;
         if (best < 0 || swork[sn] > swork[frontier[best]]) best = i;
       }
       if (best < 0) break;
@@ -290,7 +295,8 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     const int nT = (int)tpos.size();
     std::vector<std::array<int, 4>> zc(nT, {-1, -1, -1, -1});
     // K (nT^2 per slab) may not outgrow the factor itself (batched per-slab factors)
-    bool ok = nT > 0 && nT <= 4096 && (int64_t)nT * nT * (ncta > 48 ? 8 : 1) <= p.factor_size;
+    bool ok = nT > 0 && nT <= 4096 &&
+              (int64_t)nT * nT * (ncta <= 48 ? 1 : (max_sub < ncta ? 2 : 8)) <= p.factor_size;
     for (int r : roots) {  // subtree roots' updates land on top unknowns
       for (int a = 0; a < p.nb[r] && ok; ++a) {
         const int tgt = bpos[p.idx_off[r] + p.ns[r] + a];
