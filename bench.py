@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c3-kernels", action="store_true", help="skip the C3 J.v / assembly roofline entries")
     return ap.parse_args()
 
 
@@ -336,8 +337,31 @@ def run_ours(args, rank, world):
         "assembly (residual_patch + values_patch)": {"algorithmic_bytes": asm_bytes, "ms": asm_ms,
                                                      "GBps": asm_bytes / asm_ms / 1e6,
                                                      "frac": asm_bytes / asm_ms / 1e6 / peak},
-        "note": "C2 operators are partly L2-resident (168 MB); tools/bench_spmv.py and tools/asm_probe.py "
-                "give the C3/C5 figures"}
+        "note": "C2 operators are partly L2-resident (168 MB); the C3 entries are measured in this run after "
+                "the timed region; tools/bench_spmv.py and tools/asm_probe.py give the C5 figures"}
+
+    # the same kernels at C3 (tearing 64^2, Nt=128: 1.37 GB per J.v, beyond L2)
+    if rank == 0 and not args.no_c3_kernels:
+        try:
+            d3 = p.discretize_config("C3")
+            s3 = p.initial_state(d3)
+            j3 = p.assemble_jacobian(s3, d3)
+            v3 = torch.randn(j3.size, dtype=torch.float64, device=dev)
+            o3 = torch.empty_like(v3)
+            L3, P3, nt3 = d3.layout, d3.pattern, d3.n_steps
+            jv3 = tmeas(lambda: j3._into(v3, o3), 30)
+            as3 = tmeas(lambda: p.assemble_jacobian(s3, d3), 5) + tmeas(lambda: p.residual(s3, d3), 5)
+            jb3 = nt3 * (8 * P3.nnz + 16 * L3.slab_size) + 12 * d3.jc_nnz + 8 * L3.n_p + 4 * P3.nnz
+            ab3 = nt3 * 8 * (2 * L3.slab_size + P3.nnz + P3.fp_nnz)
+            kernel_rooflines["C3"] = {
+                "J_apply (sell_spmv_kernel)": {"algorithmic_bytes": jb3, "ms": jv3, "GBps": jb3 / jv3 / 1e6,
+                                               "frac": jb3 / jv3 / 1e6 / peak},
+                "assembly (residual_patch + values_patch)": {"algorithmic_bytes": ab3, "ms": as3,
+                                                             "GBps": ab3 / as3 / 1e6, "frac": ab3 / as3 / 1e6 / peak}}
+            del d3, s3, j3, v3, o3
+            torch.cuda.empty_cache()
+        except Exception as exc:  # keep the line
+            kernel_rooflines["C3"] = {"error": str(exc)[:200]}
 
     line = {
         "metric": "FGMRES iterations/s (C2 Newton solve, P_T preconditioner, FP64)",

@@ -16,9 +16,6 @@
 #include "capi_common.hpp"
 #include "stspmv.hpp"
 
-#ifndef STMHD_SELL_MINB
-#define STMHD_SELL_MINB 4  // CTAs per SM the register budget is sized for
-#endif
 
 namespace stmhd {
 
@@ -39,9 +36,9 @@ struct SellArgs {
 
 // S slabs per thread share every column (and coupling) load: per batch of 4 entries
 // a thread has 4 column loads and 4*S value loads + 4*S x gathers in flight.
-template <int S, int B>
-__global__ void __launch_bounds__(256, STMHD_SELL_MINB) sell_spmv_kernel(SellArgs a) {
-  const int sidx = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+template <int S, int B, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) sell_spmv_kernel(SellArgs a) {
+  const int sidx = blockIdx.x * WARPS + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (sidx >= a.nslices) return;
   const int k0 = blockIdx.y * S;
   const int ns = min(S, a.nt - k0);
@@ -218,16 +215,31 @@ void StSpmvPlan::apply(int nt, const double *sell, double alpha_a, double alpha_
     const char *e = getenv("STMHD_SELL_SB");
     return e ? atoi(e) : 0;
   }();
-  // measured (r01): J.v (rows ~45 entries) 2 slabs x 4, C5 (rows ~14) 4 slabs x 4
-  const int S = sb ? sb / 10 : (nnz_a >= (int64_t)16 * nrows ? 2 : 4), B = sb ? sb % 10 : 4;
-  const dim3 blk(256);
-  auto grid = [&](int s_) { return dim3(cdiv(nslices, 8), cdiv(nt, s_)); };
-  if (S == 1 && B == 8) sell_spmv_kernel<1, 8><<<grid(1), blk, 0, s>>>(a);
-  else if (S == 1) sell_spmv_kernel<1, 4><<<grid(1), blk, 0, s>>>(a);
-  else if (S == 2 && B == 8) sell_spmv_kernel<2, 8><<<grid(2), blk, 0, s>>>(a);
-  else if (S == 2) sell_spmv_kernel<2, 4><<<grid(2), blk, 0, s>>>(a);
-  else if (S == 4 && B == 2) sell_spmv_kernel<4, 2><<<grid(4), blk, 0, s>>>(a);
-  else sell_spmv_kernel<4, 4><<<grid(4), blk, 0, s>>>(a);
+  // measured (r01, 128-thread CTAs): 2 slabs x 4 entries per thread is best for both
+  // J.v (rows ~45 entries; C3 62 % of HBM) and C5 (rows ~14; 62 %)
+  const int S = sb ? sb / 10 : 2, B = sb ? sb % 10 : 4;
+  static const int wenv = [] {
+    const char *e = getenv("STMHD_SELL_WARPS");
+    return e ? atoi(e) : 4;  // r01 sweep: 128-thread CTAs (finer tail, more CTAs/SM) 0.40 -> 0.34 ms at C3
+  }();
+  auto launch = [&](auto kern, int s_, int w_) {
+    kern<<<dim3(cdiv(nslices, w_), cdiv(nt, s_)), w_ * 32, 0, s>>>(a);
+  };
+  if (wenv == 4) {
+    if (S == 1 && B == 8) launch(sell_spmv_kernel<1, 8, 4>, 1, 4);
+    else if (S == 1 && B == 2) launch(sell_spmv_kernel<1, 2, 4>, 1, 4);
+    else if (S == 1) launch(sell_spmv_kernel<1, 4, 4>, 1, 4);
+    else if (S == 2 && B == 2) launch(sell_spmv_kernel<2, 2, 4>, 2, 4);
+    else if (S == 2) launch(sell_spmv_kernel<2, 4, 4>, 2, 4);
+    else launch(sell_spmv_kernel<4, 4, 4>, 4, 4);
+  } else {
+    if (S == 1 && B == 8) launch(sell_spmv_kernel<1, 8, 8>, 1, 8);
+    else if (S == 1 && B == 2) launch(sell_spmv_kernel<1, 2, 8>, 1, 8);
+    else if (S == 1) launch(sell_spmv_kernel<1, 4, 8>, 1, 8);
+    else if (S == 2 && B == 2) launch(sell_spmv_kernel<2, 2, 8>, 2, 8);
+    else if (S == 2) launch(sell_spmv_kernel<2, 4, 8>, 2, 8);
+    else launch(sell_spmv_kernel<4, 4, 8>, 4, 8);
+  }
   STMHD_LAUNCH_CHECK();
 }
 
