@@ -206,7 +206,7 @@ def element_linear_maps(T, dt, mu, eta, mu0):
 RSZ = 21
 
 
-def build_residual_plan(disc, px: int = 8, py: int = 8):
+def build_residual_plan(disc, px: int = 16, py: int = 8):
     if disc.vel.nloc != 6 or disc.prs.nloc != 3:
         return None
     mesh, L = disc.mesh, disc.layout

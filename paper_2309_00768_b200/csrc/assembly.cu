@@ -832,7 +832,13 @@ static void residual_patch(stmhd_disc_s *d, const AsmArgs &a, cudaStream_t s) {
   P.codes = d->D<uint4>("pr_codes");
   P.res = a.res;
   const size_t smem = (size_t)d->I("pr_max_slots") * kResSZ * sizeof(double);
-  require(smem <= 48 * 1024, "patch residual: element vectors exceed shared memory");
+  static bool attr = false;
+  if (!attr) {
+    STMHD_CUDA_CHECK(cudaFuncSetAttribute(residual_patch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          110 * 1024));
+    attr = true;
+  }
+  require(smem <= 110 * 1024, "patch residual: element vectors exceed shared memory");
   residual_patch_kernel<<<dim3((unsigned)d->I("pr_npatch"), a.nt), 256, smem, s>>>(P);
   STMHD_LAUNCH_CHECK();
 }

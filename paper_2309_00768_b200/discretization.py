@@ -193,7 +193,8 @@ class Discretization:
             up("pa_codes", pp["codes"]), up("pa_w", pp["w"])
             for k, v in (("pa_npatch", pp["npatch"]), ("pa_max_slots", pp["max_slots"])):
                 _lib.check(lib.stmhd_disc_set_int(h, k.encode(), int(v)))
-        rp_ = build_residual_plan(self)
+        rs = os.environ.get("STMHD_RPATCH", "16x8").split("x")  # residual patch cells (r01 sweep: 16x8 best)
+        rp_ = build_residual_plan(self, int(rs[0]), int(rs[1]))
         if rp_ is not None:
             up("pr_desc", rp_["desc"]), up("pr_slots", rp_["slots"]), up("pr_out", rp_["out"])
             up("pr_codes", rp_["codes"]), up("pr_add", rp_["add"])
