@@ -351,7 +351,7 @@ struct PatchArgs {
   int64_t js_stride, fp_stride;
 };
 
-constexpr int kPatchESZ = 270, kPatchRound = 256, kPatchMaxC = 6, kPatchThreads = 576;
+constexpr int kPatchESZ = 270, kPatchRound = 256, kPatchMaxC = 6, kPatchThreads = 640;
 constexpr int kPatchSSZ = 24;  // state row: u (12), 1, pad, grad A (2), j moments (6), pad (2)
 constexpr int kPatchItems = 2 * 162 + 2 * 108;
 
