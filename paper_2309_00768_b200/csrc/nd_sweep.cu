@@ -1771,6 +1771,8 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   };
   // prefer the most warps whose plan keeps the CTA-local subtree phase (fewer
   // cluster/grid barriers per slab), else the most warps whose flat plan fits
+  static const int warps_env = env_int2("STMHD_SWEEP_WARPS", 0);  // experiments: warps per CTA
+  if (warps_force <= 0 && warps_env > 0) warps_force = warps_env;
   if (warps_force > 0) st.warps = warps_force;
   int warps = st.warps;
   if (!warps) {
