@@ -633,6 +633,7 @@ struct SweepArgs {
   int null_work;  // diagnostics: skip all task work (barrier/loop floor)
   unsigned *gbar;  // grid mode (one CTA per SM, cooperative launch): software grid barrier word
   int kpref;       // L2 prefetch of the slab's dense-top rows at the slab start
+  unsigned long long *progress;  // L2 prefetch cluster: (epoch << 32) | slab in progress (CTA 0)
   unsigned long long *trace;
   unsigned long long *prof;  // PROF instantiation: 6 counters per warp
   unsigned long long *tline; // PROF instantiation: per-warp event timeline of slab 1, CTA 0 (128 per warp)
@@ -1137,7 +1138,68 @@ __device__ __forceinline__ void run_program(const int4 hd, const int2 *items, co
 struct SweepMulti {
   SweepArgs st[3];
   int first[4];  // grid-family launch: stage i owns CTAs [first[i], first[i+1])
+  int nst;       // stages; cluster index nst (if launched) is the L2 prefetch cluster
+  int pf_dist;   // prefetch slabs [k + 1, k + pf_dist] while a stage works on slab k
 };
+
+// L2 prefetch cluster (cluster launch only): the sweeps stream every slab's factor
+// and dense-top rows once, through per-warp TMA rings whose depth shared memory
+// caps, so each level waits on an HBM round trip.  Idle SMs pull the next slabs'
+// data into L2 (126 MB) while the stages work, so the rings hit L2 instead
+// (~250 vs ~600+ cycles).  Pure hint: no effect on results.
+__device__ __forceinline__ void l2_prefetch_range(const void *base, int64_t bytes, int part, int nparts, int lane) {
+  uintptr_t b0 = reinterpret_cast<uintptr_t>(base), b1 = b0 + (uintptr_t)bytes;
+  b0 = (b0 + 15) & ~(uintptr_t)15;
+  b1 &= ~(uintptr_t)15;
+  if (b1 <= b0) return;
+  const uintptr_t len = b1 - b0, per = ((len + nparts - 1) / nparts + 15) & ~(uintptr_t)15;
+  const uintptr_t p0 = b0 + (uintptr_t)part * per, p1 = min(b1, p0 + per);
+  constexpr uintptr_t kChunk = 32768;
+  for (uintptr_t c = p0 + (uintptr_t)lane * kChunk; c < p1; c += 32 * kChunk) {
+    const unsigned sz = (unsigned)min(kChunk, p1 - c);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(c), "r"(sz) : "memory");
+  }
+}
+
+__device__ void l2_prefetch_cluster(const SweepMulti &m, int crank) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  int next[3] = {0, 0, 0};
+  unsigned long long last_change;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(last_change));
+  long long seen[3] = {-2, -2, -2};
+  for (;;) {
+    bool all = true, moved = false;
+    for (int s = 0; s < m.nst; ++s) {
+      const SweepArgs &a = m.st[s];
+      if (next[s] >= a.nslab) continue;
+      all = false;
+      unsigned long long v;
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.progress) : "memory");
+      const long long cur = (int)(v >> 32) == a.epoch ? (long long)(v & 0xffffffffu) : -1;
+      if (cur != seen[s]) {
+        seen[s] = cur;
+        moved = true;
+      }
+      const long long lim = min((long long)a.nslab - 1, max(cur, 0LL) + m.pf_dist);
+      for (; next[s] <= lim; ++next[s]) {
+        const int j = next[s];
+        l2_prefetch_range(a.factors + (int64_t)j * a.fstride, a.fstride * 8, crank, 16, lane);
+        if (a.dense && a.kstride) l2_prefetch_range(a.ktop + (int64_t)j * a.kstride, a.kstride * 8, crank, 16, lane);
+        if (a.prog_hdr && a.prog_per_slab)
+          l2_prefetch_range(a.prog_vals + (int64_t)j * a.prog_nent, a.prog_nent * 8, crank, 16, lane);
+        if (a.post_hdr && a.post_per_slab)
+          l2_prefetch_range(a.post_vals + (int64_t)j * a.post_nent, a.post_nent * 8, crank, 16, lane);
+      }
+    }
+    if (all) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (moved) last_change = t;
+    else if (t - last_change > 4000000000ull) return;  // stages not progressing: stop hinting
+    __nanosleep(256);
+  }
+}
 
 template <bool PROF>
 __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant__ SweepMulti m) {
@@ -1150,6 +1212,10 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   const bool grid = m.st[0].gbar != nullptr;
   unsigned cid;
   int crank;
+  if (!grid && (int)cluster_index() >= m.nst) {
+    l2_prefetch_cluster(m, (int)cluster_rank());
+    return;
+  }
   if (grid) {
     const int b = (int)blockIdx.x;
     cid = b >= m.first[2] ? 2u : (b >= m.first[1] ? 1u : 0u);
@@ -1239,6 +1305,10 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   for (int k = 0; k < a.nslab; ++k) {
     const double *rhs = a.rhsp + (int64_t)k * n;
     double *x = a.xp + (int64_t)k * n;
+    if (a.progress && threadIdx.x == 0 && crank == 0) {
+      const unsigned long long v = ((unsigned long long)(unsigned)a.epoch << 32) | (unsigned)k;
+      asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a.progress), "l"(v) : "memory");
+    }
     if (a.dense && a.kpref && lane == 0 && !a.null_work) {
       // the dense-top K rows of this warp for slab k, into L2 one slab phase ahead of
       // their use (the ring then streams them from L2)
@@ -1719,6 +1789,7 @@ struct SweepStage {
   int warps = 0;  // warps per CTA (0: not chosen yet)
   int ncta = 0;   // CTAs of the sweep: kCluster (one cluster) or one per SM (grid mode)
   DevBuf gbar;    // grid-mode barrier word
+  DevBuf progress;  // slab in progress (L2 prefetch cluster)
   const std::vector<int> *ext_pos[2] = {nullptr, nullptr};
   const CplProgram *vals_prog = nullptr, *post_prog = nullptr;
 };
@@ -2044,6 +2115,11 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
     } else {
       st.a.flag_out = nullptr;
     }
+    if (!st.progress.ptr) {
+      st.progress.alloc_async(sizeof(unsigned long long), s);
+      STMHD_CUDA_CHECK(cudaMemsetAsync(st.progress.ptr, 0, sizeof(unsigned long long), s));
+    }
+    st.a.progress = st.progress.as<unsigned long long>();
     smem = std::max(smem, st.smem);
     require(st.warps == stg[0]->warps, "sweep: stages of one launch need the same warps per CTA");
   }
@@ -2101,8 +2177,38 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
     STMHD_CUDA_CHECK(cudaMemsetAsync(tlb.ptr, 0, tlb.bytes, s));
     m.st[ts].tline = tlb.as<unsigned long long>();
   }
+  // L2 prefetch cluster (cluster mode): one extra 16-CTA cluster when the device
+  // can hold it next to the stages (STMHD_SWEEP_L2PF = prefetch distance in slabs, 0 off)
+  static const int pf_env = env_int2("STMHD_SWEEP_L2PF", 1);
+  int pf = 0;
+  if (!grid && pf_env > 0) {
+    static int max_clusters = -1;
+    if (max_clusters < 0) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(kCluster * 4);
+      q.blockDim = dim3(warps * 32);
+      q.dynamicSmemBytes = smem;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = kCluster;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      int mc = 0;
+      if (cudaOccupancyMaxActiveClusters(&mc, (const void *)nd_sweep_kernel<false>, &q) != cudaSuccess) {
+        cudaGetLastError();
+        mc = 0;
+      }
+      max_clusters = mc;
+      if (env_int2("STMHD_SWEEP_L2PF_DEBUG", 0)) fprintf(stderr, "[sweep] max active 16-CTA clusters %d\n", mc);
+    }
+    pf = max_clusters >= nst + 1 ? 1 : 0;
+  }
+  m.nst = nst;
+  m.pf_dist = pf_env;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid ? first[nst] : kCluster * nst);
+  cfg.gridDim = dim3(grid ? first[nst] : kCluster * (nst + pf));
   for (int i = 0; i < 4; ++i) m.first[i] = i <= nst ? first[i] : first[nst];
   cfg.blockDim = dim3(warps * 32);
   cfg.dynamicSmemBytes = smem;
