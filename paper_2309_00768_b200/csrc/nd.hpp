@@ -106,7 +106,10 @@ struct NDSweepPlan {
   //   x_T = K z_T,  z_T = top rows of the coupled rhs + the subtree roots' updates,
   // K = (A^{-1})_TT (inverse of the top Schur complement, NDFactor::ktop) -- one GEMV
   // step instead of 2 * ntop tree levels.  Top unknowns in elimination order.
-  int dense = 0, ntT = 0, kc = 0, nch = 0, kpad = 0;
+  // K is stored in row groups of kr rows: block (group g, column chunk c) holds kr x kc
+  // entries column-major ([kc][kr]), so one ring item feeds kr rows (kr = 1: plain rows).
+  int dense = 0, ntT = 0, kc = 0, nch = 0, kpad = 0, kr = 1;
+  int64_t kstride() const { return (int64_t)((ntT + kr - 1) / kr * kr) * kpad; }
   DevBuf ztab;              // int4 x 2 per top unknown {pos, cb0, cb1, cb2}, {cb3, -1, -1, -1}
   DevBuf tidx;              // n: top index of a permuted position, or -1
   DevBuf tsn, tchild;       // top supernodes (postorder) and their top children (K construction)
@@ -178,7 +181,7 @@ struct NDFactor {
   DevBuf status;   // int: 0 ok, 1+ singular (first failing supernode+1)
   uint64_t gen = 0;  // bumped by every factorisation
   // dense inverse of the top Schur complement per batch entry (nd_sweep.cu), built
-  // lazily for the sweep plan that uses it: [nbatch][n_T][kpad] doubles
+  // lazily for the sweep plan that uses it: [nbatch][kstride()] doubles (row groups of kr)
   mutable DevBuf ktop;
   mutable DevBuf scratch, bar;  // batched-solve scratch and grid-barrier words (per factor)
   // small shared factors (nbatch == 1, n <= 2048): dense A^{-1} (column-major), built

@@ -317,8 +317,13 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     if (ok) {
       sp->dense = 1;
       sp->ntT = nT;
-      sp->nch = (nT + 639) / 640;
-      sp->kc = ((nT + sp->nch - 1) / sp->nch + 1) / 2 * 2;  // even: 16-byte aligned chunks
+      // row groups of kr rows x kc columns per ring item (<= one slot); kc even keeps
+      // the items 16-byte aligned
+      static const int kr_env = env_int2("STMHD_SWEEP_DENSE_R", 4);
+      sp->kr = (kr_env == 1 || kr_env == 2 || kr_env == 4 || kr_env == 8) ? kr_env : 4;
+      const int kcmax = (int)(slot_dbl / sp->kr) & ~1;
+      sp->nch = (nT + kcmax - 1) / kcmax;
+      sp->kc = ((nT + sp->nch - 1) / sp->nch + 1) / 2 * 2;
       sp->kpad = sp->nch * sp->kc;
       for (int i = 0; i < nT; ++i) {
         ztab.push_back(make_int4(tpos[i], zc[i][0], zc[i][1], zc[i][2]));
@@ -443,21 +448,22 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   // dense top: one phase level of row tasks (row i of K: nch column chunks of kc)
   std::vector<std::vector<SweepTask>> dense_t(W);
   if (sp->dense) {
-    for (int i = 0; i < sp->ntT; ++i) {
+    const int ng = (sp->ntT + sp->kr - 1) / sp->kr;
+    for (int g = 0; g < ng; ++g) {
       SweepTask t{};
-      t.foff = i * sp->kpad;
+      t.foff = g * sp->kr * sp->kpad;
       t.goff = 0;
-      t.first = tpos[i];
+      t.first = g * sp->kr;  // first row of the group (top index; positions via ztab)
       t.cboff = 0;
       t.c0 = 0;
       t.c1 = (short)sp->nch;
       t.ns = (short)sp->kc;
       t.f = (short)sp->kc;
-      t.rows = 1;
-      t.R = 1;
+      t.rows = (short)sp->kr;
+      t.R = (unsigned char)sp->kr;
       t.flags = 2;
-      t.bsz = sp->kc;
-      dense_t[i % W].push_back(t);
+      t.bsz = sp->kr * sp->kc;
+      dense_t[g % W].push_back(t);
     }
   }
   sp->nl = 2 * sp->nsub + (sp->dense ? 1 : 2 * sp->ntop);
@@ -1021,17 +1027,21 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
   __syncwarp();
 }
 
-// Dense-top row task: x[first] = K[row] . z_T, the row streamed as nch column chunks
-// of kc doubles through the warp's TMA ring (R = 1: lane k covers columns k + 32 q).
+// Dense-top row-group task: x[pos(first + r)] = K[first + r] . z_T for the group's R
+// rows, streamed as nch column chunks ([kc][R] blocks) through the warp's TMA ring
+// (lane = kq * R + r covers columns kq + (32 / R) q of row r).
 template <bool PROF>
 __device__ __forceinline__ void dense_task(const SweepArgs &a, const SweepTask &tk, const double *zs, double *x,
                                            int k, WarpCtx &w, unsigned long long (*mbar)[2]) {
   const int lane = w.lane;
+  const int R = tk.R, kl = 32 / R;
+  // output positions first: the load overlaps the chunk stream instead of the store
+  const int pos = (lane < R && tk.first + lane < a.ntT) ? a.ztab[2 * (tk.first + lane)].x : -1;
   double acc = 0.0;
   for (int c = tk.c0; c < tk.c1; ++c) {
     const int sl = w.jc & 1;
     mbar_wait(&mbar[w.wl][sl], (unsigned)(w.jc >> 1) & 1u);
-    acc += chunk_gemv_smem(w.slot0 + sl * w.slotsz, tk.ns, 32, lane, 1, zs + (int64_t)c * tk.ns, lane);
+    acc += chunk_gemv_smem(w.slot0 + sl * w.slotsz, R * tk.ns, kl, lane / R, R, zs + (int64_t)c * tk.ns, lane);
     __syncwarp();
     ++w.jc;
     if (lane == 0) ring_issue(a, w, mbar);
@@ -1041,7 +1051,7 @@ __device__ __forceinline__ void dense_task(const SweepArgs &a, const SweepTask &
     w.acc[4] += 1;
     w.acc[5] += tk.c1 - tk.c0;
   }
-  if (lane == 0) x[tk.first] = acc;
+  if (pos >= 0) x[pos] = acc;
 }
 
 // Run this CTA's items of a coupling program.  MODE 0 (slab start): rhs rows, item
@@ -1630,7 +1640,7 @@ struct TopKArgs {
   const int *emap, *tidx, *bpos;
   const double *factors;
   int64_t fstride;
-  int ntsn, nT, kpad, nbatch, ncb;
+  int ntsn, nT, kpad, kr, nbatch, ncb;
   double *scratch;    // per CTA: Xw (nT x 32) | CBw (tcb_total x 32)
   int64_t scr_stride;
   double *K;          // [nbatch][nT][kpad]
@@ -1723,14 +1733,16 @@ __global__ void __launch_bounds__(256) topk_kernel(TopKArgs g) {
       __syncthreads();
     }
     if (col < g.nT)
-      for (int i = wl; i < g.nT; i += nw) g.K[(int64_t)b * g.kstride + (int64_t)i * g.kpad + col] = Xw[(int64_t)i * 32 + lane];
+      for (int i = wl; i < g.nT; i += nw)  // row groups of kr: [group][col][kr]
+        g.K[(int64_t)b * g.kstride + (int64_t)(i - i % g.kr) * g.kpad + (int64_t)col * g.kr + i % g.kr] =
+            Xw[(int64_t)i * 32 + lane];
     __syncthreads();
   }
 }
 
 static void build_dense_top(const NDFactor &fac, const NDSweepPlan &sp, cudaStream_t s) {
   const NDPlan &p = *fac.dev->plan;
-  const int64_t kstride = (int64_t)sp.ntT * sp.kpad;
+  const int64_t kstride = sp.kstride();
   const size_t kbytes = (size_t)fac.nbatch * kstride * sizeof(double);
   if (fac.ktop.bytes != kbytes) fac.ktop.alloc_async(kbytes, s);
   STMHD_CUDA_CHECK(cudaMemsetAsync(fac.ktop.ptr, 0, kbytes, s));  // padded columns stay zero
@@ -1747,6 +1759,7 @@ static void build_dense_top(const NDFactor &fac, const NDSweepPlan &sp, cudaStre
   g.ntsn = sp.ntsn;
   g.nT = sp.ntT;
   g.kpad = sp.kpad;
+  g.kr = sp.kr;
   g.nbatch = fac.nbatch;
   g.ncb = (sp.ntT + 31) / 32;
   const int nitems = g.nbatch * g.ncb;
@@ -1949,7 +1962,7 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
     if (fac.ktop_plan != &sp || fac.ktop_gen != fac.gen) build_dense_top(fac, sp, s);
     a.ztab = sp.ztab.as<int4>();
     a.ktop = fac.ktop.as<double>();
-    a.kstride = fac.nbatch == 1 ? 0 : (int64_t)sp.ntT * sp.kpad;
+    a.kstride = fac.nbatch == 1 ? 0 : sp.kstride();
   }
   a.slot = slot;
   a.vstride = vstride;
