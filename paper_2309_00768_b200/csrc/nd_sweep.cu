@@ -640,6 +640,7 @@ struct SweepArgs {
   unsigned *gbar;  // grid mode (one CTA per SM, cooperative launch): software grid barrier word
   int kpref;       // L2 prefetch of the slab's dense-top rows at the slab start
   unsigned long long *progress;  // L2 prefetch cluster: (epoch << 32) | slab in progress (CTA 0)
+  int ldgsts;      // ring items by warp-wide cp.async (16 B per lane) instead of one cp.async.bulk
   unsigned long long *trace;
   unsigned long long *prof;  // PROF instantiation: 6 counters per warp
   unsigned long long *tline; // PROF instantiation: per-warp event timeline of slab 1, CTA 0 (128 per warp)
@@ -750,7 +751,7 @@ struct WarpCtx {
   int jc;                       // chunks consumed (slot jc & 1, mbarrier parity (jc >> 1) & 1)
   int icount, rt, rc, rslab;    // TMA ring cursor (lane 0): two chunks ahead of jc
   // PROF instantiation: cycles in gather / TMA wait / GEMV+store / barriers, tasks, chunks
-  long long acc[8];
+  long long acc[10];  // PROF: 8 issue cycles (ring_issue after a chunk)
   unsigned long long *tl_out;  // timeline (PROF, slab 1 of CTA 0) or null
   int tl_n;
 };
@@ -814,6 +815,31 @@ __device__ __forceinline__ void ring_issue(const SweepArgs &a, WarpCtx &w, unsig
     ++w.icount;
     item_next(w, w.rt, w.rc, w.rslab);
   }
+}
+
+// Warp-wide variant (a.ldgsts, every lane calls it): 16-byte cp.async per lane, the
+// slot's mbarrier (expected count 32) completes once every lane's copies landed.  A
+// cp.async.bulk issue blocks the issuing warp ~350-430 cycles (tools/tma_ring_probe.cu),
+// on the critical path after every chunk; the per-lane copies issue in ~10 cycles each.
+__device__ __forceinline__ void ring_issue_warp(const SweepArgs &a, WarpCtx &w, unsigned long long (*mbar)[2]) {
+  if (w.rslab < a.nslab && w.nt > 0) {
+    const int sl = w.icount & 1;
+    int dbl;
+    const double *src = item_src(a, w.tl[w.rt], w.rc, w.rslab, dbl);
+    double *dst = w.slot0 + sl * w.slotsz;
+    for (int i = 2 * w.lane; i < dbl; i += 64)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst + i)), "l"(src + i) : "memory");
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar[w.wl][sl])) : "memory");
+    ++w.icount;
+    item_next(w, w.rt, w.rc, w.rslab);
+  }
+}
+
+// Refill the ring after a consumed item (call from every lane, after the __syncwarp
+// that ends the item's reads).
+__device__ __forceinline__ void ring_next(const SweepArgs &a, WarpCtx &w, unsigned long long (*mbar)[2]) {
+  if (a.ldgsts) ring_issue_warp(a, w, mbar);
+  else if (w.lane == 0) ring_issue(a, w, mbar);
 }
 
 // GEMV of one shared-memory chunk block [K][R] (R a power of two, lane = kq*R + rl):
@@ -886,7 +912,7 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
   if (PROF) tl_mark(w, 2);
   if (tk.flags & 4) {  // table consumed: its slot goes back to the ring
     ++w.jc;
-    if (lane == 0) ring_issue(a, w, mbar);
+    ring_next(a, w, mbar);
   }
   if (PROF) {
     const long long t1 = pclock<PROF>();
@@ -920,9 +946,11 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
     }
     __syncwarp();
     ++w.jc;
-    if (lane == 0) ring_issue(a, w, mbar);
+    long long ti0 = pclock<PROF>();
+    ring_next(a, w, mbar);
     if (PROF) {
       const long long t1 = pclock<PROF>();
+      w.acc[8] += t1 - ti0;
       w.acc[2] += t1 - t0;
       t0 = t1;
       tl_mark(w, 3);
@@ -984,7 +1012,7 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
   if (PROF) tl_mark(w, 2);
   if (tk.flags & 4) {
     ++w.jc;
-    if (lane == 0) ring_issue(a, w, mbar);
+    ring_next(a, w, mbar);
   }
   if (PROF) {
     const long long t1 = pclock<PROF>();
@@ -1016,9 +1044,11 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
     }
     __syncwarp();
     ++w.jc;
-    if (lane == 0) ring_issue(a, w, mbar);
+    long long ti0 = pclock<PROF>();
+    ring_next(a, w, mbar);
     if (PROF) {
       const long long t1 = pclock<PROF>();
+      w.acc[8] += t1 - ti0;
       w.acc[2] += t1 - t0;
       t0 = t1;
       tl_mark(w, 3);
@@ -1044,7 +1074,7 @@ __device__ __forceinline__ void dense_task(const SweepArgs &a, const SweepTask &
     acc += chunk_gemv_smem(w.slot0 + sl * w.slotsz, R * tk.ns, kl, lane / R, R, zs + (int64_t)c * tk.ns, lane);
     __syncwarp();
     ++w.jc;
-    if (lane == 0) ring_issue(a, w, mbar);
+    ring_next(a, w, mbar);
     if (PROF) tl_mark(w, 3);
   }
   if (PROF) {
@@ -1255,7 +1285,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   w.slot0 = w.v + (a.vstride - 2 * a.slot);
   w.slotsz = a.slot;
   w.jc = w.icount = w.rt = w.rc = w.rslab = 0;
-  for (int i = 0; i < 8; ++i) w.acc[i] = 0;
+  for (int i = 0; i < 10; ++i) w.acc[i] = 0;
   w.tl_out = nullptr;
   w.tl_n = 0;
   long long tb = 0;
@@ -1300,13 +1330,15 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     if (nt > 0) w.rc = first_item(tl[0]);
   }
   if (lane == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[wl][0])) : "memory");
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[wl][1])) : "memory");
+    const unsigned cnt = a.ldgsts ? 32u : 1u;  // warp-wide cp.async: one arrival per lane
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&mbar[wl][0])), "r"(cnt) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&mbar[wl][1])), "r"(cnt) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    if (!a.null_work && w.nt > 0) {  // fill the TMA ring
-      ring_issue(a, w, mbar);
-      ring_issue(a, w, mbar);
-    }
+  }
+  __syncwarp();
+  if (!a.null_work && w.nt > 0) {  // fill the ring
+    ring_next(a, w, mbar);
+    ring_next(a, w, mbar);
   }
   __syncwarp();
   const int64_t n = a.n;
@@ -1457,7 +1489,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     }
   }
   if (PROF && lane == 0)
-    for (int i = 0; i < 8; ++i) a.prof[(crank * a.warps + wl) * 8 + i] = (unsigned long long)w.acc[i];
+    for (int i = 0; i < 10; ++i) a.prof[(crank * a.warps + wl) * 10 + i] = (unsigned long long)w.acc[i];
 }
 
 __global__ void permute_in_kernel(const double *rhs, int64_t ld, const int *pos, int64_t n, int nslab,
@@ -1967,6 +1999,7 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   a.slot = slot;
   a.vstride = vstride;
   a.null_work = env_int2("STMHD_SWEEP_NULL", 0);
+  a.ldgsts = env_int2("STMHD_SWEEP_LDGSTS", 0);
   a.kpref = env_int2("STMHD_SWEEP_KPREF", 0);  // measured: no gain (dense step not HBM-latency bound)
   a.post_hdr = nullptr;  // set by sweep_stage_set_post for this launch
   a.gbar = nullptr;
@@ -2184,7 +2217,7 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
   DevBuf pr;
   DevBuf tlb;
   if (prof_on) {
-    pr.alloc((size_t)stg[ts]->ncta * warps * 8 * sizeof(unsigned long long));
+    pr.alloc((size_t)stg[ts]->ncta * warps * 10 * sizeof(unsigned long long));
     m.st[ts].prof = pr.as<unsigned long long>();
     tlb.alloc((size_t)warps * 128 * sizeof(unsigned long long));
     STMHD_CUDA_CHECK(cudaMemsetAsync(tlb.ptr, 0, tlb.bytes, s));
@@ -2280,21 +2313,21 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
   }
   if (prof_on) {
     const int nwp = stg[ts]->ncta * warps;
-    std::vector<unsigned long long> h((size_t)nwp * 8);
+    std::vector<unsigned long long> h((size_t)nwp * 10);
     STMHD_CUDA_CHECK(cudaMemcpyAsync(h.data(), pr.ptr, h.size() * 8, cudaMemcpyDeviceToHost, s));
     STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-    double mean[8] = {0}, mx[8] = {0};
+    double mean[10] = {0}, mx[10] = {0};
     for (int w = 0; w < nwp; ++w)
-      for (int i = 0; i < 8; ++i) {
-        mean[i] += (double)h[w * 8 + i] / nwp;
-        mx[i] = std::max(mx[i], (double)h[w * 8 + i]);
+      for (int i = 0; i < 10; ++i) {
+        mean[i] += (double)h[w * 10 + i] / nwp;
+        mx[i] = std::max(mx[i], (double)h[w * 10 + i]);
       }
     const double us = 1.0 / 1963.0 / nrhs0;  // cycles -> us per slab at the loaded SM clock
     fprintf(stderr,
             "[sweep-prof] per slab per warp (us) mean/max: gather %.2f/%.2f wait %.2f/%.2f gemv %.2f/%.2f "
-            "barrier %.2f/%.2f | tasks %.1f/%.0f chunks %.1f/%.0f | gemv-only fwd %.2f bwd %.2f\n",
+            "barrier %.2f/%.2f | tasks %.1f/%.0f chunks %.1f/%.0f | gemv-only fwd %.2f bwd %.2f | issue %.2f\n",
             mean[0] * us, mx[0] * us, mean[1] * us, mx[1] * us, mean[2] * us, mx[2] * us, mean[3] * us, mx[3] * us,
-            mean[4] / nrhs0, mx[4] / nrhs0, mean[5] / nrhs0, mx[5] / nrhs0, mean[6] * us, mean[7] * us);
+            mean[4] / nrhs0, mx[4] / nrhs0, mean[5] / nrhs0, mx[5] / nrhs0, mean[6] * us, mean[7] * us, mean[8] * us);
     // timeline of slab 1, CTA 0: per warp, events (1 level start fwd, 2 gathered, 3 chunk, 4 level done fwd,
     // 5 level start bwd, 6 level done bwd) in us from the first event
     std::vector<unsigned long long> tv((size_t)warps * 128);

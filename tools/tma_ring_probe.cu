@@ -17,7 +17,29 @@ __global__ void ring_kernel(const double *src, long long per_warp, int S, int D,
   double *slots = sm + (long long)wl * D * S;
   const int nch = (int)(per_warp / S);
   double acc = 0.0;
-  if (use_ldg) {
+  long long t_arrive = 0, t_issue = 0;
+  if (use_ldg == 2) {
+    auto issue = [&](int c) {
+      if (c < nch) {
+        const double *g = base + (long long)c * S;
+        double *d = slots + (c % D) * S;
+        for (int i = 2 * lane; i < S; i += 64)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(d + i)), "l"(g + i) : "memory");
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    for (int d = 0; d < D; ++d) issue(d);
+    for (int c = 0; c < nch; ++c) {
+      if (D == 2) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      else asm volatile("cp.async.wait_group 3;\n" ::: "memory");
+      __syncwarp();
+      const double *b = slots + (c % D) * S;
+      if (wmode != 4)
+        for (int i = lane; i < S; i += 32) acc += b[i];
+      __syncwarp();
+      issue(c + D);
+    }
+  } else if (use_ldg) {
     for (int c = 0; c < nch; ++c) {
       const double *p = base + (long long)c * S;
       for (int i = lane; i < S; i += 32) acc += __ldg(p + i);
@@ -87,48 +109,70 @@ __global__ void ring_kernel(const double *src, long long per_warp, int S, int D,
       }
       __syncwarp();
       if (c + D < nch) {
+        long long q0 = clock64();
         if (lane == 0)
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&mbar[wl][sl])),
                        "r"(S * 8)
                        : "memory");
         __syncwarp();
+        long long q1 = clock64();
+        if (lane == 0) { t_arrive += q1 - q0; }
         if (lane < P) {
           const int ps = S / P;
+          if (wmode == 0)
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                   smem_u32(slots + sl * S + lane * ps)),
               "l"(base + (long long)(c + D) * S + lane * ps), "r"(ps * 8), "r"(smem_u32(&mbar[wl][sl]))
               : "memory");
+          else if (wmode == 1)
+          asm volatile(
+              "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                  smem_u32(slots + sl * S + lane * ps)),
+              "l"(base + (long long)(c + D) * S + lane * ps), "r"(ps * 8), "r"(smem_u32(&mbar[wl][sl]))
+              : "memory");
+          else
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+                  smem_u32(slots + sl * S + lane * ps)),
+              "l"(base + (long long)(c + D) * S + lane * ps), "r"(ps * 8), "r"(smem_u32(&mbar[wl][sl])), "l"(0x14F0000000000000ull)
+              : "memory");
         }
+        __syncwarp();
+        if (lane == 0) t_issue += clock64() - q1;
       }
     }
   }
   if (acc == 12345.678) out[0] = acc;
+  if (lane == 0 && blockIdx.x == 0 && wl == 0) {
+    out[1] = (double)t_arrive / nch;
+    out[2] = (double)t_issue / nch;
+  }
 }
 
 int main(int argc, char **argv) {
   const long long total = 1LL << 27;  // doubles (1 GB)
   double *src, *out;
   cudaMalloc(&src, total * 8);
-  cudaMalloc(&out, 8);
+  cudaMalloc(&out, 64);
   cudaMemset(src, 0, total * 8);
   cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const int Gs[] = {16, 32};
-  const int Ws[] = {8, 16, 32};
-  const int Ss[] = {320, 640, 1280};
-  const int Ds[] = {1, 2, 4};
+  const int Gs[] = {16};
+  const int Ws[] = {8, 16};
+  const int Ss[] = {320, 640};
+  const int Ds[] = {2, 4};
   const int Ps[] = {1};
   for (int P : Ps)
-  for (int wmode = 0; wmode < 5; wmode += 4)
+  for (int wmode = 0; wmode < 3; wmode += 1)
   for (int l2 = 0; l2 < 1; ++l2)
     for (int G : Gs)
       for (int W : Ws)
         for (int S : Ss)
           for (int D : Ds)
-            for (int ldg = 0; ldg < 1; ++ldg) {
+            for (int ldg = 0; ldg < 1; ldg += 2) {
               const size_t smem = (size_t)W * D * S * 8;
               if (smem > 200 * 1024) continue;
               // l2 = 1: each warp re-reads a small range (L2 resident: 32 MB total)
@@ -144,8 +188,11 @@ int main(int argc, char **argv) {
               float ms;
               cudaEventElapsedTime(&ms, e0, e1);
               const double bytes = (double)per_warp * 8 * G * W * reps;
+              double ho[3];
+              cudaMemcpy(ho, out, 24, cudaMemcpyDeviceToHost);
+              printf("arrive %.0f cyc issue %.0f cyc | ", ho[1], ho[2]);
               printf("P=%d mode%d %s G=%3d W=%2d S=%4d D=%d %s : %8.1f GB/s total  %6.1f GB/s per SM\n", P, wmode, l2 ? "L2 " : "HBM", G, W,
-                     S, D, ldg ? "ldg" : "tma", bytes / ms / 1e6, bytes / ms / 1e6 / G);
+                     S, D, ldg ? "ldgsts" : "tma", bytes / ms / 1e6, bytes / ms / 1e6 / G);
             }
   cudaError_t e = cudaGetLastError();
   printf("%s\n", cudaGetErrorString(e));
