@@ -2225,7 +2225,7 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
   }
   // L2 prefetch cluster (cluster mode): one extra 16-CTA cluster when the device
   // can hold it next to the stages (STMHD_SWEEP_L2PF = prefetch distance in slabs, 0 off)
-  static const int pf_env = env_int2("STMHD_SWEEP_L2PF", 1);
+  static const int pf_env = env_int2("STMHD_SWEEP_L2PF", 0);  // off: ~1 % on the wave sweep only, +40 % DRAM reads
   int pf = 0;
   if (!grid && pf_env > 0) {
     static int max_clusters = -1;
