@@ -52,3 +52,23 @@ def test_grid_modes_match_cluster_mode(tmp_path):
     for k in ("z", "s"):
         err = np.linalg.norm(a[k] - b[k]) / np.linalg.norm(a[k])
         assert err < 1e-10, (k, err)
+
+
+@pytest.mark.parametrize("opt", [
+    {"STMHD_SWEEP_DENSE_R": "1"},   # dense top as plain K rows (one row per ring item)
+    {"STMHD_SWEEP_DENSE_R": "8"},   # row groups of 8
+    {"STMHD_SWEEP_L2PF": "1"},      # extra L2 prefetch cluster next to the stages
+    {"STMHD_SWEEP_LDGSTS": "1"},    # warp-wide cp.async item ring instead of cp.async.bulk
+])
+def test_sweep_options_match_default(tmp_path, opt):
+    """The sweep's optional layouts and item paths (nd_sweep.cu, off by default) give
+    the same P_T^{-1} (pipelined three-stage launch) and C5 inverse (single stage)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    a = _run(tmp_path, {}, "default.npz")
+    b = _run(tmp_path, opt, "opt.npz")
+    for k in ("z", "s"):
+        err = np.linalg.norm(a[k] - b[k]) / np.linalg.norm(a[k])
+        assert err < 1e-12, (k, opt, err)
