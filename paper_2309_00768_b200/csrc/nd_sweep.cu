@@ -1388,7 +1388,9 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       }
       __syncthreads();
       const double *vk = a.prog_vals + (a.prog_per_slab ? (int64_t)k * a.prog_nent : 0);
+      long long tp0 = pclock<PROF>();
       run_program<0>(a.prog_hdr[crank], a.prog_items, a.prog_ecol, vk, rhs, nullptr, sv, a.tbuf, s_src);
+      if (PROF) w.acc[9] += pclock<PROF>() - tp0;
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step, crank);
     }
@@ -2325,9 +2327,10 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
     const double us = 1.0 / 1963.0 / nrhs0;  // cycles -> us per slab at the loaded SM clock
     fprintf(stderr,
             "[sweep-prof] per slab per warp (us) mean/max: gather %.2f/%.2f wait %.2f/%.2f gemv %.2f/%.2f "
-            "barrier %.2f/%.2f | tasks %.1f/%.0f chunks %.1f/%.0f | gemv-only fwd %.2f bwd %.2f | issue %.2f\n",
+            "barrier %.2f/%.2f | tasks %.1f/%.0f chunks %.1f/%.0f | gemv-only fwd %.2f bwd %.2f | issue %.2f | coupling %.2f/%.2f\n",
             mean[0] * us, mx[0] * us, mean[1] * us, mx[1] * us, mean[2] * us, mx[2] * us, mean[3] * us, mx[3] * us,
-            mean[4] / nrhs0, mx[4] / nrhs0, mean[5] / nrhs0, mx[5] / nrhs0, mean[6] * us, mean[7] * us, mean[8] * us);
+            mean[4] / nrhs0, mx[4] / nrhs0, mean[5] / nrhs0, mx[5] / nrhs0, mean[6] * us, mean[7] * us, mean[8] * us,
+            mean[9] * us, mx[9] * us);
     // timeline of slab 1, CTA 0: per warp, events (1 level start fwd, 2 gathered, 3 chunk, 4 level done fwd,
     // 5 level start bwd, 6 level done bwd) in us from the first event
     std::vector<unsigned long long> tv((size_t)warps * 128);
