@@ -168,3 +168,45 @@ def test_solve_bitwise_reproducible(p):
     assert st1.newton_iters == st2.newton_iters
     assert st1.gmres_iters == st2.gmres_iters
     assert np.array_equal(_np(s1.vec.data), _np(s2.vec.data))
+
+
+# -- preconditioner pieces (reference tests/test_precond.py:39-48,139-154) ------------
+
+
+def test_alfven_scaling_tearing_equilibrium_analytic_device(p):
+    """The device Alfven kernel (assembly pass) on the Harris sheet: the mean field is
+    exactly (2/5) log cosh(5/2) in every slab (reference precond.py:46-57,89-90)."""
+    import torch
+
+    prob = p.by_name("tearing_mode")
+    disc = p.discretize(prob, 0.25, 0.5, 1.0)
+    state = p.initial_state(disc)
+    a = torch.as_tensor(disc.pot.interp(prob.a_eq), dtype=torch.float64, device="cuda")
+    state.vec.fields("A")[:] = a
+    jac = p.assemble_jacobian(state, disc)
+    s = p.SpaceTimePreconditioner(jac, disc, state).alfven
+    b_norm = 0.4 * np.log(np.cosh(2.5))
+    assert np.all(np.abs(np.sqrt(s * prob.mu0) - b_norm) < 1e-8)
+    assert np.all(np.abs(s - b_norm**2 / prob.mu0) < 1e-10)
+
+
+@pytest.fixture(scope="module")
+def small_pc(p, small):
+    disc, state, jac = small
+    return disc, p.SpaceTimePreconditioner(jac, disc, state)
+
+
+@pytest.mark.parametrize("pair,field,tol", [
+    (("pressure_schur_inverse", "pressure_schur_apply"), "n_p", 1e-10),
+    (("magnetic_schur_inverse", "magnetic_schur_apply"), "n_a", 1e-9),
+    (("solve_velocity", "apply_velocity"), "n_u", 1e-10),
+    (("solve_wave", "apply_wave"), "n_a", 1e-10),
+])
+def test_sub_operator_round_trips(p, small_pc, pair, field, tol):
+    disc, pc = small_pc
+    inv, fwd = getattr(pc, pair[0]), getattr(pc, pair[1])
+    n = getattr(disc.layout, field) * pc.n_steps
+    for _ in range(3):
+        x = RNG.standard_normal(n)
+        y = _np(inv(fwd(x)))
+        assert np.linalg.norm(y - x) <= tol * np.linalg.norm(x)
