@@ -1280,7 +1280,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   w.lane = threadIdx.x & 31;
   w.wl = threadIdx.x >> 5;
   const int lane = w.lane, wl = w.wl;
-  const int gw = wl * a.ncta + crank;  // interleaved across CTAs (top phases)
+  // (top-phase task lists are interleaved across CTAs: global warp wl * ncta + crank)
   w.v = sm + wl * a.vstride;
   w.slot0 = w.v + (a.vstride - 2 * a.slot);
   w.slotsz = a.slot;
