@@ -210,3 +210,14 @@ def test_sub_operator_round_trips(p, small_pc, pair, field, tol):
         x = RNG.standard_normal(n)
         y = _np(inv(fwd(x)))
         assert np.linalg.norm(y - x) <= tol * np.linalg.norm(x)
+
+
+def test_singular_velocity_block_raises_preconditioner_error(p, small):
+    """A zero-pivot F_u factorisation surfaces as PreconditionerError('F_u')
+    (reference precond.py:108-113; status STMHD_SINGULAR through the C-ABI)."""
+    disc, state, _ = small
+    jac = p.assemble_jacobian(state, disc)
+    jac.values.zero_()
+    with pytest.raises(p.PreconditionerError) as err:
+        p.SpaceTimePreconditioner(jac, disc, state)
+    assert err.value.block == "F_u"
