@@ -1681,70 +1681,98 @@ struct TopKArgs {
   int64_t kstride;
 };
 
-// acc[i] = sum_k blk(r0 + i, k) V[k][lane], i < 4 (rows >= nrows give 0), for a factor
-// block stored as row chunks [K][R] (element (r, k) at (r / R) * bsz + k * R + r % R).
+// acc[i][h] = sum_k blk(r0 + i, k) V[k][lane + 32 h], i < 4 (rows >= nrows give 0), h < NC,
+// for a factor block stored as row chunks [K][R] (element (r, k) at (r / R) * bsz + k * R +
+// r % R).  Every factor load feeds NC x 32 columns.
+template <int NC>
 __device__ __forceinline__ void topk_rows4(const double *blk, int R, int bsz, int r0, int nrows, int K,
-                                           const double *V, int lane, double acc[4]) {
+                                           const double *V, int lane, double (&acc)[4][NC]) {
+  constexpr int CS = 32 * NC;
   const double *row[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = min(r0 + i, nrows - 1);
     row[i] = blk + (int64_t)(r / R) * bsz + (r % R);
-    acc[i] = 0.0;
+#pragma unroll
+    for (int h = 0; h < NC; ++h) acc[i][h] = 0.0;
   }
   int k = 0;
   for (; k + 4 <= K; k += 4) {
-    double fv[4][4], vv[4];
+    double fv[4][4], vv[4][NC];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      vv[j] = V[(k + j) * 32 + lane];
+#pragma unroll
+      for (int h = 0; h < NC; ++h) vv[j][h] = V[(k + j) * CS + lane + 32 * h];
 #pragma unroll
       for (int i = 0; i < 4; ++i) fv[i][j] = __ldg(row[i] + (int64_t)(k + j) * R);
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i] = fma(fv[i][j], vv[j], acc[i]);
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int h = 0; h < NC; ++h) acc[i][h] = fma(fv[i][j], vv[j][h], acc[i][h]);
   }
   for (; k < K; ++k) {
-    const double v = V[k * 32 + lane];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) acc[i] = fma(__ldg(row[i] + (int64_t)k * R), v, acc[i]);
+    for (int i = 0; i < 4; ++i) {
+      const double f = __ldg(row[i] + (int64_t)k * R);
+#pragma unroll
+      for (int h = 0; h < NC; ++h) acc[i][h] = fma(f, V[k * CS + lane + 32 * h], acc[i][h]);
+    }
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i)
-    if (r0 + i >= nrows) acc[i] = 0.0;
+    if (r0 + i >= nrows)
+#pragma unroll
+      for (int h = 0; h < NC; ++h) acc[i][h] = 0.0;
 }
 
-__global__ void __launch_bounds__(256) topk_kernel(TopKArgs g) {
-  extern __shared__ __align__(16) double V[];  // front x 32
+// K = (A^{-1})_TT for every slab: item = (slab, block of 32 NC identity columns), lane
+// column lane + 32 h; the columns are pushed through the top supernodes' own FL / FU
+// blocks (forward in postorder, backward in reverse), so K reproduces exactly what the
+// top tree levels of the sweep would compute.
+template <int NC>
+__global__ void __launch_bounds__(256 * NC) topk_kernel(TopKArgs g) {
+  constexpr int CS = 32 * NC;
+  extern __shared__ __align__(16) double V[];  // front x CS
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double *Xw = g.scratch + (int64_t)blockIdx.x * g.scr_stride;
-  double *CBw = Xw + (int64_t)g.nT * 32;
+  double *CBw = Xw + (int64_t)g.nT * CS;
   const int nitems = g.nbatch * g.ncb;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int b = item / g.ncb, col = (item % g.ncb) * 32 + lane;
+    const int b = item / g.ncb, col = (item % g.ncb) * CS + lane;
     const double *F = g.factors + (int64_t)b * g.fstride;
     for (int si = 0; si < g.ntsn; ++si) {  // forward, postorder
       const TopSN t = g.tsn[si];
       const int f = t.ns + t.nb;
-      for (int r = wl; r < f; r += nw) V[r * 32 + lane] = (r < t.ns && g.tidx[t.first + r] == col) ? 1.0 : 0.0;
+      for (int r = wl; r < f; r += nw) {
+        const int ti = r < t.ns ? g.tidx[t.first + r] : -1;
+#pragma unroll
+        for (int h = 0; h < NC; ++h) V[r * CS + lane + 32 * h] = (ti == col + 32 * h) ? 1.0 : 0.0;
+      }
       __syncthreads();
       for (int c = 0; c < t.nchild; ++c) {  // extend-add the top children's updates
         const int4 ch = g.tchild[t.child0 + c];
         const int cb0 = g.tsn[ch.x].tcb_off;
-        for (int a = wl; a < ch.z; a += nw) V[g.emap[ch.y + a] * 32 + lane] += CBw[(int64_t)(cb0 + a) * 32 + lane];
+        for (int a = wl; a < ch.z; a += nw)
+#pragma unroll
+          for (int h = 0; h < NC; ++h)
+            V[g.emap[ch.y + a] * CS + lane + 32 * h] += CBw[(int64_t)(cb0 + a) * CS + lane + 32 * h];
         __syncthreads();
       }
       for (int r0 = wl * 4; r0 < f; r0 += nw * 4) {  // 4 rows per warp, 16 factor loads in flight
-        double acc[4];
-        topk_rows4(F + t.fl_off, t.rf, t.bszf, r0, f, t.ns, V, lane, acc);
+        double acc[4][NC];
+        topk_rows4<NC>(F + t.fl_off, t.rf, t.bszf, r0, f, t.ns, V, lane, acc);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int r = r0 + i;
           if (r >= f) break;
-          if (r < t.ns) Xw[(int64_t)g.tidx[t.first + r] * 32 + lane] = acc[i];  // y
-          else CBw[(int64_t)(t.tcb_off + r - t.ns) * 32 + lane] = V[r * 32 + lane] - acc[i];
+#pragma unroll
+          for (int h = 0; h < NC; ++h) {
+            if (r < t.ns) Xw[(int64_t)g.tidx[t.first + r] * CS + lane + 32 * h] = acc[i][h];  // y
+            else CBw[(int64_t)(t.tcb_off + r - t.ns) * CS + lane + 32 * h] = V[r * CS + lane + 32 * h] - acc[i][h];
+          }
         }
       }
       __syncthreads();
@@ -1754,22 +1782,28 @@ __global__ void __launch_bounds__(256) topk_kernel(TopKArgs g) {
       const int f = t.ns + t.nb;
       for (int r = wl; r < f; r += nw) {
         const int pos = r < t.ns ? t.first + r : g.bpos[t.goff + r];
-        V[r * 32 + lane] = Xw[(int64_t)g.tidx[pos] * 32 + lane];  // own y, or the ancestors' x
+#pragma unroll
+        for (int h = 0; h < NC; ++h)  // own y, or the ancestors' x
+          V[r * CS + lane + 32 * h] = Xw[(int64_t)g.tidx[pos] * CS + lane + 32 * h];
       }
       __syncthreads();
       for (int k0 = wl * 4; k0 < t.ns; k0 += nw * 4) {
-        double acc[4];
-        topk_rows4(F + t.fu_off, t.rb, t.bszb, k0, t.ns, f, V, lane, acc);
+        double acc[4][NC];
+        topk_rows4<NC>(F + t.fu_off, t.rb, t.bszb, k0, t.ns, f, V, lane, acc);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          if (k0 + i < t.ns) Xw[(int64_t)g.tidx[t.first + k0 + i] * 32 + lane] = acc[i];
+          if (k0 + i < t.ns)
+#pragma unroll
+            for (int h = 0; h < NC; ++h) Xw[(int64_t)g.tidx[t.first + k0 + i] * CS + lane + 32 * h] = acc[i][h];
       }
       __syncthreads();
     }
-    if (col < g.nT)
-      for (int i = wl; i < g.nT; i += nw)  // row groups of kr: [group][col][kr]
-        g.K[(int64_t)b * g.kstride + (int64_t)(i - i % g.kr) * g.kpad + (int64_t)col * g.kr + i % g.kr] =
-            Xw[(int64_t)i * 32 + lane];
+#pragma unroll
+    for (int h = 0; h < NC; ++h)
+      if (col + 32 * h < g.nT)
+        for (int i = wl; i < g.nT; i += nw)  // row groups of kr: [group][col][kr]
+          g.K[(int64_t)b * g.kstride + (int64_t)(i - i % g.kr) * g.kpad + (int64_t)(col + 32 * h) * g.kr + i % g.kr] =
+              Xw[(int64_t)i * CS + lane + 32 * h];
     __syncthreads();
   }
 }
@@ -1795,23 +1829,32 @@ static void build_dense_top(const NDFactor &fac, const NDSweepPlan &sp, cudaStre
   g.kpad = sp.kpad;
   g.kr = sp.kr;
   g.nbatch = fac.nbatch;
-  g.ncb = (sp.ntT + 31) / 32;
+  // NC column halves per lane (STMHD_TOPK_NC, 1 or 2): each factor load feeds 32 NC
+  // columns; NC = 2 runs 16 warps per CTA with the wider front block when it fits
+  static const int nc_env = env_int2("STMHD_TOPK_NC", 2);
+  int nc = nc_env == 1 ? 1 : 2;
+  if ((size_t)fmax * 64 * sizeof(double) > 200 * 1024) nc = 1;
+  const int cs = 32 * nc;
+  g.ncb = (sp.ntT + cs - 1) / cs;
+  const size_t smem = (size_t)fmax * cs * sizeof(double);
+  require(smem <= 200 * 1024, "dense top: front too large");
+  const int per_sm = std::max(1, std::min(2, (int)((220 * 1024) / std::max<size_t>(smem, 1))));
   const int nitems = g.nbatch * g.ncb;
-  const int grid = std::max(1, std::min(nitems, 2 * num_sms()));
-  g.scr_stride = (int64_t)(sp.ntT + sp.tcb_total) * 32;
+  const int grid = std::max(1, std::min(nitems, per_sm * num_sms()));
+  g.scr_stride = (int64_t)(sp.ntT + sp.tcb_total) * cs;
   DevBuf scr;
   scr.alloc_async((size_t)grid * g.scr_stride * sizeof(double), s);
   g.scratch = scr.as<double>();
   g.K = fac.ktop.as<double>();
   g.kstride = kstride;
-  const size_t smem = (size_t)fmax * 32 * sizeof(double);
-  require(smem <= 200 * 1024, "dense top: front too large");
-  static size_t attr = 0;
-  if (smem > attr) {
-    STMHD_CUDA_CHECK(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
+  static size_t attr[2] = {0, 0};
+  const void *fn = nc == 2 ? (const void *)topk_kernel<2> : (const void *)topk_kernel<1>;
+  if (smem > attr[nc - 1]) {
+    STMHD_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr[nc - 1] = smem;
   }
-  topk_kernel<<<grid, 256, smem, s>>>(g);
+  if (nc == 2) topk_kernel<2><<<grid, 512, smem, s>>>(g);
+  else topk_kernel<1><<<grid, 256, smem, s>>>(g);
   STMHD_LAUNCH_CHECK();
   fac.ktop_plan = &sp;
   fac.ktop_gen = fac.gen;
