@@ -1838,7 +1838,10 @@ static void build_dense_top(const NDFactor &fac, const NDSweepPlan &sp, cudaStre
   g.ncb = (sp.ntT + cs - 1) / cs;
   const size_t smem = (size_t)fmax * cs * sizeof(double);
   require(smem <= 200 * 1024, "dense top: front too large");
-  const int per_sm = std::max(1, std::min(2, (int)((220 * 1024) / std::max<size_t>(smem, 1))));
+  // one 16-warp CTA per SM for NC = 2 (two 8-warp CTAs for NC = 1): the same warps per
+  // SM and the same scratch footprint (a larger pooled scratch was measured to slow the
+  // next factorisation's workspace allocations)
+  const int per_sm = nc == 2 ? 1 : std::max(1, std::min(2, (int)((220 * 1024) / std::max<size_t>(smem, 1))));
   const int nitems = g.nbatch * g.ncb;
   const int grid = std::max(1, std::min(nitems, per_sm * num_sms()));
   g.scr_stride = (int64_t)(sp.ntT + sp.tcb_total) * cs;
