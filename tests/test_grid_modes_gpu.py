@@ -59,6 +59,7 @@ def test_grid_modes_match_cluster_mode(tmp_path):
     {"STMHD_SWEEP_DENSE_R": "8"},   # row groups of 8
     {"STMHD_SWEEP_L2PF": "1"},      # extra L2 prefetch cluster next to the stages
     {"STMHD_SWEEP_LDGSTS": "1"},    # warp-wide cp.async item ring instead of cp.async.bulk
+    {"STMHD_TOPK_NC": "1"},         # dense-top K built with 32 identity columns per item
 ])
 def test_sweep_options_match_default(tmp_path, opt):
     """The sweep's optional layouts and item paths (nd_sweep.cu, off by default) give
