@@ -271,22 +271,51 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     th[sn] = h;
     ntop = std::max(ntop, h + 1);
   }
-  std::vector<std::vector<int>> top_sn(ntop);
-  for (int sn = 0; sn < p.nsn; ++sn)
-    if (owner[sn] < 0) top_sn[th[sn]].push_back(sn);
-  sp->ntop = ntop;
   int nsub = 0;
   for (int r = 0; r < (int)roots.size(); ++r) nsub = std::max(nsub, p.level[roots[r]] + 1);
   sp->nsub = roots.empty() ? 0 : nsub;
   sp->sub_len = maxlen;
   sp->sub_cb = maxcb;
   // ---- dense top: one GEMV with K = (A^{-1})_TT replaces the top tree levels ----
+  // K covers the top `kl` heights of the top tree (the K region: those supernodes and
+  // all their ancestors); the heights below it (the band) stay tree levels, run
+  // cluster/grid-wide between the subtree phase and the dense step.  kl = ntop: the
+  // whole top is dense (no band).  The largest kl whose K fits the size rule wins.
   static const int dense_env = env_int2("STMHD_SWEEP_DENSE_TOP", 1);
+  static const int klev_env = env_int2("STMHD_SWEEP_KLEVELS", -1);  // force kl (0: no dense top)
+  static const int kmax_env = env_int2("STMHD_SWEEP_KMAX", 1100);   // largest K order with a band
+  std::vector<char> isK(p.nsn, 0);
+  int kl = 0;
   std::vector<int> tpos, tidx_h(p.n, -1);
   std::vector<int4> ztab;
   if (dense_env && mode <= 1 && sp->nsub > 0 && ntop > 0) {
-    for (int sn = 0; sn < p.nsn; ++sn)  // top unknowns in elimination order
-      if (owner[sn] < 0)
+    std::vector<int64_t> tcount(ntop + 1, 0);  // unknowns of the top kl heights
+    for (int sn = 0; sn < p.nsn; ++sn)
+      if (owner[sn] < 0) tcount[ntop - th[sn]] += p.ns[sn];
+    for (int d = 1; d <= ntop; ++d) tcount[d] += tcount[d - 1];
+    auto fits = [&](int d) {
+      const int64_t nT = tcount[d];
+      if (nT <= 0 || nT > 4096) return false;
+      if (d == ntop)  // whole top: K (nT^2 per slab) may not outgrow the factor itself
+        return nT * nT * (ncta <= 48 ? 1 : (max_sub < ncta ? 2 : 8)) <= p.factor_size;
+      return nT <= kmax_env && 2 * nT * nT <= p.factor_size;
+    };
+    if (klev_env >= 0) kl = std::min(klev_env, ntop);
+    else
+      for (int d = ntop; d >= 1 && !kl; --d)
+        if (fits(d)) kl = d;
+    if (kl > 0 && tcount[kl] > 4096) kl = 0;
+  }
+  for (int sn = 0; sn < p.nsn; ++sn)
+    if (owner[sn] < 0 && th[sn] >= ntop - kl) isK[sn] = 1;
+  const int nband = ntop - kl;
+  std::vector<std::vector<int>> top_sn(nband);
+  for (int sn = 0; sn < p.nsn; ++sn)
+    if (owner[sn] < 0 && !isK[sn]) top_sn[th[sn]].push_back(sn);
+  sp->ntop = nband;
+  if (kl > 0) {
+    for (int sn = 0; sn < p.nsn; ++sn)  // K unknowns in elimination order
+      if (isK[sn])
         for (int t = 0; t < p.ns[sn]; ++t) {
           const int q = (int)(p.first[sn] + t);
           tidx_h[q] = (int)tpos.size();
@@ -294,24 +323,29 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
         }
     const int nT = (int)tpos.size();
     std::vector<std::array<int, 4>> zc(nT, {-1, -1, -1, -1});
-    // K (nT^2 per slab) may not outgrow the factor itself (batched per-slab factors)
-    bool ok = nT > 0 && nT <= 4096 &&
-              (int64_t)nT * nT * (ncta <= 48 ? 1 : (max_sub < ncta ? 2 : 8)) <= p.factor_size;
-    for (int r : roots) {  // subtree roots' updates land on top unknowns
-      for (int a = 0; a < p.nb[r] && ok; ++a) {
-        const int tgt = bpos[p.idx_off[r] + p.ns[r] + a];
-        const int i = tgt >= 0 ? tidx_h[tgt] : -1;
-        if (i < 0) {
-          ok = false;
-          break;
+    bool ok = nT > 0;
+    // updates of the K region's children outside it (band nodes or subtree roots; they
+    // write their update vectors to global memory) land on K unknowns: z_T inputs
+    for (int sn = 0; sn < p.nsn && ok; ++sn) {
+      if (!isK[sn]) continue;
+      for (int ci = p.child_ptr[sn]; ci < p.child_ptr[sn + 1] && ok; ++ci) {
+        const int r = p.child_list[ci];
+        if (isK[r]) continue;
+        for (int a = 0; a < p.nb[r]; ++a) {
+          const int tgt = bpos[p.idx_off[r] + p.ns[r] + a];
+          const int i = tgt >= 0 ? tidx_h[tgt] : -1;
+          if (i < 0) {
+            ok = false;
+            break;
+          }
+          int sl = 0;
+          while (sl < 4 && zc[i][sl] >= 0) ++sl;
+          if (sl == 4) {
+            ok = false;
+            break;
+          }
+          zc[i][sl] = (int)(p.cbv_off[r] + a);
         }
-        int sl = 0;
-        while (sl < 4 && zc[i][sl] >= 0) ++sl;
-        if (sl == 4) {
-          ok = false;
-          break;
-        }
-        zc[i][sl] = (int)(p.cbv_off[r] + a);
       }
     }
     if (ok) {
@@ -329,6 +363,14 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
         ztab.push_back(make_int4(tpos[i], zc[i][0], zc[i][1], zc[i][2]));
         ztab.push_back(make_int4(zc[i][3], -1, -1, -1));
       }
+    } else {  // no dense top: the whole top runs as tree levels
+      std::fill(isK.begin(), isK.end(), 0);
+      std::fill(tidx_h.begin(), tidx_h.end(), -1);
+      tpos.clear();
+      top_sn.assign(ntop, {});
+      for (int sn = 0; sn < p.nsn; ++sn)
+        if (owner[sn] < 0) top_sn[th[sn]].push_back(sn);
+      sp->ntop = ntop;
     }
   }
   // ---- subtree front tables resident in shared memory (dense mode) ----
@@ -339,7 +381,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   static const int stab_env = env_int2("STMHD_SWEEP_SMEM_TABLES", 1);
   std::vector<int> ftab_off(p.nsn, -1), btab_off(p.nsn, -1), sn_of_first(p.n, -1);
   std::vector<int> tab_all, tab_ptr(ncta + 1, 0), tab_nf(ncta, 0);
-  bool stab = stab_env && mode == 0 && sp->dense && sp->nsub > 0 && maxlen < 32768 && maxcb < 32768 &&
+  bool stab = stab_env && mode == 0 && sp->dense && sp->ntop == 0 && sp->nsub > 0 && maxlen < 32768 && maxcb < 32768 &&
               sp->ntT < 32768;
   if (stab) {
     for (int sn = 0; sn < p.nsn; ++sn) sn_of_first[p.first[sn]] = sn;
@@ -466,7 +508,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
       dense_t[g % W].push_back(t);
     }
   }
-  sp->nl = 2 * sp->nsub + (sp->dense ? 1 : 2 * sp->ntop);
+  sp->nl = 2 * sp->nsub + 2 * sp->ntop + (sp->dense ? 1 : 0);
   {
     std::vector<SweepTask> all;
     std::vector<int> off, bnd;
@@ -480,12 +522,9 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
           all.insert(all.end(), v.begin(), v.end());
         };
         for (int h = 0; h < sp->nsub; ++h) add(sub_t[1][((size_t)c * sp->nsub + h) * warps + w]);
-        if (sp->dense) {
-          add(dense_t[w * ncta + c]);
-        } else {
-          for (int t = 0; t < sp->ntop; ++t) add(top_t[1][(size_t)t * W + w * ncta + c]);
-          for (int t = sp->ntop - 1; t >= 0; --t) add(top_t[0][(size_t)t * W + w * ncta + c]);
-        }
+        for (int t = 0; t < sp->ntop; ++t) add(top_t[1][(size_t)t * W + w * ncta + c]);  // band forward
+        if (sp->dense) add(dense_t[w * ncta + c]);
+        for (int t = sp->ntop - 1; t >= 0; --t) add(top_t[0][(size_t)t * W + w * ncta + c]);  // band backward
         for (int h = sp->nsub - 1; h >= 0; --h) add(sub_t[0][((size_t)c * sp->nsub + h) * warps + w]);
         bnd.push_back((int)(all.size() - o));
         maxw = std::max(maxw, (int)(all.size() - o));
@@ -493,15 +532,15 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     off.push_back((int)all.size());
     if (all.empty()) all.push_back(SweepTask{});
     sp->max_wtasks = maxw;
-    if (getenv("STMHD_SWEEP_TRACE")) {
+    if (getenv("STMHD_SWEEP_TRACE") || getenv("STMHD_SWEEP_PLAN_INFO")) {
       std::vector<int64_t> fsum(ncta, 0), nbsum(ncta, 0);
       for (int sn = 0; sn < p.nsn; ++sn)
         if (owner[sn] >= 0) {
           fsum[owner[sn]] += p.ns[sn] + p.nb[sn];
           nbsum[owner[sn]] += p.nb[sn];
         }
-      fprintf(stderr, "[sweep-plan] n=%lld D=%d ntop=%d nsub=%d max_wtasks=%d max sub front entries %lld (nb %lld)\n",
-              (long long)p.n, D, sp->ntop, sp->nsub, maxw, (long long)*std::max_element(fsum.begin(), fsum.end()),
+      fprintf(stderr, "[sweep-plan] n=%lld D=%d band=%d dense=%d (K levels %d, nT %d) nsub=%d max_wtasks=%d max sub front entries %lld (nb %lld)\n",
+              (long long)p.n, D, sp->ntop, sp->dense, kl, sp->ntT, sp->nsub, maxw, (long long)*std::max_element(fsum.begin(), fsum.end()),
               (long long)*std::max_element(nbsum.begin(), nbsum.end()));
     }
     // shared memory: subtree vectors + per-warp task lists must fit next to the
@@ -510,7 +549,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     // gather buffer: in dense mode only subtree fronts are gathered
     int fmax = 1;
     for (int sn = 0; sn < p.nsn; ++sn)
-      if (!sp->dense || owner[sn] >= 0) fmax = std::max(fmax, p.ns[sn] + p.nb[sn]);
+      if (!isK[sn]) fmax = std::max(fmax, p.ns[sn] + p.nb[sn]);
     sp->vstride = (int)((fmax + 15) / 16 * 16 + 2 * slot_sz);
     const int64_t need = (int64_t)warps * sp->vstride + 3 * maxlen + maxcb + tdoubles + sp->kpad + sp->tab_ints / 2 + 4;
     if (!flat && D > 0 && need > smem_budget) {
@@ -530,7 +569,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     std::vector<int4> tch;
     int64_t tcb = 0;
     for (int sn = 0; sn < p.nsn; ++sn) {
-      if (owner[sn] >= 0) continue;
+      if (!isK[sn]) continue;
       require(p.fl_off[sn] < INT32_MAX && p.fu_off[sn] < INT32_MAX && p.idx_off[sn] < INT32_MAX,
               "nd sweep: factor too large for the dense-top construction");
       TopSN t{};
@@ -549,7 +588,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
       t.child0 = (int)tch.size();
       for (int ci = p.child_ptr[sn]; ci < p.child_ptr[sn + 1]; ++ci) {
         const int c = p.child_list[ci];
-        if (owner[c] >= 0) continue;  // subtree roots: their updates are inputs (z_T)
+        if (!isK[c]) continue;  // band nodes / subtree roots: their updates are inputs (z_T)
         require(tsn_index[c] >= 0, "nd sweep: top tree not in postorder");
         tch.push_back(make_int4(tsn_index[c], (int)p.emap_off[c], p.nb[c], 0));
       }
@@ -1354,7 +1393,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     if (a.dense && a.kpref && lane == 0 && !a.null_work) {
       // the dense-top K rows of this warp for slab k, into L2 one slab phase ahead of
       // their use (the ring then streams them from L2)
-      for (int ti = w.bnd[a.nsub]; ti < w.bnd[a.nsub + 1]; ++ti) {
+      for (int ti = w.bnd[a.nsub + a.ntop]; ti < w.bnd[a.nsub + a.ntop + 1]; ++ti) {
         const SweepTask &t = w.tl[ti];
         const double *src = a.ktop + (int64_t)k * a.kstride + t.foff;
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"((unsigned)(t.c1 * t.bsz * 8))
@@ -1412,9 +1451,16 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       tb = pclock<PROF>(); sweep_barrier(a, crank, gphase); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step, crank);
     }
+    // band forward levels (cluster/grid-wide tree levels below the K region)
+    for (int t = 0; t < a.ntop; ++t, ++L) {
+      const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
+      for (int ti = w.bnd[L]; ti < t1; ++ti) forward_task<false, PROF>(a, w.tl[ti], F, rhs, sv, w, mbar);
+      tb = pclock<PROF>(); sweep_barrier(a, crank, gphase); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+      sweep_trace(a, step, crank);
+    }
     if (a.dense) {
-      // z_T = coupled rhs of the top unknowns + the subtree roots' updates (all CTAs
-      // gather the whole vector), then x_T = K z_T as row tasks
+      // z_T = coupled rhs of the K unknowns + the updates of the K region's children
+      // (all CTAs gather the whole vector), then x_T = K z_T as row tasks
       if (PROF) tl_mark(w, 5);
       const double *rt = a.prog_hdr ? a.tbuf : rhs;
       for (int i = threadIdx.x; i < a.kpad; i += blockDim.x) {
@@ -1441,23 +1487,17 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
         __syncthreads();
       }
       sweep_trace(a, step, crank);
-    } else {
-      for (int t = 0; t < a.ntop; ++t, ++L) {
-        const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
-        for (int ti = w.bnd[L]; ti < t1; ++ti) forward_task<false, PROF>(a, w.tl[ti], F, rhs, sv, w, mbar);
-        tb = pclock<PROF>(); sweep_barrier(a, crank, gphase); if (PROF) w.acc[3] += pclock<PROF>() - tb;
-        sweep_trace(a, step, crank);
+    }
+    // band backward levels
+    for (int t = a.ntop - 1; t >= 0; --t, ++L) {
+      const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
+      for (int ti = w.bnd[L]; ti < t1; ++ti) backward_task<false, PROF>(a, w.tl[ti], F, x, sv, w, mbar);
+      if (t > 0 || a.nsub || k + 1 < a.nslab) {
+        tb = pclock<PROF>();
+        sweep_barrier(a, crank, gphase);
+        if (PROF) w.acc[3] += pclock<PROF>() - tb;
       }
-      for (int t = a.ntop - 1; t >= 0; --t, ++L) {
-        const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
-        for (int ti = w.bnd[L]; ti < t1; ++ti) backward_task<false, PROF>(a, w.tl[ti], F, x, sv, w, mbar);
-        if (t > 0 || a.nsub || k + 1 < a.nslab) {
-          tb = pclock<PROF>();
-          sweep_barrier(a, crank, gphase);
-          if (PROF) w.acc[3] += pclock<PROF>() - tb;
-        }
-        sweep_trace(a, step, crank);
-      }
+      sweep_trace(a, step, crank);
     }
     for (int h = a.nsub - 1; h >= 0; --h, ++L) {
       const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
@@ -2348,7 +2388,7 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
     STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
     const bool fz = a.prog_hdr != nullptr;
     auto entries = [&](int k) {
-      return (int)fz + ((a.nsub || fz) ? 1 : 0) + (a.dense ? 2 : 2 * a.ntop) + (a.nsub && k + 1 < a.nslab);
+      return (int)fz + ((a.nsub || fz) ? 1 : 0) + (a.dense ? 2 : 0) + 2 * a.ntop + (a.nsub && k + 1 < a.nslab);
     };
     const int per = entries(1), base = 1 + entries(0);
     fprintf(stderr, "[sweep] n=%lld levels=%d top=%d sub=%d fused=%d stages=%d total=%.1f us | slab1 (us):",
