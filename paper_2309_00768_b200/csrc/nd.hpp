@@ -109,6 +109,12 @@ struct NDSweepPlan {
   // K is stored in row groups of kr rows: block (group g, column chunk c) holds kr x kc
   // entries column-major ([kc][kr]), so one ring item feeds kr rows (kr = 1: plain rows).
   int dense = 0, ntT = 0, kc = 0, nch = 0, kpad = 0, kr = 1;
+  // the row groups of K are spread over the CTAs (group g on CTA g % ncta, local index
+  // g / ncta) and each group's nch column chunks over that CTA's warps in dpieces
+  // pieces; the partial dot products meet in shared memory (dred, dgroups x dpieces x kr
+  // doubles per CTA) and are summed in a fixed order, so the result is deterministic
+  int dpieces = 1, dgroups = 0;
+  int zlen() const { return kpad + dgroups * dpieces * kr; }  // shared doubles: z_T + partials
   int64_t kstride() const { return (int64_t)((ntT + kr - 1) / kr * kr) * kpad; }
   DevBuf ztab;              // int4 x 2 per top unknown {pos, cb0, cb1, cb2}, {cb3, -1, -1, -1}
   DevBuf tidx;              // n: top index of a permuted position, or -1

@@ -283,7 +283,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   // whole top is dense (no band).  The largest kl whose K fits the size rule wins.
   static const int dense_env = env_int2("STMHD_SWEEP_DENSE_TOP", 1);
   static const int klev_env = env_int2("STMHD_SWEEP_KLEVELS", -1);  // force kl (0: no dense top)
-  static const int kmax_env = env_int2("STMHD_SWEEP_KMAX", 1100);   // largest K order with a band
+  static const int kmax_env = env_int2("STMHD_SWEEP_KMAX", 1600);   // largest K order with a band
   std::vector<char> isK(p.nsn, 0);
   int kl = 0;
   std::vector<int> tpos, tidx_h(p.n, -1);
@@ -488,24 +488,46 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   // per physical warp (cta c, warp w; top-phase global warp id w * ncta + c): its
   // list in kernel order and the bound of every phase level
   // dense top: one phase level of row tasks (row i of K: nch column chunks of kc)
-  std::vector<std::vector<SweepTask>> dense_t(W);
+  std::vector<std::vector<SweepTask>> dense_t(W);  // by global warp w * ncta + c
   if (sp->dense) {
     const int ng = (sp->ntT + sp->kr - 1) / sp->kr;
-    for (int g = 0; g < ng; ++g) {
-      SweepTask t{};
-      t.foff = g * sp->kr * sp->kpad;
-      t.goff = 0;
-      t.first = g * sp->kr;  // first row of the group (top index; positions via ztab)
-      t.cboff = 0;
-      t.c0 = 0;
-      t.c1 = (short)sp->nch;
-      t.ns = (short)sp->kc;
-      t.f = (short)sp->kc;
-      t.rows = (short)sp->kr;
-      t.R = (unsigned char)sp->kr;
-      t.flags = 2;
-      t.bsz = sp->kr * sp->kc;
-      dense_t[g % W].push_back(t);
+    static const int dsplit_env = env_int2("STMHD_SWEEP_DENSE_SPLIT", 1);
+    int npc = dsplit_env ? std::max(1, std::min(sp->nch, (W + ng - 1) / ng)) : 1;
+    const int pc = (sp->nch + npc - 1) / npc;  // chunks per piece
+    npc = (sp->nch + pc - 1) / pc;
+    sp->dpieces = npc;
+    sp->dgroups = (ng + ncta - 1) / ncta;
+    for (int c = 0; c < ncta; ++c) {
+      std::vector<std::pair<int, SweepTask>> items;  // (chunks, task)
+      for (int g = c, j = 0; g < ng; g += ncta, ++j)
+        for (int q = 0; q < npc; ++q) {
+          const int c0 = q * pc, c1 = std::min(sp->nch, (q + 1) * pc);
+          if (c1 <= c0) continue;
+          SweepTask t{};
+          t.foff = g * sp->kr * sp->kpad;
+          t.goff = 0;
+          t.first = g * sp->kr;  // first row of the group (top index; positions via ztab)
+          t.cboff = j * npc + q;  // partial-sum slot in the CTA's dred
+          t.c0 = (short)c0;
+          t.c1 = (short)c1;
+          t.ns = (short)sp->kc;
+          t.f = (short)sp->kc;
+          t.rows = (short)sp->kr;
+          t.R = (unsigned char)sp->kr;
+          t.flags = 2;
+          t.bsz = sp->kr * sp->kc;
+          items.push_back({c1 - c0, t});
+        }
+      std::stable_sort(items.begin(), items.end(), [](const auto &a, const auto &b) { return a.first > b.first; });
+      std::vector<int> load(warps, 0);
+      for (auto &it : items) {
+        const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        dense_t[(size_t)w * ncta + c].push_back(it.second);
+        load[w] += it.first;
+      }
+      if (c == 0 && getenv("STMHD_SWEEP_PLAN_INFO"))
+        fprintf(stderr, "[sweep-plan] dense: nT %d kc %d nch %d groups %d pieces %d x %d chunks, CTA 0: %zu items, max chunks per warp %d\n",
+                sp->ntT, sp->kc, sp->nch, ng, npc, pc, items.size(), *std::max_element(load.begin(), load.end()));
     }
   }
   sp->nl = 2 * sp->nsub + 2 * sp->ntop + (sp->dense ? 1 : 0);
@@ -551,7 +573,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     for (int sn = 0; sn < p.nsn; ++sn)
       if (!isK[sn]) fmax = std::max(fmax, p.ns[sn] + p.nb[sn]);
     sp->vstride = (int)((fmax + 15) / 16 * 16 + 2 * slot_sz);
-    const int64_t need = (int64_t)warps * sp->vstride + 3 * maxlen + maxcb + tdoubles + sp->kpad + sp->tab_ints / 2 + 4;
+    const int64_t need = (int64_t)warps * sp->vstride + 3 * maxlen + maxcb + tdoubles + sp->zlen() + sp->tab_ints / 2 + 4;
     if (!flat && D > 0 && need > smem_budget) {
       const int next = sp->tab_ints ? 1 : (sp->dense ? 2 : 3);
       return get_sweep_plan(ncta, warps, smem_budget, s, next);
@@ -641,7 +663,8 @@ struct SweepArgs {
   const int *tab, *tab_ptr, *tab_nf;
   int tab_ints;
   // dense top (NDSweepPlan::dense): z_T gather table and K = (A^{-1})_TT per slab
-  int dense, ntT, kpad;
+  int dense, ntT, kpad, zlen;  // zlen: shared doubles of z_T + the dense partial sums
+  int dpieces, dgroups, kr;
   const int4 *ztab;
   const double *ktop;
   int64_t kstride;             // doubles per slab of ktop (0: one K for all slabs)
@@ -1100,12 +1123,10 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
 // rows, streamed as nch column chunks ([kc][R] blocks) through the warp's TMA ring
 // (lane = kq * R + r covers columns kq + (32 / R) q of row r).
 template <bool PROF>
-__device__ __forceinline__ void dense_task(const SweepArgs &a, const SweepTask &tk, const double *zs, double *x,
-                                           int k, WarpCtx &w, unsigned long long (*mbar)[2]) {
+__device__ __forceinline__ void dense_task(const SweepArgs &a, const SweepTask &tk, const double *zs, double *dred,
+                                           WarpCtx &w, unsigned long long (*mbar)[2]) {
   const int lane = w.lane;
   const int R = tk.R, kl = 32 / R;
-  // output positions first: the load overlaps the chunk stream instead of the store
-  const int pos = (lane < R && tk.first + lane < a.ntT) ? a.ztab[2 * (tk.first + lane)].x : -1;
   double acc = 0.0;
   for (int c = tk.c0; c < tk.c1; ++c) {
     const int sl = w.jc & 1;
@@ -1120,7 +1141,7 @@ __device__ __forceinline__ void dense_task(const SweepArgs &a, const SweepTask &
     w.acc[4] += 1;
     w.acc[5] += tk.c1 - tk.c0;
   }
-  if (pos >= 0) x[pos] = acc;
+  if (lane < R) dred[tk.cboff * R + lane] = acc;  // partial of rows first + lane over the piece's columns
 }
 
 // Run this CTA's items of a coupling program.  MODE 0 (slab start): rhs rows, item
@@ -1337,7 +1358,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   sv.ftab = nullptr;
   sv.btab = nullptr;
   if (a.tab_ints) {  // this CTA's subtree front tables, resident for the whole launch
-    int *tb = reinterpret_cast<int *>((reinterpret_cast<uintptr_t>(sv.zs + a.kpad) + 15) & ~(uintptr_t)15);
+    int *tb = reinterpret_cast<int *>((reinterpret_cast<uintptr_t>(sv.zs + a.zlen) + 15) & ~(uintptr_t)15);
     const int o = a.tab_ptr[crank], nt = a.tab_ptr[crank + 1] - o;
     for (int i = threadIdx.x; i < nt; i += blockDim.x) tb[i] = a.tab[o + i];
     sv.ftab = tb;
@@ -1352,7 +1373,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     // the whole sweep: no global round trip per level or task afterwards)
     const int gid = crank * a.warps + wl;
     const uintptr_t base =
-        (reinterpret_cast<uintptr_t>(sv.zs + a.kpad) + 15 + (size_t)a.tab_ints * 4) & ~(uintptr_t)15;
+        (reinterpret_cast<uintptr_t>(sv.zs + a.zlen) + 15 + (size_t)a.tab_ints * 4) & ~(uintptr_t)15;
     char *area = reinterpret_cast<char *>(base) + (size_t)wl * a.tstride;
     int *bnd = reinterpret_cast<int *>(area);
     SweepTask *tl = reinterpret_cast<SweepTask *>(area + ((a.nl + 1 + 3) / 4) * 16);
@@ -1463,24 +1484,46 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       // (all CTAs gather the whole vector), then x_T = K z_T as row tasks
       if (PROF) tl_mark(w, 5);
       const double *rt = a.prog_hdr ? a.tbuf : rhs;
-      for (int i = threadIdx.x; i < a.kpad; i += blockDim.x) {
-        double z = 0.0;
-        if (i < a.ntT) {
-          const int4 t0 = a.ztab[2 * i], t1 = a.ztab[2 * i + 1];
-          const double r0 = rt[t0.x];
-          const double c0 = t0.y >= 0 ? a.cbv[t0.y] : 0.0, c1 = t0.z >= 0 ? a.cbv[t0.z] : 0.0;
-          const double c2 = t0.w >= 0 ? a.cbv[t0.w] : 0.0, c3 = t1.x >= 0 ? a.cbv[t1.x] : 0.0;
-          z = r0 + ((c0 + c1) + (c2 + c3));
+      for (int i0 = threadIdx.x; i0 < a.kpad; i0 += 4 * blockDim.x) {
+        int4 t0[4], t1[4];  // four entries per thread: every table load, then every value load in flight
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = i0 + q * blockDim.x;
+          t0[q] = i < a.ntT ? a.ztab[2 * i] : make_int4(-1, -1, -1, -1);
+          t1[q] = i < a.ntT ? a.ztab[2 * i + 1] : make_int4(-1, -1, -1, -1);
         }
-        sv.zs[i] = z;
+        double z[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double r0 = t0[q].x >= 0 ? rt[t0[q].x] : 0.0;
+          const double c0 = t0[q].y >= 0 ? a.cbv[t0[q].y] : 0.0, c1 = t0[q].z >= 0 ? a.cbv[t0[q].z] : 0.0;
+          const double c2 = t0[q].w >= 0 ? a.cbv[t0[q].w] : 0.0, c3 = t1[q].x >= 0 ? a.cbv[t1[q].x] : 0.0;
+          z[q] = r0 + ((c0 + c1) + (c2 + c3));
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (i0 + q * (int)blockDim.x < a.kpad) sv.zs[i0 + q * blockDim.x] = z[q];
       }
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step, crank);
       const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
       if (PROF) tl_mark(w, 1);
-      for (int ti = w.bnd[L]; ti < t1; ++ti) dense_task<PROF>(a, w.tl[ti], sv.zs, x, k, w, mbar);
+      double *dred = sv.zs + a.kpad;
+      for (int ti = w.bnd[L]; ti < t1; ++ti) dense_task<PROF>(a, w.tl[ti], sv.zs, dred, w, mbar);
       if (PROF) tl_mark(w, 4);
       ++L;
+      __syncthreads();
+      // x_T rows of this CTA's groups: the pieces' partials summed in a fixed order
+      for (int t = threadIdx.x; t < a.dgroups * a.kr; t += blockDim.x) {
+        const int j = t / a.kr, r = t - j * a.kr;
+        const int row = (crank + a.ncta * j) * a.kr + r;
+        if (row < a.ntT) {
+          const double *pr = dred + (int64_t)j * a.dpieces * a.kr + r;
+          double sum = pr[0];
+          for (int q = 1; q < a.dpieces; ++q) sum += pr[q * a.kr];
+          x[a.ztab[2 * row].x] = sum;
+        }
+      }
       tb = pclock<PROF>(); sweep_barrier(a, crank, gphase); if (PROF) w.acc[3] += pclock<PROF>() - tb;  // x_T visible
       if (a.tab_ints) {  // stage x_T in shared memory for the subtree backward tables
         for (int i = threadIdx.x; i < a.ntT; i += blockDim.x) sv.zs[i] = x[a.ztab[2 * i].x];
@@ -1970,7 +2013,7 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   // slabs such as configuration 5); the choice sticks to the stage
   auto smem_of = [&](const NDSweepPlan &c, int w) {
     const size_t tstr = ((c.nl + 1 + 3) / 4) * 16 + (size_t)c.max_wtasks * sizeof(SweepTask);
-    return ((size_t)w * c.vstride + 3 * c.sub_len + c.sub_cb + c.kpad + 4) * sizeof(double) + (size_t)c.tab_ints * 4 +
+    return ((size_t)w * c.vstride + 3 * c.sub_len + c.sub_cb + c.zlen() + 4) * sizeof(double) + (size_t)c.tab_ints * 4 +
            (size_t)w * tstr;
   };
   // prefer the most warps whose plan keeps the CTA-local subtree phase (fewer
@@ -2078,6 +2121,10 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   a.dense = sp.dense;
   a.ntT = sp.ntT;
   a.kpad = sp.kpad;
+  a.zlen = sp.zlen();
+  a.dpieces = sp.dpieces;
+  a.dgroups = sp.dgroups;
+  a.kr = sp.kr;
   if (sp.dense) {
     if (fac.ktop_plan != &sp || fac.ktop_gen != fac.gen) build_dense_top(fac, sp, s);
     a.ztab = sp.ztab.as<int4>();
@@ -2098,7 +2145,7 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
     }
     a.gbar = st.gbar.as<unsigned>();
   }
-  st.smem = ((size_t)warps * a.vstride + 3 * a.sub_len + a.sub_cb + a.kpad + 4) * sizeof(double) +
+  st.smem = ((size_t)warps * a.vstride + 3 * a.sub_len + a.sub_cb + a.zlen + 4) * sizeof(double) +
             (size_t)a.tab_ints * 4 + (size_t)warps * a.tstride;
   require(st.smem <= (size_t)kSmemMax, "nd sweep: subtree vectors or fronts too large for shared memory");
   // consumers wait on their producers' flags (set at launch)

@@ -1,10 +1,12 @@
-"""Velocity sweep / P_T^-1 time and agreement for several dense-top depths.
+"""Velocity sweep / P_T^-1 time and agreement for several sweep settings.
 
 Each setting runs in a child process (the STMHD_* switches are read once per
-process).  Prints per setting: solve_velocity ms, apply_inverse ms, and the
-relative difference of both results to the all-tree-levels run (KLEVELS=0).
+process).  A setting is a dense-top depth (STMHD_SWEEP_KLEVELS) or a comma list
+of NAME=VALUE switches.  Prints per setting: solve_velocity ms, apply_inverse ms,
+setup s, and the relative difference of both results to the first setting.
 
   python tools/klevels_probe.py C3 0 2 3 4 -1
+  python tools/klevels_probe.py C3 -1 STMHD_SWEEP_LDGSTS=1 STMHD_SWEEP_WARPS=16,STMHD_CHUNK_MAX=512
 """
 import json
 import os
@@ -54,9 +56,14 @@ def main():
 
     for s in settings:
         env = dict(os.environ)
-        env["STMHD_SWEEP_KLEVELS"] = s
+        if "=" in s:
+            for kv in s.split(","):
+                k, v = kv.split("=")
+                env[k] = v
+        else:
+            env["STMHD_SWEEP_KLEVELS"] = s
         env["STMHD_SWEEP_PLAN_INFO"] = "1"
-        tag = f"gpurun_out/klev_{cfg}_{s}"
+        tag = f"gpurun_out/klev_{cfg}_{abs(hash(s))}"
         r = subprocess.run([sys.executable, "-c", CHILD, cfg, tag], env=env, capture_output=True, text=True)
         line = [ln for ln in r.stdout.splitlines() if ln.startswith("RESULT ")]
         if r.returncode or not line:
