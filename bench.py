@@ -1,23 +1,34 @@
 #!/usr/bin/env python
-"""Benchmark: space-time Newton--FGMRES solve of BASELINE config C2 on B200.
+"""Benchmark: space-time Newton--FGMRES solve of BASELINE config C4 at Nt=512 on B200.
 
 Metric (BASELINE.json): preconditioned FGMRES iterations per second over a full
-Newton solve (FP64), plus the Newton solve time.  One "step" = one complete
-all-at-once solve of configuration C2 (island coalescence, 32x32 P2/P1,
-dt=0.05, Nt=64; Newton to relative residual 1e-6, FGMRES(50) rel 1e-8, P_T
-preconditioner) from the equilibrium-projection initial state.
+Newton solve (FP64), plus the Newton solve time.  The N=1 workload is the largest
+single-GPU Newton--FGMRES configuration of BASELINE.json: C4 at Nt=512
+-- island coalescence on a 64x64 P2/P1 mesh, T=1, dt=1/512 (23.5 M unknowns),
+Newton to relative residual 1e-6, FGMRES(50) rel 1e-8, P_T preconditioner, from the
+equilibrium-projection initial state.  One "step" = one complete solve.
+
+Every timed step copies the initial state from pinned host memory to the device,
+solves, and reads the solution back; CUDA events split the step into the copy-in,
+the device-resident solve (`value`) and the copy-out (`e2e` = the whole step).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N>1 (torchrun, one rank per GPU): the space-time sweeps do not shard
-(SURVEY 8(e)), so every rank solves an independent replica; value = all
-ranks' iterations / max-over-ranks device time ("scaling": "weak").
+N>1 (torchrun, one rank per GPU): the space-time sweeps do not shard (SURVEY
+8(e)), so every rank solves an independent replica; value = all ranks'
+iterations / max-over-ranks device time ("scaling": "weak").
 
-`--impl reference` times the reference algorithm on the host CPU through the
-oracle port (oracle/, the reference is pure Python): a bounded sample (C2 mesh,
-first 8 slabs, one Newton linearisation + one 50-iteration FGMRES cycle) per
-step, extrapolated linearly in the slab count to the full C2 solve with the
-reference's own iteration counts (458 + 413).
+After the timed region (rank 0, N=1) the line adds: rooflines of the P_T^-1 apply
+(the dominant kernel, nd_sweep_kernel), J.v and assembly at C4_512; the other
+BASELINE configurations (C2 full solve, C4 at Nt=64/128/256, the C5 operator
+micro-benchmark in a child process); and `cpu_baseline` -- the oracle port (the
+reference algorithm: SuperLU P_T, sparsetools SpMV, MGS GMRES) pinned to one host
+core on a bounded slab-prefix sample, extrapolated (labelled) to the full solve.
+
+`--impl reference` times that CPU implementation alone (the reference is pure
+Python and does not exist on the GPU box; the oracle port pinned to it by golden
+vectors stands in for it): each step one bounded sample, per-op costs scaled to
+the full C4_512 solve with the reference iteration counts.
 """
 
 from __future__ import annotations
@@ -34,11 +45,19 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIG = "C2"
-# Reference iteration counts for C2 (Newton steps 1,2); the oracle and the GPU
-# path both reproduce them (tests).
-REF_GMRES = [458, 413]
-SAMPLE_SLABS, SAMPLE_ITERS = 8, 50
+CONFIG = "C4_512"
+NT_FULL = 512
+# FGMRES counts of this configuration (Newton steps 1, 2), measured on the B200 and
+# used by the reference arm's extrapolation; the unmodified reference gives the same
+# counts at C4_64 ([96, 89], tests/golden/cfg_c4_64.npz) and C2 ([458, 413]).
+REF_GMRES = [108, 98]
+# CPU samples: first SAMPLE_SLABS slabs of the configuration, one Newton linearisation
+# and SAMPLE_ITERS FGMRES(50) iterations
+SAMPLE_SLABS, SAMPLE_ITERS = 4, 40
+REF_SLABS, REF_ITERS = 2, 20  # --impl reference: per step (K + W steps must fit minutes)
+WORKLOAD = ("C4 island coalescence 64x64 P2/P1, T=1, dt=1/512, Nt=512 (23.5 M unknowns), "
+            "Newton rel 1e-6, FGMRES(50) rel 1e-8, P_T")
+METRIC = "FGMRES iterations/s (C4 Nt=512 Newton solve, P_T preconditioner, FP64)"
 
 
 def parse():
@@ -48,7 +67,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-c3-kernels", action="store_true", help="skip the C3 J.v / assembly roofline entries")
+    ap.add_argument("--no-extras", action="store_true", help="skip the other configurations")
+    ap.add_argument("--c5-child", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -105,16 +125,21 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_sample(threads_one=True):
-    """One bounded oracle sample in a subprocess (so thread env vars apply)."""
+def cpu_sample(config=CONFIG, slabs=SAMPLE_SLABS, iters=SAMPLE_ITERS):
+    """One bounded oracle sample in a subprocess pinned to one core (BASELINE.md 3:
+    the reference is single-threaded by construction -- SuperLU, sparsetools, Python
+    loops -- so one core with OMP/OPENBLAS=1)."""
     env = dict(os.environ)
     env["PYTHONPATH"] = ROOT + os.pathsep + env.get("PYTHONPATH", "")
-    cmd = [sys.executable, "-m", "oracle.cpu_sample", "--config", CONFIG, "--slabs", str(SAMPLE_SLABS),
-           "--iters", str(SAMPLE_ITERS)]
-    if threads_one:
-        env.update(OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
-        if shutil_which("taskset"):
-            cmd = ["taskset", "-c", "0"] + cmd
+    env.update(OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    cmd = [sys.executable, "-m", "oracle.cpu_sample", "--config", config, "--slabs", str(slabs),
+           "--iters", str(iters)]
+    if shutil_which("taskset"):
+        try:
+            core = sorted(os.sched_getaffinity(0))[0]
+        except (AttributeError, OSError):
+            core = 0
+        cmd = ["taskset", "-c", str(core)] + cmd
     out = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=900)
     if out.returncode != 0:
         raise RuntimeError("cpu sample failed: " + out.stderr[-2000:])
@@ -127,8 +152,23 @@ def shutil_which(name):
     return shutil.which(name)
 
 
+def host_info():
+    cpu = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu": cpu, "nproc": os.cpu_count()}
+
+
 def extrapolate(sample, nt_full, gmres_iters):
-    """Full-solve CPU time from a slab-prefix sample (linear in the slab count)."""
+    """Full-solve CPU seconds from a slab-prefix sample.  Every per-slab cost of the
+    reference is linear in the slab count (causal block structure: residual, Jacobian,
+    P_T setup, J.v, P_T^-1 and the MGS basis all loop over slabs), so the per-op times
+    scale by nt_full / slabs; Newton does (newton + 1) residuals."""
     scale = nt_full / sample["slabs"]
     newton = len(gmres_iters)
     t = scale * ((newton + 1) * sample["t_residual"] + newton * (sample["t_jacobian"] + sample["t_pc_setup"])
@@ -136,96 +176,248 @@ def extrapolate(sample, nt_full, gmres_iters):
     return t, sum(gmres_iters) / t
 
 
+def sample_text(smp, nt_full, counts, t_full):
+    return (f"oracle port of the reference algorithm (SuperLU P_T, sparsetools SpMV, MGS GMRES; pinned "
+            f"to one core) on the {CONFIG} mesh restricted to its first {smp['slabs']} of {nt_full} slabs: "
+            f"residual + Jacobian + P_T setup + {smp['iters']} FGMRES(50) iterations "
+            f"({smp['t_iter'] * 1e3:.0f} ms each); per-op times x{nt_full // smp['slabs']} with the counts "
+            f"{counts} -> {t_full:.0f} s per solve (EXTRAPOLATED)")
+
+
 # ---------------------------------------------------------------------------------
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    import numpy  # noqa: F401  (threads: all the host threads it can use)
-
-    times = []
-    sample = None
+    times, samples = [], []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        sample = cpu_sample(threads_one=False)
+        smp = cpu_sample(CONFIG, REF_SLABS, REF_ITERS)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
-            times.append((dt, sample))
-    samples = [s for _, s in times]
-    t_iter = statistics.median(s["t_iter"] for s in samples)
+            times.append(dt)
+            samples.append(smp)
     agg = dict(samples[-1])
-    agg["t_iter"] = t_iter
-    for k in ("t_residual", "t_jacobian", "t_pc_setup"):
+    for k in ("t_residual", "t_jacobian", "t_pc_setup", "t_iter"):
         agg[k] = statistics.median(s[k] for s in samples)
-    t_full, value = extrapolate(agg, 64, REF_GMRES)
-    cores = os.cpu_count()
+    t_full, value = extrapolate(agg, NT_FULL, REF_GMRES)
     line = {
-        "impl": "reference",
-        "metric": "FGMRES iterations/s (C2 Newton solve, P_T preconditioner, FP64)",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "FGMRES it/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * statistics.mean(t for t, _ in times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE C2 analytic problem)",
-        "config": {"workload": "C2 island coalescence 32x32 P2/P1, dt=0.05, Nt=64, Newton rel 1e-6, FGMRES(50) rel 1e-8",
-                   "l2": "n/a (CPU)"},
+        "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE C4 analytic problem)",
+        "config": {"workload": WORKLOAD, "l2": "n/a (CPU)"},
         "newton_solve_s_extrapolated": t_full,
-        "cpu_baseline": {"value": value, "unit": "FGMRES it/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle port (reference algorithm: SuperLU P_T, MGS GMRES) on C2 mesh, first "
-                                   f"{SAMPLE_SLABS} of 64 slabs: 1 residual+Jacobian+P_T setup and "
-                                   f"{SAMPLE_ITERS} FGMRES iterations per step; extrapolated x{64 // SAMPLE_SLABS} "
-                                   f"to the full solve with the reference counts {REF_GMRES}"},
+        "cpu_baseline": {"value": value, "unit": "FGMRES it/s", "cores": 1, "kind": "port",
+                         "sample": sample_text(agg, NT_FULL, REF_GMRES, t_full) + "; one sample per step",
+                         "host": host_info()},
         "e2e": {"value": value, "unit": "FGMRES it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------------
-def run_ours(args, rank, world):
-    import numpy as np
+def splu_fill(m):
+    """L+U nnz of the reference's SuperLU factorisation (scipy splu, COLAMD)."""
+    import scipy.sparse as sp
     import scipy.sparse.linalg as spla
+
+    lu = spla.splu(sp.csc_matrix(m))
+    return int(lu.L.nnz + lu.U.nnz)
+
+
+def pt_algorithmic_bytes(p, disc, state, torch, dev):
+    """SURVEY 8(d) P_T^-1 bytes: Nt 8 [fill(F_u) + fill(C_A) + nnz(f_a, f_p, z_j, z_a, sub1)]
+    + 12 [fill(M_A, M_j, K_p, M_p) + nnz(M_A/dt, K_jA, M_p, sub2, B^T, M_u/dt)] + 16 N, with
+    the reference SuperLU (COLAMD) fills of slab 0 at a perturbed state (structural fill)."""
+    stp = p.SpaceTimeState(state.vec.copy(), state.ic_u, state.ic_a)
+    stp.vec.data += 1e-3 * torch.randn(stp.vec.data.shape, dtype=torch.float64, device=dev,
+                                       generator=torch.Generator(device=dev).manual_seed(0))
+    jac = p.assemble_jacobian(stp, disc)
+    pc = p.SpaceTimePreconditioner(jac, disc, stp)
+    s0 = jac.slabs[0]
+    nt, L = disc.n_steps, disc.layout
+    per_slab = (splu_fill(s0.f_u) + splu_fill(pc.c_a[0]) + s0.f_a.nnz + pc.f_p[0].nnz + s0.z_j.nnz + s0.z_a.nnz
+                + pc.c_a_sub1[0].nnz)
+    const = (splu_fill(disc.mass_a_bc) + splu_fill(disc.mass_j) + splu_fill(disc.stiff_p_pinned)
+             + splu_fill(disc.mass_p) + disc.mass_a_dt_bc.nnz + disc.mixed_ja_bc.nnz + disc.mass_p.nnz
+             + pc.c_a_sub2.nnz + disc.div_t_bc.nnz + disc.mass_u_dt_bc.nnz)
+    del pc, jac
+    return nt * 8 * per_slab + 12 * const + 16 * nt * L.slab_size
+
+
+def tmeas(torch, fn, r=10):
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(r):
+        fn()
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / r
+
+
+def newton_cfg(p, rel):
+    return p.NewtonConfig(abs_tol=1e-300, rel_tol=rel, max_iters=1 if rel is None else 25,
+                          gmres=p.GmresConfig(rel_tol=1e-8, abs_tol=1e-300, max_iters=100000, restart=50))
+
+
+def other_configs(p, torch, dev, peak):
+    """The other BASELINE configurations (not bench lines): C2 full solve, C4 at
+    Nt=64/128/256 (one solve each, device-timed), C3 per-call operator times."""
+    out = {}
+    for name in ("C2", "C4_64", "C4_128", "C4_256"):
+        d = p.discretize_config(name)
+        _, _, _, nt, rel = p.config_problem(name)
+        cfg = newton_cfg(p, rel)
+        p.solve_all_at_once(d, cfg)  # warm-up (plans, dense tops, pools)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _, st = p.solve_all_at_once(d, cfg)
+        e1.record()
+        e1.synchronize()
+        s = e0.elapsed_time(e1) / 1e3
+        out[name] = {"solve_s": s, "newton": st.newton_iters, "fgmres": st.gmres_iters,
+                     "fgmres_it_per_s": st.total_gmres / s,
+                     "relative_residual": st.residual_norms[-1] / st.residual_norms[0]}
+        del d
+        torch.cuda.empty_cache()
+    out["C2"]["reference_counts"] = [458, 413]
+    out["C4_64"]["reference_counts"] = [96, 89]
+    # C3: tearing 64^2, mu=eta=1e-3, Nt=128 -- stagnates in the reference algorithm itself
+    # (DESIGN 7), so per-call operator times only
+    d3 = p.discretize_config("C3")
+    s3 = p.initial_state(d3)
+    j3 = p.assemble_jacobian(s3, d3)
+    pc3 = p.SpaceTimePreconditioner(j3, d3, s3)
+    v3 = torch.randn(j3.size, dtype=torch.float64, device=dev)
+    o3 = torch.empty_like(v3)
+    out["C3"] = {"J_apply_ms": tmeas(torch, lambda: j3._into(v3, o3), 30),
+                 "P_apply_ms": tmeas(torch, lambda: pc3._into(v3, o3), 5),
+                 "assembly_ms": tmeas(torch, lambda: p.assemble_jacobian(s3, d3), 5),
+                 "residual_ms": tmeas(torch, lambda: p.residual(s3, d3), 5),
+                 "note": "FGMRES(50) with P_T stagnates at C3 in the reference algorithm (DESIGN 7)"}
+    del d3, s3, j3, pc3, v3, o3
+    torch.cuda.empty_cache()
+    return out
+
+
+def c5_child():
+    """C5 operator micro-benchmark (BASELINE configs[4]; child process so its 77 GB of
+    factors never meet the C4 solve's): 100 batched block-bidiagonal SpMVs and 20
+    exact-inverse applications (the preconditioner application) over
+    1024 slabs of a 256^2 P1 scalar advection-diffusion block."""
+    import torch
+
+    from paper_2309_00768_b200.c5 import C5Operator
+
+    peak = peak_gbs()
+    nt, n = 1024, 256
+    t0 = time.perf_counter()
+    op = C5Operator(n, nt, seed=0)
+    op.factor()
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(nt * op.n, dtype=torch.float64, device="cuda", generator=g)
+    y = torch.empty_like(x)
+    spmv_ms = tmeas(torch, lambda: op.apply(x, y), 100)
+    inv_ms = tmeas(torch, lambda: op.solve(x, y), 20)
+    op.solve(x, y)
+    rt = float(torch.linalg.norm(op.apply(y) - x) / torch.linalg.norm(x))
+    c = op.coupling
+    spmv_bytes = nt * (8 * op.nnz + 16 * op.n) + 12 * c.nnz + 4 * op.nnz
+    fill = splu_fill(op.matrix(0))
+    sweep_bytes = nt * 8 * fill + 12 * c.nnz + 16 * nt * op.n
+    print("C5JSON " + json.dumps({
+        "workload": "C5 256x256 P1 scalar advection-diffusion, Nt=1024 (67.6 M unknowns), dt=1e-2, eps=1e-3",
+        "spmv_ms": spmv_ms, "spmv_100_s": spmv_ms * 0.1,
+        "spmv": {"algorithmic_bytes": spmv_bytes, "GBps": spmv_bytes / spmv_ms / 1e6,
+                 "frac": spmv_bytes / spmv_ms / 1e6 / peak},
+        "inverse_ms": inv_ms, "inverse_20_s": inv_ms * 0.02, "inverse_per_slab_us": 1e3 * inv_ms / nt,
+        "inverse": {"algorithmic_bytes": sweep_bytes, "GBps": sweep_bytes / inv_ms / 1e6,
+                    "frac": sweep_bytes / inv_ms / 1e6 / peak, "superlu_fill_per_slab": fill},
+        "round_trip_rel": rt, "setup_s": setup,
+        "timed": "100 SpMVs + 20 exact-inverse applications, CUDA events (the inverse is the exact "
+                 "sequential block forward substitution, SURVEY 8(d) interpretation)"}), flush=True)
+
+
+def peak_gbs():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6534.5))
+    except Exception:
+        return 6534.5  # fallback: the pool's measured copy peak of round 1
+
+
+def run_ours(args, rank, world):
     import torch
     import torch.distributed as dist
 
     import paper_2309_00768_b200 as p
     from paper_2309_00768_b200 import _lib
+    from paper_2309_00768_b200.replicas import aggregate
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    c5 = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        # C5 first, in a child process: its 77 GB of factors must not meet this process's pools
+        try:
+            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--c5-child"], cwd=ROOT,
+                               capture_output=True, text=True, timeout=900)
+            c5l = [ln for ln in r.stdout.splitlines() if ln.startswith("C5JSON ")]
+            c5 = json.loads(c5l[0][7:]) if c5l else {"error": r.stderr[-300:]}
+        except Exception as exc:
+            c5 = {"error": str(exc)[:300]}
     torch.cuda.set_device(dev)
     lib = _lib.load()
     disc = p.discretize_config(CONFIG)
     _, _, _, nt, rel = p.config_problem(CONFIG)
-    cfg = p.NewtonConfig(abs_tol=1e-300, rel_tol=rel, max_iters=25,
-                         gmres=p.GmresConfig(rel_tol=1e-8, abs_tol=1e-300, max_iters=100000, restart=50))
+    cfg = newton_cfg(p, rel)
     st0 = p.initial_state(disc)
+    # pinned host copies of the inputs (the initial state and the initial conditions)
+    h_state = st0.vec.data.cpu().pin_memory()
+    h_icu, h_ica = st0.ic_u.cpu().pin_memory(), st0.ic_a.cpu().pin_memory()
+    h_out = torch.empty_like(h_state).pin_memory()
+    h2d = (h_state.numel() + h_icu.numel() + h_ica.numel()) * 8
+    d2h = h_out.numel() * 8
     flush = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)  # > L2 (126 MB)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    def solve_once(state=None):
-        st = state if state is not None else p.SpaceTimeState(st0.vec.copy(), st0.ic_u.clone(), st0.ic_a.clone())
-        return p.solve_all_at_once(disc, cfg, state=st)
+    def step():
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        vec = h_state.to(dev, non_blocking=True)
+        icu, ica = h_icu.to(dev, non_blocking=True), h_ica.to(dev, non_blocking=True)
+        ev[1].record()
+        state = p.SpaceTimeState(p.BlockVector(disc.layout, disc.n_steps, vec), icu, ica)
+        state, stats = p.solve_all_at_once(disc, cfg, state=state)
+        ev[2].record()
+        h_out.copy_(state.vec.data, non_blocking=True)
+        ev[3].record()
+        ev[3].synchronize()
+        return ev[1].elapsed_time(ev[2]), ev[0].elapsed_time(ev[3]), stats
 
     for _ in range(args.warmup):
-        solve_once()
+        step()
     torch.cuda.synchronize()
 
-    # ---- device-resident timed region ----
     clocks = Clocks(dev.index)
-    iters, ms, breakdown = 0, [], {}
+    dev_ms, e2e_ms, iters, breakdown = [], [], 0, {}
     barrier()
     torch.cuda.synchronize()
     launches0 = int(lib.stmhd_launch_count())
     clocks.start()
     stats_last = None
     for _ in range(args.steps):
-        flush.zero_()  # L2 flush between timed iterations (untimed)
+        flush.zero_()  # L2 flush between timed solves (untimed)
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        _, stats = solve_once()
-        e1.record()
-        e1.synchronize()
-        ms.append(e0.elapsed_time(e1))
+        dms, ems, stats = step()
+        dev_ms.append(dms)
+        e2e_ms.append(ems)
         iters += stats.total_gmres
         for k, v in stats.timings.items():
             breakdown[k] = breakdown.get(k, 0.0) + v
@@ -234,71 +426,36 @@ def run_ours(args, rank, world):
     clk = clocks.stop()
     launches = int(lib.stmhd_launch_count()) - launches0
     barrier()
-    from paper_2309_00768_b200.replicas import aggregate
-
-    total_s, iters_all = aggregate(sum(ms) / 1e3, iters, dev)
+    total_s, iters_all = aggregate(sum(dev_ms) / 1e3, iters, dev)
+    e2e_s, _ = aggregate(sum(e2e_ms) / 1e3, iters, dev)
     value = iters_all / total_s
-
-    # ---- e2e through the public API with host buffers ----
-    h_state = st0.vec.data.cpu().pin_memory()
-    h_icu, h_ica = st0.ic_u.cpu().pin_memory(), st0.ic_a.cpu().pin_memory()
-    h_out = torch.empty_like(h_state).pin_memory()
-    e2e_ms, e2e_iters = [], 0
-    barrier()
-    clocks2 = Clocks(dev.index)  # same sampler load as the device-resident region
-    clocks2.start()
-    for _ in range(args.steps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        vec = h_state.to(dev, non_blocking=True)
-        icu, ica = h_icu.to(dev, non_blocking=True), h_ica.to(dev, non_blocking=True)
-        state = p.SpaceTimeState(p.BlockVector(disc.layout, disc.n_steps, vec), icu, ica)
-        state, stats = solve_once(state)
-        h_out.copy_(state.vec.data, non_blocking=True)
-        e1.record()
-        e1.synchronize()
-        e2e_ms.append(e0.elapsed_time(e1))
-        e2e_iters += stats.total_gmres
-    clocks2.stop()
-    e2e_s, e2e_iters = aggregate(sum(e2e_ms) / 1e3, e2e_iters, dev)
-    e2e_value = e2e_iters / e2e_s
-    h2d = (h_state.numel() + h_icu.numel() + h_ica.numel()) * 8
-    d2h = h_out.numel() * 8
-
-    # ---- roofline of the dominant kernel: the F_u time sweep (nd_solve_kernel) ----
+    e2e_value = iters_all / e2e_s
+    peak = peak_gbs()
+    line = {
+        "metric": METRIC, "value": value, "unit": "FGMRES it/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_s * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE C4 analytic problem: island coalescence, equilibrium initial state)",
+        "config": {"workload": WORKLOAD, "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "512 MB flush between timed solves; per-solve factors ~26 GB > L2"},
+        "newton_solve_s": total_s / args.steps, "newton_steps": stats_last.newton_iters,
+        "fgmres_iters": stats_last.gmres_iters,
+        "relative_residual": stats_last.residual_norms[-1] / stats_last.residual_norms[0],
+        "phase_s_per_solve": {k: v / args.steps for k, v in breakdown.items()},
+        "e2e": {"value": e2e_value, "unit": "FGMRES it/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "note": "same timed solves: pinned-host state in, device solve, solution out"},
+        "gpu_launches": launches, "clocks": clk,
+    }
+    if rank != 0:
+        return
+    # ---- rooflines at C4_512 (after the timed region): P_T^-1 (dominant), J.v, assembly ----
     jac = p.assemble_jacobian(st0, disc)
     pc = p.SpaceTimePreconditioner(jac, disc, st0)
     L = disc.layout
-    vu = torch.randn(nt * L.n_u, dtype=torch.float64, device=dev)
-    pc.solve_velocity(vu)
-    torch.cuda.synchronize()
-    reps = 10
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        pc.solve_velocity(vu)
-    e1.record()
-    e1.synchronize()
-    sweep_ms = e0.elapsed_time(e1) / reps
-    # algorithmic bytes use the structural fill: factor slab 0 at a perturbed state
-    # (at u = 0 scipy drops the vanishing cross-component entries)
-    stp = p.SpaceTimeState(st0.vec.copy(), st0.ic_u, st0.ic_a)
-    stp.vec.data += 1e-3 * torch.randn(stp.vec.data.shape, dtype=torch.float64, device=dev,
-                                       generator=torch.Generator(device=dev).manual_seed(0))
-    f_u0 = p.assemble_jacobian(stp, disc).slabs[0].f_u.tocsc()
-    lu = spla.splu(f_u0)
-    fill = int(lu.L.nnz + lu.U.nnz)  # reference SuperLU (COLAMD) fill, SURVEY 8(d)
-    nnz_mu = disc.mass_u_dt_bc.nnz
-    sweep_bytes = nt * 8 * fill + 12 * nnz_mu + 16 * nt * L.n_u
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = sweep_bytes / (sweep_ms / 1e3) / 1e9
+    v = torch.randn(jac.size, dtype=torch.float64, device=dev)
+    out = torch.empty_like(v)
+    pt_ms = tmeas(torch, lambda: pc._into(v, out), 10)
+    pt_bytes = pt_algorithmic_bytes(p, disc, st0, torch, dev)
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "sweep_traffic.json")))
@@ -306,104 +463,56 @@ def run_ours(args, rank, world):
             traffic = prof.get("dram_bytes_per_launch")
     except Exception:
         pass
-    # per-iteration operator costs
-    v = torch.randn(jac.size, dtype=torch.float64, device=dev)
-    out = torch.empty_like(v)
-
-    def tmeas(fn, r=10):
-        fn()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(r):
-            fn()
-        b.record()
-        b.synchronize()
-        return a.elapsed_time(b) / r
-
-    per_iter = {"J_apply_ms": tmeas(lambda: jac._into(v, out), 50),
-                "P_apply_ms": tmeas(lambda: pc._into(v, out), 5),
-                "assembly_ms": tmeas(lambda: p.assemble_jacobian(st0, disc), 5),
-                "residual_ms": tmeas(lambda: p.residual(st0, disc), 5)}
-    # the other north-star kernels against the same peak (SURVEY 8(d) algorithmic bytes)
+    achieved = pt_bytes / (pt_ms / 1e3) / 1e9
+    line["roofline"] = {
+        "kernel": "nd_sweep_kernel: one P_T^-1 apply (pipelined wave | M_j | F_u sweeps, ~95% of the apply) "
+                  "+ its batched pre-steps", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes_per_launch": pt_bytes, "launch_ms": pt_ms,
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json"))
+        else "fallback 6534.5 GB/s (round-1 measured copy peak)",
+        "bytes_formula": "SURVEY 8(d): reference SuperLU (COLAMD) fills, so independent of the GPU factorisation"}
     P_ = disc.pattern
     jv_bytes = nt * (8 * P_.nnz + 16 * L.slab_size) + 12 * disc.jc_nnz + 8 * L.n_p + 4 * P_.nnz
     asm_bytes = nt * 8 * (2 * L.slab_size + P_.nnz + P_.fp_nnz)
-    asm_ms = per_iter["assembly_ms"] + per_iter["residual_ms"]
-    kernel_rooflines = {
-        "J_apply (sell_spmv_kernel)": {"algorithmic_bytes": jv_bytes, "ms": per_iter["J_apply_ms"],
-                                       "GBps": jv_bytes / per_iter["J_apply_ms"] / 1e6,
-                                       "frac": jv_bytes / per_iter["J_apply_ms"] / 1e6 / peak},
+    jv_ms = tmeas(torch, lambda: jac._into(v, out), 30)
+    asm_ms = tmeas(torch, lambda: p.assemble_jacobian(st0, disc), 5) + tmeas(torch, lambda: p.residual(st0, disc), 5)
+    line["kernel_rooflines"] = {
+        "P_T^-1 apply": {"algorithmic_bytes": pt_bytes, "ms": pt_ms, "GBps": achieved, "frac": achieved / peak},
+        "J_apply (sell_spmv_kernel)": {"algorithmic_bytes": jv_bytes, "ms": jv_ms, "GBps": jv_bytes / jv_ms / 1e6,
+                                       "frac": jv_bytes / jv_ms / 1e6 / peak},
         "assembly (residual_patch + values_patch)": {"algorithmic_bytes": asm_bytes, "ms": asm_ms,
                                                      "GBps": asm_bytes / asm_ms / 1e6,
                                                      "frac": asm_bytes / asm_ms / 1e6 / peak},
-        "note": "C2 operators are partly L2-resident (168 MB); the C3 entries are measured in this run after "
-                "the timed region; tools/bench_spmv.py and tools/asm_probe.py give the C5 figures"}
-
-    # the same kernels at C3 (tearing 64^2, Nt=128: 1.37 GB per J.v, beyond L2)
-    if rank == 0 and not args.no_c3_kernels:
+        "config": CONFIG}
+    del jac, pc, v, out
+    torch.cuda.empty_cache()
+    if world == 1 and not args.no_extras:
         try:
-            d3 = p.discretize_config("C3")
-            s3 = p.initial_state(d3)
-            j3 = p.assemble_jacobian(s3, d3)
-            v3 = torch.randn(j3.size, dtype=torch.float64, device=dev)
-            o3 = torch.empty_like(v3)
-            L3, P3, nt3 = d3.layout, d3.pattern, d3.n_steps
-            jv3 = tmeas(lambda: j3._into(v3, o3), 30)
-            as3 = tmeas(lambda: p.assemble_jacobian(s3, d3), 5) + tmeas(lambda: p.residual(s3, d3), 5)
-            jb3 = nt3 * (8 * P3.nnz + 16 * L3.slab_size) + 12 * d3.jc_nnz + 8 * L3.n_p + 4 * P3.nnz
-            ab3 = nt3 * 8 * (2 * L3.slab_size + P3.nnz + P3.fp_nnz)
-            kernel_rooflines["C3"] = {
-                "J_apply (sell_spmv_kernel)": {"algorithmic_bytes": jb3, "ms": jv3, "GBps": jb3 / jv3 / 1e6,
-                                               "frac": jb3 / jv3 / 1e6 / peak},
-                "assembly (residual_patch + values_patch)": {"algorithmic_bytes": ab3, "ms": as3,
-                                                             "GBps": ab3 / as3 / 1e6, "frac": ab3 / as3 / 1e6 / peak}}
-            del d3, s3, j3, v3, o3
-            torch.cuda.empty_cache()
-        except Exception as exc:  # keep the line
-            kernel_rooflines["C3"] = {"error": str(exc)[:200]}
-
-    line = {
-        "metric": "FGMRES iterations/s (C2 Newton solve, P_T preconditioner, FP64)",
-        "value": value, "unit": "FGMRES it/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_s * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE C2 analytic problem, equilibrium initial state)",
-        "config": {"workload": "C2 island coalescence 32x32 P2/P1, dt=0.05, Nt=64, Newton rel 1e-6, FGMRES(50) rel 1e-8",
-                   "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "512 MB flush between timed solves; per-solve factors 0.6 GB > L2"},
-        "newton_solve_s": total_s / args.steps,
-        "newton_steps": stats_last.newton_iters, "fgmres_iters": stats_last.gmres_iters,
-        "relative_residual": stats_last.residual_norms[-1] / stats_last.residual_norms[0],
-        "phase_s_per_solve": {k: v / args.steps for k, v in breakdown.items()},
-        "per_call_ms": per_iter,
-        "kernel_rooflines": kernel_rooflines,
-        "e2e": {"value": e2e_value, "unit": "FGMRES it/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "roofline": {"kernel": "nd_sweep_kernel (F_u time sweep, solve_velocity)", "bound": "hbm",
-                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "algorithmic_bytes_per_launch": sweep_bytes,
-                     "launch_ms": sweep_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
-        "gpu_launches": launches,
-        "clocks": clk,
-    }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            line["other_configs"] = other_configs(p, torch, dev, peak)
+        except Exception as exc:
+            line["other_configs"] = {"error": str(exc)[:300]}
+        line["c5_operator"] = c5
+    if world == 1 and not args.no_cpu_baseline:
         try:
-            smp = cpu_sample(threads_one=True)
+            smp = cpu_sample()
             t_full, cv = extrapolate(smp, nt, stats_last.gmres_iters)
-            line["cpu_baseline"] = {
-                "value": cv, "unit": "FGMRES it/s", "cores": 1, "kind": "port",
-                "sample": f"oracle port (SuperLU P_T + MGS GMRES, 1 pinned core) on C2 mesh, first {SAMPLE_SLABS} "
-                          f"of {nt} slabs: residual+Jacobian+P_T setup + {SAMPLE_ITERS} FGMRES iterations; "
-                          f"extrapolated x{nt // SAMPLE_SLABS} with this run's counts {stats_last.gmres_iters} "
-                          f"-> {t_full:.0f} s per solve"}
+            line["cpu_baseline"] = {"value": cv, "unit": "FGMRES it/s", "cores": 1, "kind": "port",
+                                    "sample": sample_text(smp, nt, stats_last.gmres_iters, t_full),
+                                    "host": host_info(),
+                                    "calibration": "unmodified reference, full C2 solve on one core of the build "
+                                                   "container: 737.7 s, counts [458, 413] "
+                                                   "(tests/golden/cfg_c2.npz times_json)"}
         except Exception as exc:  # keep the GPU line even if the CPU sample fails
             line["cpu_baseline"] = {"value": None, "unit": "FGMRES it/s", "cores": 1, "kind": "port",
                                     "sample": f"failed: {exc}"[:300]}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    print(json.dumps(line), flush=True)
 
 
 def main():
     args = parse()
+    if args.c5_child:
+        c5_child()
+        return
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     if world > 1:

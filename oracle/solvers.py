@@ -208,7 +208,9 @@ def gmres_mgs(apply_a, apply_pinv, b, rel_tol=1e-2, abs_tol=1e-14, max_iters=200
     cap = max_iters if max_total is None else min(max_iters, max_total)
     while total < cap and not conv:
         m = min(m_restart, cap - total)
-        V = np.zeros((n, m + 1))   # column basis, as the reference stores it
+        # column basis, as the reference stores it (restart + 1 columns: a capped timing
+        # sample keeps the reference's column stride)
+        V = np.zeros((n, max(m, min(m_restart, max_iters)) + 1))
         H = np.zeros((m + 1, m))
         cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
         V[:, 0] = r / beta
