@@ -50,10 +50,16 @@ typedef struct stmhd_disc_s *stmhd_disc;
 typedef struct stmhd_pc_s *stmhd_pc;
 typedef struct stmhd_lu_s *stmhd_lu;
 
+/* 2 since stmhd_pc_apply directions 2/3 (round 2); the Python loader refuses others */
 int stmhd_abi_version(void);
 /* number of kernels this library has launched so far (all handles) */
 int64_t stmhd_launch_count(void);
 const char *stmhd_last_error(void);
+/* synchronise `stream` and return STMHD_CUDA if a completed pipelined preconditioner
+   launch recorded a producer timeout (stages not co-resident); 0 otherwise.  Later
+   pipelined launches also report it.  Replaces a device trap, which would kill the
+   context. */
+int stmhd_device_fault(void *stream);
 /* block name of the last SINGULAR status inside the preconditioner ("F_u", "C_A", ...) */
 const char *stmhd_last_block(void);
 
@@ -96,7 +102,9 @@ int stmhd_jac_apply_sell(stmhd_disc d, void *stream, const double *sell, const d
 int stmhd_pc_create(stmhd_disc d, void *stream, const double *slab_values,
                     const double *fp_values, const double *alfven, int variant, stmhd_pc *out);
 int stmhd_pc_destroy(stmhd_pc p);
-/* direction 0: x = P^{-1} r (apply_inverse); 1: x = P r (apply_forward) */
+/* direction 0: x = P^{-1} r (apply_inverse); 1: x = P r (apply_forward);
+   2 / 3: the same with the TRIANGULAR operator whatever the handle's variant (the
+   single-step preconditioner, precond.py:344-387, is always triangular) */
 int stmhd_pc_apply(stmhd_pc p, void *stream, int direction, const double *r, double *x);
 /* sub-operators on (nt x n_field) slab-major blocks:
    0 solve_velocity  1 apply_velocity  2 solve_wave   3 apply_wave   4 apply_potential

@@ -24,6 +24,7 @@ _SIGS = {
     "stmhd_launch_count": (c_i64, []),
     "stmhd_last_error": (C.c_char_p, []),
     "stmhd_last_block": (C.c_char_p, []),
+    "stmhd_device_fault": (c_int, [P]),
     "stmhd_disc_create": (c_int, [C.POINTER(c_vp)]),
     "stmhd_disc_destroy": (c_int, [c_vp]),
     "stmhd_disc_set_int": (c_int, [c_vp, C.c_char_p, c_i64]),
@@ -65,6 +66,8 @@ _SIGS = {
 }
 
 EXPORTS = tuple(_SIGS)
+# must equal stmhd_abi_version() of the loaded library (include/stmhd_b200.h)
+ABI_VERSION = 2
 
 
 def lib_path() -> str:
@@ -86,11 +89,18 @@ def load(build_if_needed: bool = True):
             try:
                 _build.build()
             except Exception as exc:  # pragma: no cover - depends on toolchain
-                if not os.path.exists(path):
-                    raise ImportError(f"stmhd_b200 native library missing and build failed: {exc}")
+                # never run a stale library against newer sources: the ctypes
+                # signatures below follow the sources, not the old binary
+                raise ImportError(f"stmhd_b200 native library is missing or stale and the rebuild "
+                                  f"failed: {exc}") from exc
         if not os.path.exists(path):
             raise ImportError(f"stmhd_b200 native library not found at {path}; run __graft_entry__.build()")
         lib = C.CDLL(path)
+        lib.stmhd_abi_version.restype = c_int
+        got = lib.stmhd_abi_version()
+        if got != ABI_VERSION:
+            raise ImportError(f"stmhd_b200 native library {path} has ABI version {got}, "
+                              f"the bindings expect {ABI_VERSION}; rebuild it (__graft_entry__.build())")
         for name, (res, args) in _SIGS.items():
             fn = getattr(lib, name, None)
             if fn is None:

@@ -249,10 +249,21 @@ int stmhd_pc_destroy(stmhd_pc p) {
 int stmhd_pc_apply(stmhd_pc p, void *stream, int direction, const double *r, double *x) {
   CAPI_BEGIN
   require(p && r && x, "stmhd_pc_apply: bad arguments");
-  if (direction == 0)
-    p->pc->apply_inverse(r, x, (cudaStream_t)stream);
+  require(direction >= 0 && direction <= 3, "stmhd_pc_apply: direction must be 0..3");
+  // directions 2/3: the TRIANGULAR operator whatever the handle's variant -- the
+  // single-step preconditioner is always the triangular one (precond.py:344-387)
+  PC &pc = *p->pc;
+  const int saved = pc.variant;
+  if (direction >= 2) pc.variant = 0;
+  struct Restore {
+    PC &pc;
+    int v;
+    ~Restore() { pc.variant = v; }
+  } restore{pc, saved};
+  if ((direction & 1) == 0)
+    pc.apply_inverse(r, x, (cudaStream_t)stream);
   else
-    p->pc->apply_forward(r, x, (cudaStream_t)stream);
+    pc.apply_forward(r, x, (cudaStream_t)stream);
   CAPI_END
 }
 

@@ -30,10 +30,17 @@ struct stmhd_lu_s {
 
 extern "C" {
 
-int stmhd_abi_version(void) { return 1; }
+int stmhd_abi_version(void) { return 2; }
 int64_t stmhd_launch_count(void) { return stmhd::g_launches.load(); }
 const char *stmhd_last_error(void) { return g_last_error.c_str(); }
 const char *stmhd_last_block(void) { return g_last_block.c_str(); }
+
+int stmhd_device_fault(void *stream) {
+  CAPI_BEGIN
+  STMHD_CUDA_CHECK(cudaStreamSynchronize((cudaStream_t)stream));
+  stmhd::sweep_check_fault((cudaStream_t)stream);
+  CAPI_END
+}
 
 int stmhd_lu_create(int64_t n, const int32_t *rowptr, const int32_t *col, const int32_t *gx,
                     const int32_t *gy, int nbatch, int leaf_max, stmhd_lu *out) {

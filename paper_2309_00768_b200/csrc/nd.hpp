@@ -268,6 +268,8 @@ void sweep_stage_set_post(SweepStage &st, SweepStage &target, const SweepCouplin
 // Stages prepared with grid = true (or ncta != 16) form a grid-family launch: no
 // clusters, cooperative launch, stage i on its own ncta CTAs with a software barrier.
 void sweep_stages_launch(SweepStage *const *st, int nst, cudaStream_t s);
+// throws STMHD_CUDA if a completed pipelined launch recorded a producer timeout
+void sweep_check_fault(cudaStream_t s);
 
 // Cluster-resident sweep in nested-dissection order (nd_sweep.cu).
 void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,

@@ -703,6 +703,8 @@ struct SweepArgs {
   int kpref;       // L2 prefetch of the slab's dense-top rows at the slab start
   unsigned long long *progress;  // L2 prefetch cluster: (epoch << 32) | slab in progress (CTA 0)
   int ldgsts;      // ring items by warp-wide cp.async (16 B per lane) instead of one cp.async.bulk
+  int *fault;       // device word: a consumer gave up waiting for a producer (timeout)
+  int *fault_host;  // host-mapped copy of the fault word, read by the host after the launch
   unsigned long long *trace;
   unsigned long long *prof;  // PROF instantiation: 6 counters per warp
   unsigned long long *tline; // PROF instantiation: per-warp event timeline of slab 1, CTA 0 (128 per warp)
@@ -1439,11 +1441,22 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
            t += blockDim.x) {
         const int e = t < a.ext_ncta[0] ? 0 : 1, c = e ? t - a.ext_ncta[0] : t;
         const int *f = a.flag_in[e] + (int64_t)k * a.ext_ncta[e] + c;
-        unsigned long long t0, t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        while (ld_acquire_gpu(f) != a.epoch) {
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-          if (t1 - t0 > 4000000000ull) __trap();  // 4 s: a producer is not running
+        if (ld_acquire_gpu(f) != a.epoch && !*(volatile int *)a.fault) {
+          unsigned long long t0, t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          while (ld_acquire_gpu(f) != a.epoch) {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 4000000000ull) {
+              // 4 s: a producer is not running (not co-resident).  Record the fault
+              // instead of trapping (a trap kills the CUDA context); the stages run
+              // to completion without further waits and the host raises STMHD_CUDA.
+              atomicExch(a.fault, 1);
+              *(volatile int *)a.fault_host = 1;
+              __threadfence_system();
+              break;
+            }
+            if (*(volatile int *)a.fault) break;
+          }
         }
       }
       __syncthreads();
@@ -2276,8 +2289,38 @@ void sweep_stage_set_post(SweepStage &st, SweepStage &target, const SweepCouplin
   a.post_n = target.a.n;
 }
 
+// Fault words of the pipelined launch: a device word the consumers poll (cheap) and a
+// host-mapped copy the host reads at the next launch / sweep_check_fault().
+static int *g_fault_dev = nullptr;
+static volatile int *g_fault_host = nullptr;
+static int *g_fault_host_dev = nullptr;
+
+static void fault_words_init() {
+  if (g_fault_dev) return;
+  STMHD_CUDA_CHECK(cudaMalloc(&g_fault_dev, sizeof(int)));
+  STMHD_CUDA_CHECK(cudaMemset(g_fault_dev, 0, sizeof(int)));
+  int *h = nullptr;
+  STMHD_CUDA_CHECK(cudaHostAlloc(&h, sizeof(int), cudaHostAllocMapped));
+  *h = 0;
+  STMHD_CUDA_CHECK(cudaHostGetDevicePointer(&g_fault_host_dev, h, 0));
+  g_fault_host = h;
+}
+
+// Raise (once) if a previous pipelined launch recorded a producer timeout.  Only
+// launches that completed are visible, so a caller that needs certainty synchronises
+// first (stmhd_device_fault does).
+void sweep_check_fault(cudaStream_t s) {
+  if (!g_fault_host || !*g_fault_host) return;
+  *g_fault_host = 0;
+  STMHD_CUDA_CHECK(cudaMemsetAsync(g_fault_dev, 0, sizeof(int), s));
+  throw Error(STMHD_CUDA, "pipelined sweep: a consumer stage timed out waiting for its producer "
+                          "(stages not co-resident); results of that launch are invalid");
+}
+
 void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
   require(nst >= 1 && nst <= 3, "sweep: 1 to 3 stages per launch");
+  fault_words_init();
+  sweep_check_fault(s);
   static int epoch = 0;
   ++epoch;
   SweepMulti m{};
@@ -2301,6 +2344,8 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
       STMHD_CUDA_CHECK(cudaMemsetAsync(st.progress.ptr, 0, sizeof(unsigned long long), s));
     }
     st.a.progress = st.progress.as<unsigned long long>();
+    st.a.fault = g_fault_dev;
+    st.a.fault_host = g_fault_host_dev;
     smem = std::max(smem, st.smem);
     require(st.warps == stg[0]->warps, "sweep: stages of one launch need the same warps per CTA");
   }
@@ -2404,15 +2449,34 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
   }
-  // the stages wait on each other: all clusters must be co-resident (cooperative
-  // launch; STMHD_PIPE_COOP=0 drops the attribute for profilers that cannot replay
-  // cooperative cluster launches -- 48 CTAs on 148 SMs are co-resident in practice and
-  // a consumer traps after 4 s instead of hanging)
-  static const int coop_env = env_int2("STMHD_PIPE_COOP", 1);
-  if (nst > 1 && coop_env && !grid) {
-    at[1].id = cudaLaunchAttributeCooperative;
-    at[1].val.cooperative = 1;
-    nat = 2;
+  // the stages wait on each other: all clusters must be co-resident.  When the
+  // occupancy query says the device holds at least nst such clusters at once they are
+  // (the launch is the only work on the device for its duration), and the launch goes
+  // without the cooperative attribute so profilers can replay it; otherwise it is a
+  // cooperative launch.  STMHD_PIPE_COOP=1 forces the attribute, 0 never sets it.  A
+  // consumer that still waits more than 4 s records a fault (sweep_check_fault).
+  static const int coop_env = env_int2("STMHD_PIPE_COOP", -1);
+  if (nst > 1 && !grid && coop_env != 0) {
+    static int max_cl = -1;
+    if (max_cl < 0) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(kCluster * nst);
+      q.blockDim = dim3(warps * 32);
+      q.dynamicSmemBytes = smem;
+      q.attrs = at;
+      q.numAttrs = 1;
+      int mc = 0;
+      if (cudaOccupancyMaxActiveClusters(&mc, (const void *)nd_sweep_kernel<false>, &q) != cudaSuccess) {
+        cudaGetLastError();
+        mc = 0;
+      }
+      max_cl = mc;
+    }
+    if (coop_env == 1 || max_cl < nst) {
+      at[1].id = cudaLaunchAttributeCooperative;
+      at[1].val.cooperative = 1;
+      nat = 2;
+    }
   }
   cfg.attrs = at;
   cfg.numAttrs = nat;

@@ -358,4 +358,7 @@ def gmres(apply_a, apply_pinv, b, x0=None, config: GmresConfig | None = None) ->
     A_into(x, r)
     r.neg_().add_(b)
     true_res = float(torch.linalg.vector_norm(r))
+    # a pipelined preconditioner launch that timed out (stages not co-resident) is
+    # reported here instead of trapping on the device
+    _lib.check(lib.stmhd_device_fault(sp_))
     return GmresResult(x, total, residuals, converged, true_res)

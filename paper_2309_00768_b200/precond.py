@@ -159,7 +159,9 @@ class SpaceTimePreconditioner:
         L = self.layout.slab_size
         full = torch.zeros(self.n_steps * L, dtype=torch.float64, device="cuda")
         full[k * L:(k + 1) * L] = as_device(v).reshape(-1)
-        out = self._into(full, torch.empty_like(full), direction)
+        # directions 2/3 force the TRIANGULAR operator: the reference's single-step
+        # preconditioner ignores the variant (precond.py:344-387)
+        out = self._into(full, torch.empty_like(full), direction + 2)
         return out[k * L:(k + 1) * L].clone()
 
     def apply_single_step_inverse(self, k: int, r_slab):

@@ -28,8 +28,8 @@ def test_library_exports_every_header_symbol():
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
     # and the Python binding declares every header symbol
-    assert set(syms) <= set(_lib.EXPORTS) | {"stmhd_bench_barrier"}, set(syms) - set(_lib.EXPORTS)
-    assert lib.stmhd_abi_version() == 1
+    assert set(syms) <= set(_lib.EXPORTS), set(syms) - set(_lib.EXPORTS)
+    assert lib.stmhd_abi_version() == _lib.ABI_VERSION == 2
 
 
 def _plan_info(mat, gx, gy, leaf):

@@ -92,6 +92,17 @@ def test_single_step_preconditioner(p, golden):
         assert relerr(pc.apply_single_step(k, x).cpu().numpy(), g[f"fwd{k}"]) < 1e-10
         rt = pc.apply_single_step_inverse(k, pc.apply_single_step(k, x)).cpu().numpy()
         assert relerr(rt, x) < 1e-9
+    # the reference's single-step operator ignores the variant (precond.py:344-387 never
+    # reads self.variant), so the same golden vectors hold for SIMPLIFIED and FULL
+    for var in (p.Variant.SIMPLIFIED, p.Variant.FULL):
+        pcv = p.SpaceTimePreconditioner(jac, disc, st, variant=var)
+        for k in range(disc.n_steps):
+            x = g[f"x{k}"]
+            assert relerr(pcv.apply_single_step_inverse(k, x).cpu().numpy(), g[f"inv{k}"]) < 1e-10, var
+            assert relerr(pcv.apply_single_step(k, x).cpu().numpy(), g[f"fwd{k}"]) < 1e-10, var
+        # ...while the space-time apply still uses the variant (differs from TRIANGULAR)
+        xs = np.concatenate([g[f"x{k}"] for k in range(disc.n_steps)])
+        assert relerr(pcv.apply_inverse(xs).cpu().numpy(), pc.apply_inverse(xs).cpu().numpy()) > 1e-8
     # one slab: the space-time and single-step applications coincide
     d1 = p.discretize(p.by_name("island_coalescence"), 0.5, 1.0, 1.0)
     s1 = p.initial_state(d1)

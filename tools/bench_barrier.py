@@ -1,6 +1,6 @@
 import ctypes
-from paper_2309_00768_b200 import _lib
-lib = _lib.load()
+import _microbench
+lib = _microbench.load()
 for bps in (1, 2):
     us = ctypes.c_double()
     lib.stmhd_bench_barrier(bps, 256, 2000, ctypes.byref(us))

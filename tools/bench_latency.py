@@ -1,6 +1,6 @@
 import ctypes
-from paper_2309_00768_b200 import _lib
-lib = _lib.load()
+import _microbench
+lib = _microbench.load()
 lib.stmhd_bench_chase2.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
 for nelem, label in ((1 << 12, "16KB"), (1 << 18, "1MB"), (1 << 23, "32MB"), (1 << 27, "512MB")):
     for cl, th in ((2, 32), (16, 32), (16, 512)):
