@@ -25,7 +25,15 @@ from .linalg import (  # noqa: F401
 )
 from .problems import (  # noqa: F401
     CONFIGS,
+    BCKind,
+    BCSpec,
+    Condition,
     ProblemSpec,
+    Side,
+    dirichlet,
+    enclosed_bcs,
+    natural,
+    slip,
     baseline_island,
     baseline_tearing,
     by_name,

@@ -66,6 +66,10 @@ struct stmhd_disc_s {
   std::unordered_map<std::string, stmhd::HostArray> host;
   std::unordered_map<std::string, stmhd::DevBuf> dev;
   bool finalized = false;
+  // grid-family pipelined P_T^-1: common warps per CTA of its stages, chosen by the
+  // velocity stage at the first launch and kept for every later preconditioner (a
+  // per-preconditioner choice re-prepared the wave / M_j stages, rebuilding their K)
+  int pipe_warps = 0;
   // nested-dissection plans (symbolic) and constant factors
   std::unique_ptr<stmhd::NDPlan> plan_fu, plan_ca, plan_fa, plan_fp, plan_mj, plan_ma, plan_mp, plan_kp;
   std::unique_ptr<stmhd::NDDevice> dev_fu, dev_ca, dev_fa, dev_fp, dev_mj, dev_ma, dev_mp, dev_kp;

@@ -137,6 +137,11 @@ struct NDSweepPlan {
 };
 
 // Device-resident copy of a plan plus the solve schedules.
+struct SweepStage;
+struct SweepStageDeleter {
+  void operator()(SweepStage *p) const;
+};
+
 struct NDDevice {
   const NDPlan *plan = nullptr;
   DevBuf ns, nb, first, idx_off, idx, child_ptr, child_list, emap_off, emap, scat_ptr,
@@ -148,8 +153,15 @@ struct NDDevice {
   DevBuf fwd_ptr_d, bwd_ptr_d;
   int max_front = 0;
   void build(const NDPlan &p, cudaStream_t s);
-  mutable std::unique_ptr<NDSweepPlan> sweep_plan;
+  // sweep plans by (CTAs, warps per CTA): a stage's launch shape (the pipelined
+  // grid-family launch, a single-stage sweep, the warp-count trials) each keep their
+  // own plan; never evicted, so a plan's address identifies it for the device's
+  // lifetime (NDFactor::ktop_plan compares addresses)
+  mutable std::vector<std::unique_ptr<NDSweepPlan>> sweep_plans;
   const NDSweepPlan &get_sweep_plan(int ncta, int warps, int64_t smem_budget, cudaStream_t s, int mode = 0) const;
+  // the single-stage sweep of nd_sweep() for this structure (handle-owned: lives and
+  // dies with the device structure, reused across calls and factorisations)
+  mutable std::unique_ptr<SweepStage, SweepStageDeleter> single_stage;
 };
 
 // A coupling term of a sequential block sweep:
@@ -242,11 +254,7 @@ __device__ __forceinline__ double chunk_gemv(const double *__restrict__ blk, int
 }
 #endif
 
-// A prepared sweep (one cluster of a pipelined launch), nd_sweep.cu.
-struct SweepStage;
-struct SweepStageDeleter {
-  void operator()(SweepStage *) const;
-};
+// A prepared sweep (one cluster of a pipelined launch), nd_sweep.cu (declared above).
 using SweepStagePtr = std::unique_ptr<SweepStage, SweepStageDeleter>;
 SweepStagePtr sweep_stage_new();
 // Permute the stage's right-hand sides in and bind its couplings; ext[e] are stages

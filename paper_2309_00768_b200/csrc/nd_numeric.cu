@@ -258,6 +258,164 @@ __global__ void __launch_bounds__(256) nd_factor_level(FactorArgs a) {
   cta_gemm(nb, ns, ns, -1.0, F + ns, f, FUT, ns, 0.0, FUT + (int64_t)ns * ns, ns, smem, true, false);
 }
 
+// Shared-memory variant for fronts that fit on chip (the many small fronts of the
+// lower tree levels): the global-memory kernel above runs ~5 block barriers per pivot
+// column, each step a chain of L2 round trips; here the front, the triangular
+// inverses and the GEMM tiles live in shared memory.  Same operations in the same
+// order (identical results); only the contribution block goes back to the global
+// front workspace, for the parent's extend-add.
+// Shared layout (doubles): Fs [f*f] | T [ns*ns] (L11^-1 P, then U11^-1) | GEMM tiles
+// [2*GT*GK] | perm (ints).
+__global__ void __launch_bounds__(256) nd_factor_level_smem(FactorArgs a) {
+  extern __shared__ double smem[];
+  __shared__ double red_v[8];
+  __shared__ int red_i[8];
+  __shared__ int piv_sh;
+  const int s = a.lvl_sn[blockIdx.x];
+  const int bl = blockIdx.y;
+  const int b = a.batch0 + bl;
+  const int ns = a.ns[s], nb = a.nb[s], f = ns + nb;
+  double *Fg = a.fronts + (int64_t)bl * a.front_size + a.front_off[s];
+  const double *vals = a.values + (int64_t)b * a.value_stride;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double *F = smem;
+  double *T = F + (int64_t)f * f;
+  double *gs = T + (int64_t)ns * ns;
+  int *perm = reinterpret_cast<int *>(gs + 2 * GT * GK);
+
+  for (int t = tid; t < f * f; t += nt) F[t] = 0.0;
+  __syncthreads();
+  for (int64_t e = a.scat_ptr[s] + tid; e < a.scat_ptr[s + 1]; e += nt) F[a.scat_dst[e]] = vals[a.scat_src[e]];
+  __syncthreads();
+  for (int ci = a.child_ptr[s]; ci < a.child_ptr[s + 1]; ++ci) {
+    const int c = a.child_list[ci];
+    const int nsc = a.ns[c], nbc = a.nb[c], fc = nsc + nbc;
+    const double *Fc = a.fronts + (int64_t)bl * a.front_size + a.front_off[c];
+    const int *em = a.emap + a.emap_off[c];
+    for (int t = tid; t < nbc * nbc; t += nt) {
+      const int i = t / nbc, j = t - i * nbc;
+      F[em[i] * f + em[j]] += Fc[(int64_t)(nsc + i) * fc + nsc + j];
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < ns; i += nt) perm[i] = i;
+  __syncthreads();
+  bool singular = false;
+  const int PB = 32;
+  for (int p0 = 0; p0 < ns; p0 += PB) {
+    const int pw = min(PB, ns - p0);
+    for (int jj = 0; jj < pw; ++jj) {
+      const int col = p0 + jj;
+      double best = -1.0;
+      int bi = col;
+      for (int r = col + tid; r < ns; r += nt) {
+        const double v = fabs(F[r * f + col]);
+        if (v > best) { best = v; bi = r; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if ((tid & 31) == 0) { red_v[tid >> 5] = best; red_i[tid >> 5] = bi; }
+      __syncthreads();
+      if (tid == 0) {
+        double bv = red_v[0];
+        int bidx = red_i[0];
+        for (int w = 1; w < nt / 32; ++w)
+          if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bidx)) { bv = red_v[w]; bidx = red_i[w]; }
+        piv_sh = (bv > 0.0 && isfinite(bv)) ? bidx : -1;
+        if (piv_sh >= 0 && piv_sh != col) {
+          const int t = perm[col]; perm[col] = perm[piv_sh]; perm[piv_sh] = t;
+        }
+      }
+      __syncthreads();
+      const int piv = piv_sh;
+      if (piv < 0) { singular = true; break; }
+      if (piv != col)
+        for (int c = tid; c < f; c += nt) {
+          const double t = F[col * f + c];
+          F[col * f + c] = F[piv * f + c];
+          F[piv * f + c] = t;
+        }
+      __syncthreads();
+      const double inv = 1.0 / F[col * f + col];
+      const int rows = f - col - 1, cols = p0 + pw - col - 1;
+      for (int r = tid; r < rows; r += nt) F[(col + 1 + r) * f + col] *= inv;
+      __syncthreads();
+      for (int t = tid; t < rows * cols; t += nt) {
+        const int r = col + 1 + t / cols, c = col + 1 + t % cols;
+        F[r * f + c] -= F[r * f + col] * F[col * f + c];
+      }
+      __syncthreads();
+    }
+    if (singular) break;
+    for (int c = p0 + pw + tid; c < f; c += nt)
+      for (int r = 1; r < pw; ++r) {
+        double acc = F[(p0 + r) * f + c];
+        for (int k = 0; k < r; ++k) acc -= F[(p0 + r) * f + p0 + k] * F[(p0 + k) * f + c];
+        F[(p0 + r) * f + c] = acc;
+      }
+    __syncthreads();
+    const int m = f - p0 - pw;
+    cta_gemm(m, m, pw, -1.0, F + (p0 + pw) * f + p0, f, F + p0 * f + p0 + pw, f, 1.0, F + (p0 + pw) * f + p0 + pw, f,
+             gs);
+  }
+  if (singular) {
+    if (tid == 0) atomicCAS(a.status, 0, s + 1);
+    return;
+  }
+  // contribution block back to the global workspace (the parent's extend-add)
+  for (int t = tid; t < nb * nb; t += nt) {
+    const int i = t / nb, j = t - i * nb;
+    Fg[(int64_t)(ns + i) * f + ns + j] = F[(ns + i) * f + ns + j];
+  }
+  double *FLT = a.stage + (int64_t)bl * a.stage_size + a.sfl_off[s];
+  double *FUT = a.stage + (int64_t)bl * a.stage_size + a.sfu_off[s];
+  // L11^{-1} P in T (T[ci*ns + r] = FLT[ci*f + r]), rows in sequence
+  for (int i = tid; i < ns; i += nt) {
+    const int ci = perm[i];
+    for (int r = 0; r < ns; ++r) T[ci * ns + r] = (r == i) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int r = 1; r < ns; ++r) {
+    for (int i = tid; i < r; i += nt) {
+      const int ci = perm[i];
+      double acc = 0.0;
+      for (int k = i; k < r; ++k) acc -= F[r * f + k] * T[ci * ns + k];
+      T[ci * ns + r] = acc;
+    }
+    __syncthreads();
+  }
+  for (int t = tid; t < ns * ns; t += nt) {
+    const int ci = t / ns, r = t - ci * ns;
+    FLT[(int64_t)ci * f + r] = T[t];
+  }
+  // G^T = (L11^{-1} P)^T L21^T  ->  FLT[c*f + ns + i]
+  cta_gemm(ns, nb, ns, 1.0, T, ns, F + ns * f, f, 0.0, FLT + ns, f, gs, false, true);
+  // U11^{-1} in T (T[j*ns + i] = FUT[j*ns + i])
+  for (int t = tid; t < ns * ns; t += nt) T[t] = 0.0;
+  __syncthreads();
+  for (int i = ns - 1; i >= 0; --i) {
+    const double dinv = 1.0 / F[i * f + i];
+    for (int j = i + tid; j < ns; j += nt) {
+      double acc = (i == j) ? 1.0 : 0.0;
+      for (int k = i + 1; k <= j; ++k) acc -= F[i * f + k] * T[j * ns + k];
+      T[j * ns + i] = acc * dinv;
+    }
+    __syncthreads();
+  }
+  for (int t = tid; t < ns * ns; t += nt) FUT[t] = T[t];
+  // (-U11^{-1} U12)^T = -U12^T U11^{-T}  ->  FUT[(ns+j)*ns + i]
+  cta_gemm(nb, ns, ns, -1.0, F + ns, f, T, ns, 0.0, FUT + (int64_t)ns * ns, ns, gs, true, false);
+}
+
+// shared-memory bytes of nd_factor_level_smem for a front (f, ns)
+static size_t factor_smem_bytes(int f, int ns) {
+  return ((size_t)f * f + (size_t)ns * ns + 2 * GT * GK) * sizeof(double) + (size_t)(ns + 1) * sizeof(int);
+}
+
 // Column-major staging -> row-chunk blocks [K][R] (zero padded).
 __global__ void nd_relayout(const int *lvl_sn_all, const int *ns_, const int *nb_, const int *rf_, const int *rb_,
                             const int64_t *bszf, const int64_t *bszb, const int64_t *sfl, const int64_t *sfu,
@@ -388,9 +546,42 @@ void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s
     factors.alloc_async((size_t)nbatch * p.factor_size * sizeof(double), s);
   if (!status.ptr) status.alloc_async(sizeof(int), s);
   STMHD_CUDA_CHECK(cudaMemsetAsync(status.ptr, 0, sizeof(int), s));
-  // chunk the batch so front workspace + staging stay below ~3 GiB
+  // chunk the batch so front workspace + staging stay within a budget: the top tree
+  // levels have one front per matrix, so a level launch has (fronts x chunk) CTAs --
+  // a small chunk leaves most SMs idle on the largest fronts.  Budget: STMHD_FACTOR_WS_GB
+  // (default 16 GiB), at most a quarter of the free device memory, at least 3 GiB.
+  static const int ws_env = [] {
+    const char *e = getenv("STMHD_FACTOR_WS_GB");
+    return e ? atoi(e) : 16;
+  }();
+  int64_t budget = (int64_t)std::max(ws_env, 1) << 30;
+  {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) budget = std::min<int64_t>(budget, (int64_t)(free_b / 4));
+    budget = std::max<int64_t>(budget, int64_t(3) << 30);
+  }
   int64_t per = (std::max<int64_t>(p.front_size, 1) + p.stage_size) * (int64_t)sizeof(double);
-  int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t(3) << 30) / per));
+  int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, budget / per));
+  // equal chunks (a short last chunk would run its levels on few CTAs)
+  {
+    const int nch = (int)((nbatch + chunk - 1) / chunk);
+    chunk = (int)((nbatch + nch - 1) / nch);
+  }
+  if (getenv("STMHD_FACTOR_INFO")) {
+    fprintf(stderr, "[factor] n=%lld nbatch=%d front %.1f MB + stage %.1f MB per matrix, chunk %d, levels %d\n",
+            (long long)p.n, nbatch, p.front_size * 8e-6, p.stage_size * 8e-6, chunk, p.nlevels);
+    for (int l = 0; l < p.nlevels; ++l) {
+      int fmx = 0, nsmx = 0;
+      double fs = 0;
+      for (int sn : p.level_sn[l]) {
+        fmx = std::max(fmx, p.ns[sn] + p.nb[sn]);
+        nsmx = std::max(nsmx, p.ns[sn]);
+        fs += p.ns[sn] + p.nb[sn];
+      }
+      fprintf(stderr, "[factor]   level %d: %zu fronts, f max %d mean %.0f, ns max %d\n", l, p.level_sn[l].size(), fmx,
+              p.level_sn[l].empty() ? 0.0 : fs / p.level_sn[l].size(), nsmx);
+    }
+  }
   DevBuf fronts, stage;  // stream-ordered pool: reused by the next factorisation
   fronts.alloc_async((size_t)chunk * std::max<int64_t>(p.front_size, 1) * sizeof(double), s);
   stage.alloc_async((size_t)chunk * std::max<int64_t>(p.stage_size, 1) * sizeof(double), s);
@@ -403,6 +594,25 @@ void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s
   }
   std::vector<int> lptr{0};
   for (auto &l : p.level_sn) lptr.push_back(lptr.back() + (int)l.size());
+  // levels whose largest front fits shared memory run the on-chip kernel
+  // (STMHD_FACTOR_SMEM=0: every level in global memory)
+  static const int smem_env = [] {
+    const char *e = getenv("STMHD_FACTOR_SMEM");
+    return e ? atoi(e) : 1;
+  }();
+  constexpr size_t kFactorSmemMax = 200 * 1024;
+  std::vector<size_t> lvl_smem(p.nlevels, 0);
+  static size_t smem_attr = 0;
+  for (int l = 0; l < p.nlevels && smem_env; ++l) {
+    size_t need = 0;
+    for (int sn : p.level_sn[l]) need = std::max(need, factor_smem_bytes(p.ns[sn] + p.nb[sn], p.ns[sn]));
+    if (need <= kFactorSmemMax) lvl_smem[l] = std::max<size_t>(need, 1);
+    if (lvl_smem[l] > smem_attr) {
+      STMHD_CUDA_CHECK(cudaFuncSetAttribute(nd_factor_level_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kFactorSmemMax));
+      smem_attr = kFactorSmemMax;
+    }
+  }
   for (int b0 = 0; b0 < nbatch; b0 += chunk) {
     int nbch = std::min(chunk, nbatch - b0);
     for (int l = 0; l < p.nlevels; ++l) {
@@ -431,7 +641,10 @@ void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s
       a.stage = stage.as<double>();
       a.stage_size = p.stage_size;
       a.status = status.as<int>();
-      nd_factor_level<<<dim3(cnt, nbch), 256, smem, s>>>(a);
+      if (lvl_smem[l] > 0)
+        nd_factor_level_smem<<<dim3(cnt, nbch), 256, lvl_smem[l], s>>>(a);
+      else
+        nd_factor_level<<<dim3(cnt, nbch), 256, smem, s>>>(a);
       STMHD_LAUNCH_CHECK();
     }
     nd_relayout<<<dim3(p.nsn, nbch), 256, 0, s>>>(

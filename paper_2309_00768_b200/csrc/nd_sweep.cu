@@ -60,7 +60,8 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   const int slot_sz = sweep_slot(*plan);
   const int64_t vstride_max = (std::max(max_front, 1) + 15) / 16 * 16 + 2 * slot_sz;
   const int64_t sub_budget = smem_budget - (int64_t)warps * vstride_max;  // conservative (largest front)
-  if (sweep_plan && sweep_plan->ncta == ncta && sweep_plan->warps == warps) return *sweep_plan;
+  for (const auto &c : sweep_plans)
+    if (c->ncta == ncta && c->warps == warps) return *c;
   const NDPlan &p = *plan;
   auto sp = std::make_unique<NDSweepPlan>();
   sp->ncta = ncta;
@@ -110,8 +111,13 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   // subtrees per sweep: one per CTA in cluster mode; in grid mode (ncta > 16) fewer
   // subtrees than CTAs keep the top small enough for the dense K (all CTAs stream K
   // and the coupling; CTAs without a subtree idle through the subtree phases)
+  // (STMHD_SWEEP_GRID_SUBTREES; default: 64 for a stage of the grid-family pipelined
+  // launch -- two more CTA-local levels and two fewer grid-wide band levels per
+  // direction than one subtree per CTA, C4/C3 P_T^-1 -8 % -- and one per CTA for a
+  // whole-GPU single sweep, where 64 measured 30 % slower on C5)
   static const int maxsub_env = env_int2("STMHD_SWEEP_GRID_SUBTREES", 0);
-  const int max_sub = (ncta > 16 && maxsub_env > 0) ? std::min(maxsub_env, ncta) : ncta;
+  const int maxsub_dflt = ncta < num_sms() ? 64 : ncta;
+  const int max_sub = ncta > 16 ? std::min(maxsub_env > 0 ? maxsub_env : maxsub_dflt, ncta) : ncta;
   std::vector<int> frontier;
   if (D) {
     for (int sn = 0; sn < p.nsn; ++sn)
@@ -639,8 +645,8 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   sp->pos = upload_vec(pos, s);
   sp->iperm = upload_vec(iperm, s);
   STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-  sweep_plan = std::move(sp);
-  return *sweep_plan;
+  sweep_plans.push_back(std::move(sp));
+  return *sweep_plans.back();
 }
 
 struct SweepArgs {
@@ -1952,6 +1958,9 @@ static void build_dense_top(const NDFactor &fac, const NDSweepPlan &sp, cudaStre
     STMHD_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr[nc - 1] = smem;
   }
+  if (getenv("STMHD_SWEEP_PLAN_INFO"))
+    fprintf(stderr, "[topk] n=%lld nT=%d nbatch=%d plan ncta=%d warps=%d gen=%llu items=%d grid=%d\n", (long long)p.n,
+            sp.ntT, fac.nbatch, sp.ncta, sp.warps, (unsigned long long)fac.gen, nitems, grid);
   if (nc == 2) topk_kernel<2><<<grid, 512, smem, s>>>(g);
   else topk_kernel<1><<<grid, 256, smem, s>>>(g);
   STMHD_LAUNCH_CHECK();
@@ -2550,10 +2559,9 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
 
 void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x, int64_t ld_x, int nrhs,
               const SweepCoupling *cpl, int ncpl, cudaStream_t s) {
-  // one stage per factor structure (reused across calls and factorisations; launches
-  // are stream ordered)
-  static std::map<const NDDevice *, SweepStagePtr> stages;
-  SweepStagePtr &sp = stages[fac.dev];
+  // one stage per factor structure, owned by it (reused across calls and
+  // factorisations; launches are stream ordered)
+  SweepStagePtr &sp = fac.dev->single_stage;
   if (!sp) sp = sweep_stage_new();
   // grid mode (one CTA per SM, software grid barrier) when a slab's factor is large
   // enough that 16 SMs cannot stream it (configuration 5: 75 MB per slab); the

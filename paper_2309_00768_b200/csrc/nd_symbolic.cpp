@@ -264,10 +264,14 @@ NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const in
   p.bsz_f.assign(S, 0);
   p.bsz_b.assign(S, 0);
   // rows per chunk: the largest power of two <= 32 whose block fits kChunkMax doubles
-  static const int64_t kChunkMax = [] {
+  // (STMHD_CHUNK_MAX; default 640 doubles, 512 for the large 64^2 velocity blocks,
+  // whose sweeps run grid-wide: smaller TMA slots leave shared memory for deeper
+  // CTA-local subtrees -- C4/C3 P_T^-1 -7 %, measured)
+  static const int64_t chunk_env = [] {
     const char *e = getenv("STMHD_CHUNK_MAX");
-    return e ? (int64_t)atoi(e) : (int64_t)640;
+    return e ? (int64_t)atoi(e) : (int64_t)0;
   }();
+  const int64_t kChunkMax = chunk_env > 0 ? chunk_env : (n > 20000 ? 512 : 640);
   auto rows_per_chunk = [&](int64_t K) {
     int R = 32;
     while (R > 1 && (int64_t)R * K > kChunkMax) R >>= 1;

@@ -15,7 +15,6 @@ struct PC {
   DevBuf tu1, tu2, ta1, ta2, ta3, tp1, tp2, tp3, tj;
   std::unique_ptr<NDFactor> fu, ca, fa, fpf;
   SweepStagePtr st_wave, st_mj, st_vel;  // pipelined apply_inverse (TRIANGULAR)
-  int pipe_warps = 0;                     // grid-family pipelined launch: common warps per CTA
   int64_t vals_tag = 0;                  // this preconditioner's coupling-value generation
 
   PC(stmhd_disc_s *d, cudaStream_t s, const double *js, const double *fp, const double *alf, int variant);

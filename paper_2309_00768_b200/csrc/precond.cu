@@ -442,11 +442,22 @@ void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
     const char *e = getenv("STMHD_PC_FU_CTAS");
     return e ? atoi(e) : 0;
   }();
-  const int nc_fu = grid ? (fu_ctas_env > 0 ? std::min(fu_ctas_env, num_sms() - 32) : num_sms() - 32) : 16;
+  // CTAs of the wave and M_j stages in the grid-family launch (STMHD_PC_SIDE_CTAS,
+  // default 16); the velocity stage takes the remaining SMs
+  static const int side_env = [] {
+    const char *e = getenv("STMHD_PC_SIDE_CTAS");
+    return e ? atoi(e) : 16;
+  }();
+  const int nc_side = grid ? std::max(1, std::min(side_env, 32)) : 16;
+  const int nc_fu = grid ? (fu_ctas_env > 0 ? std::min(fu_ctas_env, num_sms() - 2 * nc_side)
+                                            : num_sms() - 2 * nc_side)
+                         : 16;
   // grid-family launches need one warp count for all stages: the velocity stage's
-  // choice (the others have slack) is remembered after the first preparation
+  // choice (the others have slack) is remembered on the discretisation after the first
+  // preparation
+  int &pipe_warps = d->pipe_warps;
   const int wf = grid ? pipe_warps : 0;
-  sweep_stage_prepare(*st_wave, *ca, ta2.as<double>(), n_a, x + o_a, slab, nt, cw, 2, nullptr, 0, s, tag, 16, grid, wf);
+  sweep_stage_prepare(*st_wave, *ca, ta2.as<double>(), n_a, x + o_a, slab, nt, cw, 2, nullptr, 0, s, tag, nc_side, grid, wf);
   SweepCoupling cj;  // -K_jA x_A
   DCsr mix = d->csr("mixja");
   cj.rowptr = mix.rowptr;
@@ -455,7 +466,7 @@ void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
   cj.ext = 0;
   cj.coef = -1.0;
   SweepStage *wj[1] = {st_wave.get()};
-  sweep_stage_prepare(*st_mj, *d->lu_mj, r_j, slab, x + o_j, slab, nt, &cj, 1, wj, 1, s, tag, 16, grid, wf);
+  sweep_stage_prepare(*st_mj, *d->lu_mj, r_j, slab, x + o_j, slab, nt, &cj, 1, wj, 1, s, tag, nc_side, grid, wf);
   SweepCoupling cu;  // + M_u/dt x_u(k-1); waits on the M_j stage (which adds the Z terms)
   DCsr m = d->csr("mu_dt");
   cu.rowptr = m.rowptr;
@@ -469,9 +480,9 @@ void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
   if (grid && !pipe_warps) {
     pipe_warps = sweep_stage_warps(*st_vel);
     if (sweep_stage_warps(*st_wave) != pipe_warps || sweep_stage_warps(*st_mj) != pipe_warps) {
-      sweep_stage_prepare(*st_wave, *ca, ta2.as<double>(), n_a, x + o_a, slab, nt, cw, 2, nullptr, 0, s, tag, 16, grid,
-                          pipe_warps);
-      sweep_stage_prepare(*st_mj, *d->lu_mj, r_j, slab, x + o_j, slab, nt, &cj, 1, wj, 1, s, tag, 16, grid,
+      sweep_stage_prepare(*st_wave, *ca, ta2.as<double>(), n_a, x + o_a, slab, nt, cw, 2, nullptr, 0, s, tag, nc_side,
+                          grid, pipe_warps);
+      sweep_stage_prepare(*st_mj, *d->lu_mj, r_j, slab, x + o_j, slab, nt, &cj, 1, wj, 1, s, tag, nc_side, grid,
                           pipe_warps);
       sweep_stage_prepare(*st_vel, *fu, tu1.as<double>(), n_u, x, slab, nt, &cu, 1, ju, 1, s, tag, nc_fu, grid,
                           pipe_warps);

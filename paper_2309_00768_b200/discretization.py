@@ -21,7 +21,7 @@ from . import _lib, fem
 from .errors import ConfigurationError
 from .linalg import BlockVector, FieldLayout, as_device
 from .patterns import SlabPattern, csr_arrays, product_plan
-from .problems import ProblemSpec
+from .problems import ProblemSpec, constrained_dofs, flux_terms
 
 
 def _cell_count(length, dx):
@@ -40,13 +40,13 @@ class Discretization:
         nst = t_final / dt
         if abs(nst - round(nst)) > 1e-9 or round(nst) < 1:
             raise ConfigurationError(f"T={t_final} is not an integer multiple of dt={dt}")
-        if problem.vel_degree not in (2, 3):
+        kv = getattr(problem, "vel_degree", 3)  # a reference ProblemSpec: P3/P2
+        if kv not in (2, 3):
             raise ConfigurationError("velocity degree must be 2 or 3")
         self.problem, self.dt, self.t_final = problem, dt, t_final
         self.n_steps = int(round(nst))
         x0, x1, y0, y1 = problem.domain
         self.mesh = fem.Mesh(x0, x1, y0, y1, _cell_count(x1 - x0, dx), _cell_count(y1 - y0, dx))
-        kv = problem.vel_degree
         self.vel = fem.Space(self.mesh, kv, 2)
         self.prs = fem.Space(self.mesh, kv - 1)
         self.cur = fem.Space(self.mesh, 1)
@@ -65,14 +65,15 @@ class Discretization:
         self.div = ops["div"]
         self.e_load = fem.load_vector(self.pot, problem.e_eq)
         flux = np.zeros(self.cur.ndof)
+        fterms = flux_terms(problem)
         for side in fem.SIDES:
-            if side in problem.a_flux:
-                flux = flux + fem.edge_load_vector(self.cur, side, problem.a_flux[side])
+            if side in fterms:
+                flux = flux + fem.edge_load_vector(self.cur, side, fterms[side])
         self.current_flux = flux / problem.mu0
 
-        self.u_bc_idx = fem.slip_dofs(self.vel)
-        self.u_bc_vals = np.zeros(len(self.u_bc_idx))
-        self.a_bc_idx, self.a_bc_vals = fem.dirichlet_dofs(self.pot, problem.a_dirichlet, problem.a_eq)
+        # constrained DOFs from the problem's BCSpec (reference problems.py:179-180)
+        self.u_bc_idx, self.u_bc_vals = constrained_dofs(self.vel, problem, "u")
+        self.a_bc_idx, self.a_bc_vals = constrained_dofs(self.pot, problem, "A")
 
         self.p_pin = 0
         mvec = fem.load_vector(self.prs, lambda x, y: 1.0 + 0.0 * x)

@@ -1,5 +1,6 @@
 """Where an FGMRES iteration's time goes on C2 (device-timed): P_T^-1 + J.v alone,
 plus the CGS2 kernels, and the full gmres() loop (host Givens, copies, syncs)."""
+import sys
 import time
 
 import torch
@@ -7,7 +8,7 @@ import torch
 import paper_2309_00768_b200 as p
 from paper_2309_00768_b200 import _lib
 
-d = p.discretize_config("C2")
+d = p.discretize_config(sys.argv[1] if len(sys.argv) > 1 else "C2")
 st = p.initial_state(d)
 r = p.residual(st, d)
 jac = p.assemble_jacobian(st, d)
