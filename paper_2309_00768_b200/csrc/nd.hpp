@@ -125,6 +125,7 @@ struct NDSweepPlan {
   // block [tab_ptr[c], tab_ptr[c+1]): forward int32 entries, then backward uint16 pairs
   int tab_ints = 0;
   DevBuf tab, tab_ptr, tab_nf;
+  DevBuf tab_band, tab_band_ptr;  // per-CTA band positions referenced by the backward tables
   DevBuf g3p;   // int4 per front position: {permuted rhs index or -1, cb1, cb2, 0}
   DevBuf bpos;  // int per front position: permuted position of the front entry
   DevBuf bpos4; // bpos per supernode, each block 16-byte aligned (TMA ring table items)

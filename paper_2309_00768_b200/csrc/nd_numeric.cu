@@ -827,6 +827,111 @@ __global__ void __launch_bounds__(512, 1) nd_solve_cta_kernel(SolveArgs a) {
 }
 
 
+// Multi-right-hand-side variant for a shared factor (nbatch == 1): a CTA solves G
+// right-hand sides together, so every factor element a warp loads feeds G dot
+// products and the G gathers of a front are in flight at once.  Same per-RHS
+// arithmetic order as chunk_gemv (16 loads per step, 4 partial sums).
+template <int G>
+__device__ __forceinline__ void chunk_gemv_multi(const double *__restrict__ blk, int R, int K, const double *v,
+                                                 int vs, int lane, double (&out)[G]) {
+  const int kl = 32 / R, rl = lane & (R - 1), kq = lane / R;
+  double acc[G][4];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[g][i] = 0.0;
+  for (int t = kq; t < K; t += 16 * kl) {
+    double m[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) m[q] = __ldg(blk + (int64_t)min(t + q * kl, K - 1) * R + rl);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int tq = t + q * kl;
+#pragma unroll
+      for (int g = 0; g < G; ++g) acc[g][q & 3] = fma(m[q], tq < K ? v[g * vs + tq] : 0.0, acc[g][q & 3]);
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    double o = (acc[g][0] + acc[g][1]) + (acc[g][2] + acc[g][3]);
+    for (int sh = R; sh < 32; sh <<= 1) o += __shfl_xor_sync(0xffffffffu, o, sh);
+    out[g] = o;
+  }
+}
+
+template <int G>
+__global__ void __launch_bounds__(512, 1) nd_solve_cta_multi_kernel(SolveArgs a) {
+  extern __shared__ double vbuf[];
+  const int b0 = blockIdx.x * G;
+  const int w = threadIdx.x >> 5, nwarp = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const int vs = a.vstride;
+  double *v = vbuf + (int64_t)w * G * vs;
+  int nb = min(G, a.nrhs - b0);
+  for (int l = 0; l < a.nlevels; ++l) {
+    for (int i = a.fwd_ptr[l] + w; i < a.fwd_ptr[l + 1]; i += nwarp) {
+      const SolveItem it = a.fwd_items[i];
+      const int4 *gt = a.gather3 + it.goff;
+      for (int t = lane; t < it.f; t += 32) {
+        const int4 gg = gt[t];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int b = min(b0 + g, a.nrhs - 1);
+          const double *rhs = a.rhs + (int64_t)b * a.ld_rhs;
+          const double *cb = a.cbv + (int64_t)b * a.cbv_size;
+          const double r = gg.x >= 0 ? rhs[gg.x] : 0.0;
+          const double c1 = gg.y >= 0 ? cb[gg.y] : 0.0;
+          const double c2 = gg.z >= 0 ? cb[gg.z] : 0.0;
+          v[g * vs + t] = (r + c1) + c2;
+        }
+      }
+      __syncwarp();
+      const int R = 32 / it.kl;
+      const int r = it.r0 + (lane & (R - 1));
+      double out[G];
+      chunk_gemv_multi<G>(a.factors + it.foff, R, it.ns, v, vs, lane, out);
+      if (lane < R && r < it.r1)
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          if (g >= nb) break;
+          const int b = b0 + g;
+          if (r < it.ns) a.ybuf[(int64_t)b * a.n + it.first + r] = out[g];
+          else a.cbv[(int64_t)b * a.cbv_size + it.cboff + r - it.ns] = v[g * vs + r] - out[g];
+        }
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+  for (int l = a.nlevels - 1; l >= 0; --l) {
+    for (int i = a.bwd_ptr[l] + w; i < a.bwd_ptr[l + 1]; i += nwarp) {
+      const SolveItem it = a.bwd_items[i];
+      const int *idx = a.idx + it.goff;
+      for (int t = lane; t < it.f; t += 32) {
+        const int ii = t >= it.ns ? idx[t] : -1;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int b = min(b0 + g, a.nrhs - 1);
+          v[g * vs + t] = t < it.ns ? a.ybuf[(int64_t)b * a.n + it.first + t] : a.x[(int64_t)b * a.ld_x + ii];
+        }
+      }
+      __syncwarp();
+      const int R = 32 / it.kl;
+      const int r = it.r0 + (lane & (R - 1));
+      double out[G];
+      chunk_gemv_multi<G>(a.factors + it.foff, R, it.f, v, vs, lane, out);
+      if (lane < R && r < it.r1) {
+        const int xi = idx[r];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          if (g >= nb) break;
+          a.x[(int64_t)(b0 + g) * a.ld_x + xi] = out[g];
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
 // C = A B for A (n x n, column-major), B (n x nrhs, ld ldb), split over K in S parts:
 // part s writes ws[s][c][m]; FP64 tensor cores (mma.sync m8n8k4).  CTA tile 32 x 32,
 // 8 warps of one 8-row m-subtile x two 8-column c-subtiles, 8 k-steps of loads in
@@ -969,6 +1074,32 @@ void NDFactor::solve_nd(const double *rhs, int64_t ld_rhs, double *x, int64_t ld
     const char *e = getenv("STMHD_SOLVE_CTA_MIN");
     return e ? atoi(e) : 8;
   }();
+  // shared factor, many right-hand sides: G per CTA (STMHD_SOLVE_MULTI, default 4;
+  // 1 = one right-hand side per CTA)
+  static const int multi_env = [] {
+    const char *e = getenv("STMHD_SOLVE_MULTI");
+    return e ? atoi(e) : 4;
+  }();
+  if (nbatch == 1 && nrhs >= 2 * num_sms() && multi_env > 1) {
+    int G = multi_env >= 4 ? 4 : 2;
+    while (G > 1 && (size_t)(threads / 32) * G * a.vstride * sizeof(double) > 220 * 1024) G /= 2;
+    if (G > 1) {
+      const size_t sm = (size_t)(threads / 32) * G * a.vstride * sizeof(double);
+      static bool attr3 = false;
+      if (!attr3) {
+        STMHD_CUDA_CHECK(cudaFuncSetAttribute(nd_solve_cta_multi_kernel<4>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        STMHD_CUDA_CHECK(cudaFuncSetAttribute(nd_solve_cta_multi_kernel<2>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        attr3 = true;
+      }
+      const int nblk = (nrhs + G - 1) / G;
+      if (G == 4) nd_solve_cta_multi_kernel<4><<<nblk, threads, sm, s>>>(a);
+      else nd_solve_cta_multi_kernel<2><<<nblk, threads, sm, s>>>(a);
+      STMHD_LAUNCH_CHECK();
+      return;
+    }
+  }
   if (nrhs >= cta_min) {  // independent right-hand sides: one CTA each, no grid barrier
     static bool attr2 = false;
     if (!attr2) {

@@ -383,12 +383,14 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   // forward (internal subtree supernodes only; leaves gather rhs rows alone): int32
   // per front entry = child update indices (y, z) relative to the CTA's update block
   // as two int16; backward (every subtree supernode, boundary entries t >= ns): uint16
-  // = own-subtree index, or 0x8000 | top index (x_T is staged in shared memory).
+  // = own-subtree index, 0x8000 | K index (x_T is staged in shared memory), or, with
+  // band levels between the subtrees and the K region, 0xC000 | index into the CTA's
+  // list of band positions (x read from global memory after the band levels).
   static const int stab_env = env_int2("STMHD_SWEEP_SMEM_TABLES", 1);
   std::vector<int> ftab_off(p.nsn, -1), btab_off(p.nsn, -1), sn_of_first(p.n, -1);
-  std::vector<int> tab_all, tab_ptr(ncta + 1, 0), tab_nf(ncta, 0);
-  bool stab = stab_env && mode == 0 && sp->dense && sp->ntop == 0 && sp->nsub > 0 && maxlen < 32768 && maxcb < 32768 &&
-              sp->ntT < 32768;
+  std::vector<int> tab_all, tab_ptr(ncta + 1, 0), tab_nf(ncta, 0), tab_band, tab_band_ptr(ncta + 1, 0);
+  bool stab = stab_env && mode == 0 && sp->dense && sp->nsub > 0 && maxlen < 32768 && maxcb < 32768 &&
+              sp->ntT < 0x4000;
   if (stab) {
     for (int sn = 0; sn < p.nsn; ++sn) sn_of_first[p.first[sn]] = sn;
     for (int c = 0; c < ncta && c < (int)roots.size(); ++c) {
@@ -412,12 +414,22 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
           const int q = bpos[o + t];
           const int64_t rel = q - sf;
           if (rel >= 0 && rel < info[4 * c + 1]) bw.push_back((unsigned short)rel);
-          else {
-            require(tidx_h[q] >= 0, "nd sweep: subtree boundary outside the top");
+          else if (tidx_h[q] >= 0) {
             bw.push_back((unsigned short)(0x8000 | tidx_h[q]));
+          } else {  // band node
+            int bi = -1;
+            for (int i = tab_band_ptr[c]; i < (int)tab_band.size(); ++i)
+              if (tab_band[i] == q) bi = i - tab_band_ptr[c];
+            if (bi < 0) {
+              bi = (int)tab_band.size() - tab_band_ptr[c];
+              tab_band.push_back(q);
+            }
+            require(bi < 0x4000, "nd sweep: too many band boundary entries for the subtree tables");
+            bw.push_back((unsigned short)(0xC000 | bi));
           }
         }
       }
+      tab_band_ptr[c + 1] = (int)tab_band.size();
       while (bw.size() % 8) bw.push_back(0);  // 16-byte blocks
       tab_nf[c] = (int)fw.size();
       while (fw.size() % 4) fw.push_back(0);
@@ -429,7 +441,10 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
       tab_nf[c] = (int)fw.size();  // padded forward length (start of the backward entries)
       static_cast<void>(base);
     }
-    for (int c = (int)roots.size(); c < ncta; ++c) tab_ptr[c + 1] = tab_ptr[c];
+    for (int c = (int)roots.size(); c < ncta; ++c) {
+      tab_ptr[c + 1] = tab_ptr[c];
+      tab_band_ptr[c + 1] = tab_band_ptr[c];
+    }
     int maxtab = 0;
     for (int c = 0; c < ncta; ++c) maxtab = std::max(maxtab, tab_ptr[c + 1] - tab_ptr[c]);
     sp->tab_ints = (maxtab + 3) / 4 * 4;
@@ -641,6 +656,9 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     sp->tab = upload_vec(tab_all, s);
     sp->tab_ptr = upload_vec(tab_ptr, s);
     sp->tab_nf = upload_vec(tab_nf, s);
+    if (tab_band.empty()) tab_band.push_back(0);
+    sp->tab_band = upload_vec(tab_band, s);
+    sp->tab_band_ptr = upload_vec(tab_band_ptr, s);
   }
   sp->pos = upload_vec(pos, s);
   sp->iperm = upload_vec(iperm, s);
@@ -667,6 +685,7 @@ struct SweepArgs {
   double *tbuf;                // coupled right-hand side of the top rows
   // per-CTA subtree front tables resident in shared memory (NDSweepPlan::tab)
   const int *tab, *tab_ptr, *tab_nf;
+  const int *tab_band, *tab_band_ptr;  // per-CTA band positions of the backward tables
   int tab_ints;
   // dense top (NDSweepPlan::dense): z_T gather table and K = (A^{-1})_TT per slab
   int dense, ntT, kpad, zlen;  // zlen: shared doubles of z_T + the dense partial sums
@@ -806,6 +825,7 @@ struct SubView {
   double *zs;                     // dense top: z_T (kpad doubles); x_T during the subtree backward
   const int *ftab;                // subtree forward tables (shared memory) or null
   const unsigned short *btab;     // subtree backward tables
+  const int *bband;               // this CTA's band positions (global; 0xC000 table codes)
   int64_t first, len, cbfirst;
 };
 
@@ -1044,7 +1064,7 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
       if (t < tk.ns) v = ys[t];
       else {
         const unsigned code = bt[t];
-        v = (code & 0x8000u) ? sv.zs[code & 0x7fffu] : sv.xs[code];
+        v = (code & 0x8000u) ? ((code & 0x4000u) ? x[sv.bband[code & 0x3fffu]] : sv.zs[code & 0x3fffu]) : sv.xs[code];
       }
       w.v[t] = v;
     }
@@ -1365,12 +1385,14 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   sv.zs = sv.rhs_s + a.sub_len;
   sv.ftab = nullptr;
   sv.btab = nullptr;
+  sv.bband = nullptr;
   if (a.tab_ints) {  // this CTA's subtree front tables, resident for the whole launch
     int *tb = reinterpret_cast<int *>((reinterpret_cast<uintptr_t>(sv.zs + a.zlen) + 15) & ~(uintptr_t)15);
     const int o = a.tab_ptr[crank], nt = a.tab_ptr[crank + 1] - o;
     for (int i = threadIdx.x; i < nt; i += blockDim.x) tb[i] = a.tab[o + i];
     sv.ftab = tb;
     sv.btab = reinterpret_cast<const unsigned short *>(tb + a.tab_nf[crank]);
+    sv.bband = a.tab_band + a.tab_band_ptr[crank];
     __syncthreads();
   }
   sv.first = a.sub_info[4 * crank + 0];
@@ -1592,7 +1614,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       sweep_trace(a, step, crank);
     }
   }
-  if (PROF && lane == 0)
+  if (PROF && lane == 0 && a.prof)  // (only the traced stage of a pipelined launch has counters)
     for (int i = 0; i < 10; ++i) a.prof[(crank * a.warps + wl) * 10 + i] = (unsigned long long)w.acc[i];
 }
 
@@ -2101,6 +2123,8 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
     a.tab = sp.tab.as<int>();
     a.tab_ptr = sp.tab_ptr.as<int>();
     a.tab_nf = sp.tab_nf.as<int>();
+    a.tab_band = sp.tab_band.as<int>();
+    a.tab_band_ptr = sp.tab_band_ptr.as<int>();
     a.tab_ints = sp.tab_ints;
   }
   a.nlevels = p.nlevels;

@@ -14,52 +14,79 @@
 
 namespace stmhd {
 
-template <int G>
-__global__ void __launch_bounds__(256) spmv_kernel(SpmvArgs a) {
+// A CTA covers `sb` consecutive slabs of its rows (grid.y = slab blocks), U of them
+// interleaved per thread so U gathers are in flight per entry (a launch of nrows x
+// nslab small CTAs, one slab per thread, was bound by the beg -> col -> x chain of
+// L2 round trips).  Per slab the arithmetic is that of one group of G lanes
+// (strided partial sums, then the butterfly), so results do not depend on U or sb.
+template <int G, int U>
+__global__ void __launch_bounds__(256) spmv_kernel(SpmvArgs a, int sb) {
   const int lane = threadIdx.x % G;
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const int k = a.kbeg + blockIdx.y;
   const bool valid = r < a.nrows;  // keep the warp converged for the shuffles
-  double acc = 0.0;
+  const int kend = min(a.kbeg + a.nslab, a.kbeg + (int)blockIdx.y * sb + sb);
+  for (int k0 = a.kbeg + blockIdx.y * sb; k0 < kend; k0 += U) {
+    double acc[U];
 #pragma unroll
-  for (int ti = 0; ti < 4; ++ti) {
-    if (ti >= a.nterms || !valid) break;
-    const SpTerm &t = a.t[ti];
-    const int kx = k - t.lag;
-    if (kx < 0) continue;
-    const int b = t.beg[r];
-    const int e = t.end ? t.end[r] : t.beg[r + 1];
-    const double *v = t.val + (int64_t)(k - t.val_shift) * t.val_stride;
-    const double *x = t.x + (int64_t)kx * t.x_stride - t.col_off;
-    double s = 0.0;
-    if (t.rel) {
-      const int64_t base = (int64_t)kx * t.x_stride;
-      for (int q = b + lane; q < e; q += G) {
-        int c = t.col[q];
-        if (base + c - t.col_off >= 0) s += v[q] * x[c];
+    for (int u = 0; u < U; ++u) acc[u] = 0.0;
+#pragma unroll
+    for (int ti = 0; ti < 4; ++ti) {
+      if (ti >= a.nterms || !valid) break;
+      const SpTerm &t = a.t[ti];
+      const int b = t.beg[r];
+      const int e = t.end ? t.end[r] : t.beg[r + 1];
+      const double *v[U];
+      const double *x[U];
+      bool on[U];
+      int64_t base[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u, kx = k - t.lag;
+        on[u] = k < kend && kx >= 0;
+        v[u] = t.val + (int64_t)(k - t.val_shift) * t.val_stride;
+        x[u] = t.x + (int64_t)kx * t.x_stride - t.col_off;
+        base[u] = (int64_t)kx * t.x_stride - t.col_off;
       }
-    } else {
-      for (int q = b + lane; q < e; q += G) s += v[q] * x[t.col[q]];
+      double sacc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) sacc[u] = 0.0;
+      for (int q = b + lane; q < e; q += G) {
+        const int c = t.col[q];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (on[u] && (!t.rel || base[u] + c >= 0)) sacc[u] += v[u][q] * x[u][c];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (on[u]) acc[u] += t.alpha * sacc[u];
     }
-    acc += t.alpha * s;
-  }
-  acc = group_sum<G>(acc);
-  if (lane == 0 && valid) {
-    double out = acc;
-    if (a.z) out += a.beta * a.z[(int64_t)k * a.z_stride + r];
-    a.y[(int64_t)k * a.y_stride + r] = out;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double sum = group_sum<G>(acc[u]);
+      const int k = k0 + u;
+      if (lane == 0 && valid && k < kend) {
+        double out = sum;
+        if (a.z) out += a.beta * a.z[(int64_t)k * a.z_stride + r];
+        a.y[(int64_t)k * a.y_stride + r] = out;
+      }
+    }
   }
 }
 
 void spmv(const SpmvArgs &a, cudaStream_t s, int group) {
   if (a.nrows <= 0 || a.nslab <= 0) return;
   const int threads = 256;
-  dim3 grid(cdiv((int64_t)a.nrows * group, threads), a.nslab);
+  const int64_t gx = cdiv((int64_t)a.nrows * group, threads);
+  // slabs per CTA: keep >= ~16 CTAs per SM in flight
+  const int64_t want = (int64_t)num_sms() * 16;
+  int sb = (int)std::max<int64_t>(1, std::min<int64_t>(16, gx * a.nslab / want));
+  const int nby = (int)((a.nslab + sb - 1) / sb);
+  dim3 grid(gx, nby);
   switch (group) {
-    case 4: spmv_kernel<4><<<grid, threads, 0, s>>>(a); break;
-    case 8: spmv_kernel<8><<<grid, threads, 0, s>>>(a); break;
-    case 16: spmv_kernel<16><<<grid, threads, 0, s>>>(a); break;
-    default: spmv_kernel<32><<<grid, threads, 0, s>>>(a); break;
+    case 4: spmv_kernel<4, 4><<<grid, threads, 0, s>>>(a, sb); break;
+    case 8: spmv_kernel<8, 4><<<grid, threads, 0, s>>>(a, sb); break;
+    case 16: spmv_kernel<16, 4><<<grid, threads, 0, s>>>(a, sb); break;
+    default: spmv_kernel<32, 4><<<grid, threads, 0, s>>>(a, sb); break;
   }
   STMHD_LAUNCH_CHECK();
 }
