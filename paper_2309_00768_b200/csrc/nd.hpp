@@ -120,6 +120,7 @@ struct NDSweepPlan {
   DevBuf tidx;              // n: top index of a permuted position, or -1
   DevBuf tsn, tchild;       // top supernodes (postorder) and their top children (K construction)
   int ntsn = 0;
+  int kfmax = 1;            // largest front among the top (K region) supernodes
   int64_t tcb_total = 0;    // sum of nb over top supernodes
   // per-CTA subtree front tables kept in shared memory (dense mode): ints per CTA
   // block [tab_ptr[c], tab_ptr[c+1]): forward int32 entries, then backward uint16 pairs

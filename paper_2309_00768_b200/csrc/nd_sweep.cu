@@ -642,6 +642,8 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     if (tch.empty()) tch.push_back(make_int4(0, 0, 0, 0));
     sp->ntsn = (int)tsn.size();
     sp->tcb_total = tcb;
+    sp->kfmax = 1;
+    for (const TopSN &t : tsn) sp->kfmax = std::max(sp->kfmax, t.ns + t.nb);
     sp->tsn = upload_vec(tsn, s);
     sp->tchild = upload_vec(tch, s);
   }
@@ -1932,14 +1934,172 @@ __global__ void __launch_bounds__(256 * NC) topk_kernel(TopKArgs g) {
   }
 }
 
+// Tensor-core variant (FP64 mma.sync.m8n8k4): the same column pushes, 64 columns per
+// item, each warp computing 8-row x 64-column tiles of FL V / FU V (one factor load
+// per lane and k-step feeds 8 MMAs; the front block V is [row][kVS] in shared memory,
+// row stride 72 doubles so the B-fragment loads of a k-step take two wavefronts).
+// Identical operations up to the summation order inside each dot product.
+constexpr int kVS = 72;
+
+// acc[j] += blk rows r0..r0+7 (x K) . V[:, 8j .. 8j+7]; lane holds C(row lane/4,
+// cols 8j + 2(lane%4) + {0,1}).  blk is stored as row chunks [K][R].
+__device__ __forceinline__ void topk_mma_tile(const double *__restrict__ blk, int R, int bsz, int r0, int nrows, int K,
+                                              const double *V, int lane, double (&acc)[8][2]) {
+  const int ar = r0 + (lane >> 2), kq = lane & 3;
+  const bool rok = ar < nrows;
+  const double *arow = blk + (int64_t)((rok ? ar : 0) / R) * bsz + ((rok ? ar : 0) % R);
+  const double *vb = V + kq * kVS + (lane >> 2);
+  int k = 0;
+  const int k16 = K & ~15;
+  double an[4];  // next k-block's A fragments, loaded one block ahead
+#pragma unroll
+  for (int s4 = 0; s4 < 4; ++s4) an[s4] = (rok && k16 > 0) ? __ldg(arow + (int64_t)(4 * s4 + kq) * R) : 0.0;
+  for (; k < k16; k += 16) {
+    double a[4];
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4) {
+      a[s4] = an[s4];
+      an[s4] = (rok && k + 16 < k16) ? __ldg(arow + (int64_t)(k + 16 + 4 * s4 + kq) * R) : 0.0;
+    }
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4) {
+      const double *vk = vb + (k + 4 * s4) * kVS;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double b = vk[8 * j];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[j][0]), "+d"(acc[j][1])
+                     : "d"(a[s4]), "d"(b));
+      }
+    }
+  }
+  for (; k < K; k += 4) {
+    const bool kok = k + kq < K;
+    const double a = (rok && kok) ? __ldg(arow + (int64_t)(k + kq) * R) : 0.0;
+    const double *vk = vb + k * kVS;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double b = kok ? vk[8 * j] : 0.0;
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(acc[j][0]), "+d"(acc[j][1])
+                   : "d"(a), "d"(b));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512) topk_mma_kernel(TopKArgs g) {
+  constexpr int CS = 64;
+  extern __shared__ __align__(16) double V[];  // front x kVS
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double *Xw = g.scratch + (int64_t)blockIdx.x * g.scr_stride;
+  double *CBw = Xw + (int64_t)g.nT * CS;
+  const int nitems = g.nbatch * g.ncb;
+  const int crow = lane >> 2, ccol = 2 * (lane & 3);
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int b = item / g.ncb, col0 = (item % g.ncb) * CS;
+    const double *F = g.factors + (int64_t)b * g.fstride;
+    for (int si = 0; si < g.ntsn; ++si) {  // forward, postorder
+      const TopSN t = g.tsn[si];
+      const int f = t.ns + t.nb;
+      // (row, 8-column group) per thread: one index load per row, 8 contiguous values
+      // per thread with all loads of a row in flight
+      for (int e = threadIdx.x; e < f * 8; e += blockDim.x) {
+        const int r = e >> 3, c0 = (e & 7) * 8;
+        const int ti = r < t.ns ? g.tidx[t.first + r] : -1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) V[r * kVS + c0 + q] = (ti == col0 + c0 + q) ? 1.0 : 0.0;
+      }
+      __syncthreads();
+      for (int c = 0; c < t.nchild; ++c) {  // extend-add the top children's updates
+        const int4 ch = g.tchild[t.child0 + c];
+        const int cb0 = g.tsn[ch.x].tcb_off;
+        for (int e = threadIdx.x; e < ch.z * 8; e += blockDim.x) {
+          const int a = e >> 3, c0 = (e & 7) * 8;
+          const double2 *src = reinterpret_cast<const double2 *>(CBw + (int64_t)(cb0 + a) * CS + c0);
+          double2 vv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) vv[q] = src[q];
+          double *dst = V + g.emap[ch.y + a] * kVS + c0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            dst[2 * q] += vv[q].x;
+            dst[2 * q + 1] += vv[q].y;
+          }
+        }
+        __syncthreads();
+      }
+      for (int r0 = wl * 8; r0 < f; r0 += nw * 8) {
+        double acc[8][2];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+        topk_mma_tile(F + t.fl_off, t.rf, t.bszf, r0, f, t.ns, V, lane, acc);
+        const int r = r0 + crow;
+        if (r < f) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int c = 8 * j + ccol + i;
+              if (r < t.ns) Xw[(int64_t)g.tidx[t.first + r] * CS + c] = acc[j][i];  // y
+              else CBw[(int64_t)(t.tcb_off + r - t.ns) * CS + c] = V[r * kVS + c] - acc[j][i];
+            }
+        }
+      }
+      __syncthreads();
+    }
+    for (int si = g.ntsn - 1; si >= 0; --si) {  // backward, reverse postorder
+      const TopSN t = g.tsn[si];
+      const int f = t.ns + t.nb;
+      for (int e = threadIdx.x; e < f * 8; e += blockDim.x) {
+        const int r = e >> 3, c0 = (e & 7) * 8;
+        const int pos = r < t.ns ? t.first + r : g.bpos[t.goff + r];
+        const double2 *src = reinterpret_cast<const double2 *>(Xw + (int64_t)g.tidx[pos] * CS + c0);
+        double2 vv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) vv[q] = src[q];  // own y, or the ancestors' x
+        double2 *dst = reinterpret_cast<double2 *>(V + r * kVS + c0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = vv[q];
+      }
+      __syncthreads();
+      for (int k0 = wl * 8; k0 < t.ns; k0 += nw * 8) {
+        double acc[8][2];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+        topk_mma_tile(F + t.fu_off, t.rb, t.bszb, k0, t.ns, f, V, lane, acc);
+        const int r = k0 + crow;
+        if (r < t.ns)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) Xw[(int64_t)g.tidx[t.first + r] * CS + 8 * j + ccol + i] = acc[j][i];
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < g.nT * 8; e += blockDim.x) {  // row groups of kr: [group][col][kr]
+      const int i = e >> 3, c0 = (e & 7) * 8;
+      const double2 *src = reinterpret_cast<const double2 *>(Xw + (int64_t)i * CS + c0);
+      double2 vv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) vv[q] = src[q];
+      double *kb = g.K + (int64_t)b * g.kstride + (int64_t)(i - i % g.kr) * g.kpad + i % g.kr;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (col0 + c0 + 2 * q < g.nT) kb[(int64_t)(col0 + c0 + 2 * q) * g.kr] = vv[q].x;
+        if (col0 + c0 + 2 * q + 1 < g.nT) kb[(int64_t)(col0 + c0 + 2 * q + 1) * g.kr] = vv[q].y;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 static void build_dense_top(const NDFactor &fac, const NDSweepPlan &sp, cudaStream_t s) {
   const NDPlan &p = *fac.dev->plan;
   const int64_t kstride = sp.kstride();
   const size_t kbytes = (size_t)fac.nbatch * kstride * sizeof(double);
   if (fac.ktop.bytes != kbytes) fac.ktop.alloc_async(kbytes, s);
   STMHD_CUDA_CHECK(cudaMemsetAsync(fac.ktop.ptr, 0, kbytes, s));  // padded columns stay zero
-  int fmax = 1;
-  for (int sn = 0; sn < p.nsn; ++sn) fmax = std::max(fmax, p.ns[sn] + p.nb[sn]);
+  const int fmax = sp.kfmax;  // largest front of the K region (the only fronts staged here)
   TopKArgs g{};
   g.tsn = sp.tsn.as<TopSN>();
   g.tchild = sp.tchild.as<int4>();
@@ -1956,12 +2116,16 @@ static void build_dense_top(const NDFactor &fac, const NDSweepPlan &sp, cudaStre
   // NC column halves per lane (STMHD_TOPK_NC, 1 or 2): each factor load feeds 32 NC
   // columns; NC = 2 runs 16 warps per CTA with the wider front block when it fits
   static const int nc_env = env_int2("STMHD_TOPK_NC", 2);
+  // FP64 tensor-core construction (STMHD_TOPK_MMA, default on): 64 columns per item
+  static const int mma_env = env_int2("STMHD_TOPK_MMA", 1);
   int nc = nc_env == 1 ? 1 : 2;
+  if (mma_env) nc = 2;
   if ((size_t)fmax * 64 * sizeof(double) > 200 * 1024) nc = 1;
   const int cs = 32 * nc;
   g.ncb = (sp.ntT + cs - 1) / cs;
-  const size_t smem = (size_t)fmax * cs * sizeof(double);
-  require(smem <= 200 * 1024, "dense top: front too large");
+  const bool use_mma = mma_env && (size_t)fmax * kVS * sizeof(double) <= 226 * 1024;
+  const size_t smem = (size_t)fmax * (use_mma ? kVS : cs) * sizeof(double);
+  require(smem <= 226 * 1024, "dense top: front too large");
   // one 16-warp CTA per SM for NC = 2 (two 8-warp CTAs for NC = 1): the same warps per
   // SM and the same scratch footprint (a larger pooled scratch was measured to slow the
   // next factorisation's workspace allocations)
@@ -1974,16 +2138,19 @@ static void build_dense_top(const NDFactor &fac, const NDSweepPlan &sp, cudaStre
   g.scratch = scr.as<double>();
   g.K = fac.ktop.as<double>();
   g.kstride = kstride;
-  static size_t attr[2] = {0, 0};
-  const void *fn = nc == 2 ? (const void *)topk_kernel<2> : (const void *)topk_kernel<1>;
-  if (smem > attr[nc - 1]) {
+  static size_t attr[3] = {0, 0, 0};
+  const int ai = use_mma ? 2 : nc - 1;
+  const void *fn = use_mma ? (const void *)topk_mma_kernel
+                           : (nc == 2 ? (const void *)topk_kernel<2> : (const void *)topk_kernel<1>);
+  if (smem > attr[ai]) {
     STMHD_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr[nc - 1] = smem;
+    attr[ai] = smem;
   }
   if (getenv("STMHD_SWEEP_PLAN_INFO"))
     fprintf(stderr, "[topk] n=%lld nT=%d nbatch=%d plan ncta=%d warps=%d gen=%llu items=%d grid=%d\n", (long long)p.n,
             sp.ntT, fac.nbatch, sp.ncta, sp.warps, (unsigned long long)fac.gen, nitems, grid);
-  if (nc == 2) topk_kernel<2><<<grid, 512, smem, s>>>(g);
+  if (use_mma) topk_mma_kernel<<<grid, 512, smem, s>>>(g);
+  else if (nc == 2) topk_kernel<2><<<grid, 512, smem, s>>>(g);
   else topk_kernel<1><<<grid, 256, smem, s>>>(g);
   STMHD_LAUNCH_CHECK();
   fac.ktop_plan = &sp;

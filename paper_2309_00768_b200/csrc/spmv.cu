@@ -77,8 +77,8 @@ void spmv(const SpmvArgs &a, cudaStream_t s, int group) {
   if (a.nrows <= 0 || a.nslab <= 0) return;
   const int threads = 256;
   const int64_t gx = cdiv((int64_t)a.nrows * group, threads);
-  // slabs per CTA: keep >= ~16 CTAs per SM in flight
-  const int64_t want = (int64_t)num_sms() * 16;
+  // slabs per CTA: keep >= ~64 CTAs per SM worth of work (8 resident at a time)
+  const int64_t want = (int64_t)num_sms() * 64;
   int sb = (int)std::max<int64_t>(1, std::min<int64_t>(16, gx * a.nslab / want));
   const int nby = (int)((a.nslab + sb - 1) / sb);
   dim3 grid(gx, nby);
