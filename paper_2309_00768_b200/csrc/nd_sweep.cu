@@ -821,13 +821,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
   } while (!done);
 }
 
+// This CTA's band positions (global; 0xC000 backward-table codes).  Kept in shared
+// memory, not in SubView: the sweep kernel sits at its register cap and every pointer
+// held across the slab loop spills.
+__shared__ const int *s_bband;
+
 // Per-CTA view of the subtree vectors kept in shared memory.
 struct SubView {
   double *ys, *xs, *cbs, *rhs_s;  // rhs_s: coupled right-hand side of the subtree rows (fused mode)
   double *zs;                     // dense top: z_T (kpad doubles); x_T during the subtree backward
   const int *ftab;                // subtree forward tables (shared memory) or null
   const unsigned short *btab;     // subtree backward tables
-  const int *bband;               // this CTA's band positions (global; 0xC000 table codes)
   int64_t first, len, cbfirst;
 };
 
@@ -1061,14 +1065,27 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
     // shared-memory front: own y, own-subtree x (xs) or top x (staged in zs)
     const unsigned short *bt = sv.btab + tk.cboff - tk.ns;
     const double *ys = sv.ys - sv.first + tk.first;
-    for (int t = lane; t < tk.f; t += 32) {
-      double v;
-      if (t < tk.ns) v = ys[t];
-      else {
-        const unsigned code = bt[t];
-        v = (code & 0x8000u) ? ((code & 0x4000u) ? x[sv.bband[code & 0x3fffu]] : sv.zs[code & 0x3fffu]) : sv.xs[code];
+    if (a.ntop == 0) {  // no band levels: own subtree or K only (keeps this loop lean)
+      for (int t = lane; t < tk.f; t += 32) {
+        double v;
+        if (t < tk.ns) v = ys[t];
+        else {
+          const unsigned code = bt[t];
+          v = (code & 0x8000u) ? sv.zs[code & 0x3fffu] : sv.xs[code];
+        }
+        w.v[t] = v;
       }
-      w.v[t] = v;
+    } else {
+      for (int t = lane; t < tk.f; t += 32) {
+        double v;
+        if (t < tk.ns) v = ys[t];
+        else {
+          const unsigned code = bt[t];
+          v = (code & 0x8000u) ? ((code & 0x4000u) ? x[s_bband[code & 0x3fffu]] : sv.zs[code & 0x3fffu])
+                               : sv.xs[code];
+        }
+        w.v[t] = v;
+      }
     }
     __syncwarp();
   }
@@ -1387,14 +1404,13 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   sv.zs = sv.rhs_s + a.sub_len;
   sv.ftab = nullptr;
   sv.btab = nullptr;
-  sv.bband = nullptr;
   if (a.tab_ints) {  // this CTA's subtree front tables, resident for the whole launch
     int *tb = reinterpret_cast<int *>((reinterpret_cast<uintptr_t>(sv.zs + a.zlen) + 15) & ~(uintptr_t)15);
     const int o = a.tab_ptr[crank], nt = a.tab_ptr[crank + 1] - o;
     for (int i = threadIdx.x; i < nt; i += blockDim.x) tb[i] = a.tab[o + i];
     sv.ftab = tb;
     sv.btab = reinterpret_cast<const unsigned short *>(tb + a.tab_nf[crank]);
-    sv.bband = a.tab_band + a.tab_band_ptr[crank];
+    if (threadIdx.x == 0) s_bband = a.tab_band + a.tab_band_ptr[crank];
     __syncthreads();
   }
   sv.first = a.sub_info[4 * crank + 0];
@@ -1471,10 +1487,14 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
            t += blockDim.x) {
         const int e = t < a.ext_ncta[0] ? 0 : 1, c = e ? t - a.ext_ncta[0] : t;
         const int *f = a.flag_in[e] + (int64_t)k * a.ext_ncta[e] + c;
-        if (ld_acquire_gpu(f) != a.epoch && !*(volatile int *)a.fault) {
+        if (ld_acquire_gpu(f) != a.epoch) {
+          // the poll loop is on the critical path of every slab: only the flag load per
+          // iteration; the clock and the fault word are checked every 256 polls
           unsigned long long t0, t1;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-          while (ld_acquire_gpu(f) != a.epoch) {
+          for (unsigned it = 1; ld_acquire_gpu(f) != a.epoch; ++it) {
+            if (it & 255u) continue;
+            if (*(volatile int *)a.fault) break;  // an earlier wait already gave up
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
             if (t1 - t0 > 4000000000ull) {
               // 4 s: a producer is not running (not co-resident).  Record the fault
@@ -1485,7 +1505,6 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
               __threadfence_system();
               break;
             }
-            if (*(volatile int *)a.fault) break;
           }
         }
       }

@@ -82,11 +82,20 @@ void spmv(const SpmvArgs &a, cudaStream_t s, int group) {
   int sb = (int)std::max<int64_t>(1, std::min<int64_t>(16, gx * a.nslab / want));
   const int nby = (int)((a.nslab + sb - 1) / sb);
   dim3 grid(gx, nby);
-  switch (group) {
-    case 4: spmv_kernel<4, 4><<<grid, threads, 0, s>>>(a, sb); break;
-    case 8: spmv_kernel<8, 4><<<grid, threads, 0, s>>>(a, sb); break;
-    case 16: spmv_kernel<16, 4><<<grid, threads, 0, s>>>(a, sb); break;
-    default: spmv_kernel<32, 4><<<grid, threads, 0, s>>>(a, sb); break;
+  if (sb == 1) {  // one slab per CTA (small batches): no interleaving
+    switch (group) {
+      case 4: spmv_kernel<4, 1><<<grid, threads, 0, s>>>(a, sb); break;
+      case 8: spmv_kernel<8, 1><<<grid, threads, 0, s>>>(a, sb); break;
+      case 16: spmv_kernel<16, 1><<<grid, threads, 0, s>>>(a, sb); break;
+      default: spmv_kernel<32, 1><<<grid, threads, 0, s>>>(a, sb); break;
+    }
+  } else {
+    switch (group) {
+      case 4: spmv_kernel<4, 4><<<grid, threads, 0, s>>>(a, sb); break;
+      case 8: spmv_kernel<8, 4><<<grid, threads, 0, s>>>(a, sb); break;
+      case 16: spmv_kernel<16, 4><<<grid, threads, 0, s>>>(a, sb); break;
+      default: spmv_kernel<32, 4><<<grid, threads, 0, s>>>(a, sb); break;
+    }
   }
   STMHD_LAUNCH_CHECK();
 }
