@@ -164,6 +164,12 @@ def host_info():
     return {"cpu": cpu, "nproc": os.cpu_count()}
 
 
+# Unmodified reference over the port's extrapolation, measured on full solves on one
+# core of the build container (profiles/r02_cpu_calibration.json): C4_64 1.669 (the
+# factor used: same 64^2 mesh as C4_512), C2 1.711.
+CAL_FACTOR = 1.669
+
+
 def extrapolate(sample, nt_full, gmres_iters):
     """Full-solve CPU seconds from a slab-prefix sample.  Every per-slab cost of the
     reference is linear in the slab count (causal block structure: residual, Jacobian,
@@ -181,7 +187,9 @@ def sample_text(smp, nt_full, counts, t_full):
             f"to one core) on the {CONFIG} mesh restricted to its first {smp['slabs']} of {nt_full} slabs: "
             f"residual + Jacobian + P_T setup + {smp['iters']} FGMRES(50) iterations "
             f"({smp['t_iter'] * 1e3:.0f} ms each); per-op times x{nt_full // smp['slabs']} with the counts "
-            f"{counts} -> {t_full:.0f} s per solve (EXTRAPOLATED)")
+            f"{counts} -> {t_full:.0f} s per solve, x{CAL_FACTOR} calibration to the unmodified reference "
+            f"(full C4_64/C2 solves, profiles/r02_cpu_calibration.json) -> {t_full * CAL_FACTOR:.0f} s "
+            f"(EXTRAPOLATED)")
 
 
 # ---------------------------------------------------------------------------------
@@ -200,13 +208,15 @@ def run_reference(args, rank, world):
     for k in ("t_residual", "t_jacobian", "t_pc_setup", "t_iter"):
         agg[k] = statistics.median(s[k] for s in samples)
     t_full, value = extrapolate(agg, NT_FULL, REF_GMRES)
+    value /= CAL_FACTOR
     line = {
         "impl": "reference", "metric": METRIC,
         "value": value, "unit": "FGMRES it/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE C4 analytic problem)",
         "config": {"workload": WORKLOAD, "l2": "n/a (CPU)"},
-        "newton_solve_s_extrapolated": t_full,
+        "newton_solve_s_extrapolated": t_full * CAL_FACTOR,
+        "port_extrapolated_s_uncalibrated": t_full,
         "cpu_baseline": {"value": value, "unit": "FGMRES it/s", "cores": 1, "kind": "port",
                          "sample": sample_text(agg, NT_FULL, REF_GMRES, t_full) + "; one sample per step",
                          "host": host_info()},
@@ -496,12 +506,14 @@ def run_ours(args, rank, world):
         try:
             smp = cpu_sample()
             t_full, cv = extrapolate(smp, nt, stats_last.gmres_iters)
+            cv /= CAL_FACTOR
             line["cpu_baseline"] = {"value": cv, "unit": "FGMRES it/s", "cores": 1, "kind": "port",
                                     "sample": sample_text(smp, nt, stats_last.gmres_iters, t_full),
                                     "host": host_info(),
-                                    "calibration": "unmodified reference, full C2 solve on one core of the build "
-                                                   "container: 737.7 s, counts [458, 413] "
-                                                   "(tests/golden/cfg_c2.npz times_json)"}
+                                    "calibration": {"factor": CAL_FACTOR, "file": "profiles/r02_cpu_calibration.json",
+                                                    "points": "unmodified reference full solves on one core of "
+                                                              "the build container: C2 737.7 s [458, 413], C4_64 "
+                                                              "939.9 s [96, 89]"}}
         except Exception as exc:  # keep the GPU line even if the CPU sample fails
             line["cpu_baseline"] = {"value": None, "unit": "FGMRES it/s", "cores": 1, "kind": "port",
                                     "sample": f"failed: {exc}"[:300]}
