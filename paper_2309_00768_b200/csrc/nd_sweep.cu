@@ -23,6 +23,7 @@
 // the nested-dissection ordering, permuted in and out around the launch.
 #include <algorithm>
 #include <array>
+#include <climits>
 #include <cstdlib>
 #include <map>
 
@@ -721,7 +722,13 @@ struct SweepArgs {
   const int *flag_in[2];  // per producer: [slab][cta] = epoch once slab written
   int ext_ncta[2];        // per producer: its CTA count
   int nwait;
-  int *flag_out;          // this stage's flags (null: not consumed)
+  int *flag_out;          // this stage's flags (null: not consumed and not early coupling)
+  // early coupling (grid mode with CTAs that own no subtree): a subtree CTA computes the
+  // coupled right-hand side of its own rows for slab k+1 right after its subtree
+  // backward of slab k (its rows couple only to its own subtree and to separator
+  // nodes, all final by then), with no grid barrier at the slab end; the CTAs without
+  // a subtree compute the top rows after the subtree CTAs published slab k
+  int early_cpl, nroots;
   int epoch;
   int vstride;  // doubles per warp: gather buffer + 2 TMA slots
   int slot;     // doubles per TMA slot (largest chunk block)
@@ -1451,6 +1458,8 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   __syncwarp();
   const int64_t n = a.n;
   int step = 0;
+  const bool early = a.early_cpl && !a.post_hdr && a.prog_hdr;
+  const bool has_sub = sv.len > 0;
   sweep_trace(a, step, crank);
   for (int k = 0; k < a.nslab; ++k) {
     const double *rhs = a.rhsp + (int64_t)k * n;
@@ -1473,7 +1482,8 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       // fused coupling (CTA-local): rhs_k + sum_c coef_c C_c src_c for this CTA's items.
       // Sources by id: 0 x_{k-1}, 1 x_{k-1} of the own subtree (shared memory),
       // 2 x_{k-2}, 3/4 external stages' outputs at slab k; sources that do not exist
-      // yet read zeros.
+      // yet read zeros.  (Early coupling: a subtree CTA arrives here straight from its
+      // subtree backward of slab k-1, with no grid barrier in between.)
       if (threadIdx.x == 0) {
         s_src[0] = k >= 1 ? a.xp + (int64_t)(k - 1) * n : a.zero;
         s_src[1] = k >= 1 ? (const double *)sv.xs : a.zero;
@@ -1482,11 +1492,19 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
         s_src[4] = a.ext_xp[1] ? a.ext_xp[1] + (int64_t)k * a.ext_n[1] : a.zero;
         s_src[5] = s_src[6] = s_src[7] = a.zero;  // 5: own x_k (post-slab program only)
       }
-      // pipelined launch: wait until every CTA of each producer has published slab k
-      for (int t = threadIdx.x; t < (a.nwait > 0 ? a.ext_ncta[0] : 0) + (a.nwait > 1 ? a.ext_ncta[1] : 0);
-           t += blockDim.x) {
-        const int e = t < a.ext_ncta[0] ? 0 : 1, c = e ? t - a.ext_ncta[0] : t;
-        const int *f = a.flag_in[e] + (int64_t)k * a.ext_ncta[e] + c;
+      // wait until every CTA of each producer has published slab k (pipelined launch),
+      // and, for a CTA without a subtree in early mode, until every subtree CTA of this
+      // stage has published slab k-1
+      const int nprod = (a.nwait > 0 ? a.ext_ncta[0] : 0) + (a.nwait > 1 ? a.ext_ncta[1] : 0);
+      const int nsubw = (early && !has_sub && k >= 1) ? a.nroots : 0;
+      for (int t = threadIdx.x; t < nprod + nsubw; t += blockDim.x) {
+        const int *f;
+        if (t < nprod) {
+          const int e = t < a.ext_ncta[0] ? 0 : 1, c = e ? t - a.ext_ncta[0] : t;
+          f = a.flag_in[e] + (int64_t)k * a.ext_ncta[e] + c;
+        } else {
+          f = a.flag_out + (int64_t)(k - 1) * a.ncta + (t - nprod);
+        }
         if (ld_acquire_gpu(f) != a.epoch) {
           // the poll loop is on the critical path of every slab: only the flag load per
           // iteration; the clock and the fault word are checked every 256 polls
@@ -1625,12 +1643,17 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       run_program<1>(a.post_hdr[crank], a.post_items, a.post_ecol, vk, nullptr, a.post_out + (int64_t)k * a.post_n,
                      sv, nullptr, s_src);
     }
-    if (a.flag_out) {  // pipelined launch: publish this CTA's part of x_k at gpu scope
+    if (a.flag_out) {  // publish this CTA's part of x_k at gpu scope (consumers, early coupling)
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) st_release_gpu(a.flag_out + (int64_t)k * a.ncta + crank, a.epoch);
     }
-    if (a.nsub && k + 1 < a.nslab) {  // x_k visible to every CTA's next coupling
+    if (early) {
+      // no grid barrier: a subtree CTA's next coupling reads only its own x_k (shared
+      // memory) and separator values final since the band levels; the CTAs without a
+      // subtree wait for the subtree CTAs' flags before coupling the top rows
+      if (k + 1 < a.nslab) sweep_trace(a, step, crank);
+    } else if (a.nsub && k + 1 < a.nslab) {  // x_k visible to every CTA's next coupling
       tb = pclock<PROF>(); sweep_barrier(a, crank, gphase); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step, crank);
     }
@@ -1731,8 +1754,13 @@ static const CplProgram &get_program(const NDSweepPlan &sp, const NDPlan &p, con
     entries_of(q, itm, o);
     items[o].push_back(std::move(itm));
   }
-  std::vector<int> load(ncta);  // top rows -> balanced over the CTAs (tbuf)
-  for (int c = 0; c < ncta; ++c) load[c] = (int)items[c].size();
+  // top rows -> balanced over the CTAs (tbuf); only over the CTAs that own no subtree
+  // when there are some (the early-coupling schedule relies on it)
+  std::vector<int> load(ncta);
+  bool idle = false;
+  for (int c = 0; c < ncta; ++c) idle |= sp.sub_info_h[4 * c + 1] == 0;
+  for (int c = 0; c < ncta; ++c)
+    load[c] = (idle && sp.sub_info_h[4 * c + 1] > 0) ? INT_MAX / 2 : (int)items[c].size();
   for (int64_t q : top_rows) {
     const int d = (int)(std::min_element(load.begin(), load.end()) - load.begin());
     ++load[d];
@@ -2370,6 +2398,13 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   a.kpref = env_int2("STMHD_SWEEP_KPREF", 0);  // measured: no gain (dense step not HBM-latency bound)
   a.post_hdr = nullptr;  // set by sweep_stage_set_post for this launch
   a.gbar = nullptr;
+  {
+    static const int early_env = env_int2("STMHD_SWEEP_EARLY_CPL", 1);
+    int nroots = 0;
+    for (int c = 0; c < ncta; ++c) nroots += sp.sub_info_h[4 * c + 1] > 0;
+    a.nroots = nroots;
+    a.early_cpl = early_env && grid && ncpl > 0 && sp.nsub > 0 && nroots > 0 && nroots < ncta;
+  }
   if (grid) {  // grid-family launch: software barrier
     if (!st.gbar.ptr) {
       st.gbar.alloc(sizeof(unsigned));
@@ -2547,7 +2582,7 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
   for (int i = 0; i < nst; ++i) {
     SweepStage &st = *stg[i];
     st.a.epoch = epoch;
-    if (nst > 1) {  // every stage publishes per-slab flags
+    if (nst > 1 || (st.a.early_cpl && !st.a.post_hdr)) {  // per-slab flags (consumers / early coupling)
       const int64_t need = (int64_t)st.nrhs * st.ncta;
       if (st.flags_slabs < need) {
         st.flags.alloc_async(need * sizeof(int), s);
