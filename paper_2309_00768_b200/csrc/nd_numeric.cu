@@ -115,7 +115,7 @@ struct FactorArgs {
   int *status;
 };
 
-__global__ void __launch_bounds__(256) nd_factor_level(FactorArgs a) {
+__global__ void __launch_bounds__(256, 4) nd_factor_level(FactorArgs a) {
   extern __shared__ double smem[];
   __shared__ double red_v[8];
   __shared__ int red_i[8];
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(256) nd_factor_level(FactorArgs a) {
 // front workspace, for the parent's extend-add.
 // Shared layout (doubles): Fs [f*f] | T [ns*ns] (L11^-1 P, then U11^-1) | GEMM tiles
 // [2*GT*GK] | perm (ints).
-__global__ void __launch_bounds__(256) nd_factor_level_smem(FactorArgs a) {
+__global__ void __launch_bounds__(256, 4) nd_factor_level_smem(FactorArgs a) {
   extern __shared__ double smem[];
   __shared__ double red_v[8];
   __shared__ int red_i[8];

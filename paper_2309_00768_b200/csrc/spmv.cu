@@ -73,9 +73,66 @@ __global__ void __launch_bounds__(256) spmv_kernel(SpmvArgs a, int sb) {
   }
 }
 
+// Row per thread, U slabs per thread (large slab batches): consecutive threads take
+// consecutive rows, so every slab's z reads and y writes are coalesced, and each
+// entry issues U gathers at once.  Per slab the entries are summed in row order.
+template <int U>
+__global__ void __launch_bounds__(256) spmv_rows_kernel(SpmvArgs a) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.nrows) return;
+  const int k0 = a.kbeg + blockIdx.y * U, kend = min(a.kbeg + a.nslab, k0 + U);
+  double acc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc[u] = 0.0;
+#pragma unroll
+  for (int ti = 0; ti < 4; ++ti) {
+    if (ti >= a.nterms) break;
+    const SpTerm &t = a.t[ti];
+    const int b = t.beg[r];
+    const int e = t.end ? t.end[r] : t.beg[r + 1];
+    double sacc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) sacc[u] = 0.0;
+    for (int q = b; q < e; ++q) {
+      const int c = t.col[q];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u, kx = k - t.lag;
+        const int64_t xi = (int64_t)kx * t.x_stride + c - t.col_off;
+        if (k < kend && kx >= 0 && (!t.rel || xi >= 0))
+          sacc[u] += t.val[(int64_t)(k - t.val_shift) * t.val_stride + q] * t.x[xi];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k0 + u < kend && k0 + u - t.lag >= 0) acc[u] += t.alpha * sacc[u];
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int k = k0 + u;
+    if (k < kend) {
+      double out = acc[u];
+      if (a.z) out += a.beta * a.z[(int64_t)k * a.z_stride + r];
+      a.y[(int64_t)k * a.y_stride + r] = out;
+    }
+  }
+}
+
 void spmv(const SpmvArgs &a, cudaStream_t s, int group) {
   if (a.nrows <= 0 || a.nslab <= 0) return;
   const int threads = 256;
+  // large slab batches (>= 128 slabs: the 64^2 and C5 configurations): row per thread,
+  // 8 slabs per thread; smaller batches keep the lane-group kernel (and its rounding)
+  static const int rows_min = [] {
+    const char *e = getenv("STMHD_SPMV_ROWS_MIN");
+    return e ? atoi(e) : 128;
+  }();
+  if (a.nslab >= rows_min) {
+    dim3 grid(cdiv((int64_t)a.nrows, threads), (a.nslab + 7) / 8);
+    spmv_rows_kernel<8><<<grid, threads, 0, s>>>(a);
+    STMHD_LAUNCH_CHECK();
+    return;
+  }
   const int64_t gx = cdiv((int64_t)a.nrows * group, threads);
   // slabs per CTA: keep >= ~64 CTAs per SM worth of work (8 resident at a time)
   const int64_t want = (int64_t)num_sms() * 64;
