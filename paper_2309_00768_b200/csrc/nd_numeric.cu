@@ -411,6 +411,178 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level_smem(FactorArgs a) {
   cta_gemm(nb, ns, ns, -1.0, F + ns, f, T, ns, 0.0, FUT + (int64_t)ns * ns, ns, gs, true, false);
 }
 
+// Warp-per-front variant for the small fronts of the bottom levels (f <= 64, ns <= 32):
+// a CTA-wide kernel spends ~5 block barriers per pivot column on fronts this small, so
+// here one warp factors one (front, matrix) pair with __syncwarp only, several pairs
+// per CTA.  Same restricted partial pivoting (largest |entry| in the column among rows
+// col..ns-1, ties to the smaller row); the elimination is the unblocked right-looking
+// form (same operations as the blocked one, in a different order); the inverse-based
+// factors and the contribution block go where the CTA kernels put them.
+// Shared layout per warp (doubles): F [f][fs] (fs = f | 1, odd stride) | T [ns*ns] | perm.
+constexpr int kWarpFrontMax = 64, kWarpFrontNs = 32;
+
+__global__ void __launch_bounds__(256) nd_factor_level_warp(FactorArgs a, int cnt, int nbch, int wstride) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int item = blockIdx.x * (blockDim.x >> 5) + wl;
+  if (item >= cnt * nbch) return;
+  const int s = a.lvl_sn[item % cnt];
+  const int bl = item / cnt;
+  const int b = a.batch0 + bl;
+  const int ns = a.ns[s], nb = a.nb[s], f = ns + nb, fs = f | 1;
+  double *F = smem + (int64_t)wl * wstride;
+  double *T = F + f * fs;
+  const int ts = ns | 1;  // odd column stride of T: lanes on different columns hit different banks
+  int *perm = reinterpret_cast<int *>(T + kWarpFrontNs * (kWarpFrontNs + 1));
+  double *Fg = a.fronts + (int64_t)bl * a.front_size + a.front_off[s];
+  const double *vals = a.values + (int64_t)b * a.value_stride;
+  // 1. zero, scatter, extend-add (children in the fixed order)
+  for (int t = lane; t < f * fs; t += 32) F[t] = 0.0;
+  __syncwarp();
+  {
+    // 8 entries per lane in flight (the value gathers are random accesses into the
+    // matrix; one at a time would serialise on their latency)
+    const int64_t e0 = a.scat_ptr[s], e1 = a.scat_ptr[s + 1];
+    for (int64_t eb = e0 + lane; eb < e1; eb += 256) {
+      int64_t src[8];
+      int dst[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int64_t e = eb + 32 * q;
+        src[q] = e < e1 ? a.scat_src[e] : -1;
+        dst[q] = e < e1 ? (int)a.scat_dst[e] : 0;  // row-major f x f position (< 64^2)
+      }
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = src[q] >= 0 ? vals[src[q]] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (src[q] >= 0) F[(dst[q] / f) * fs + dst[q] % f] = v[q];
+    }
+  }
+  __syncwarp();
+  for (int ci = a.child_ptr[s]; ci < a.child_ptr[s + 1]; ++ci) {
+    const int c = a.child_list[ci];
+    const int nsc = a.ns[c], nbc = a.nb[c], fc = nsc + nbc;
+    const double *Fc = a.fronts + (int64_t)bl * a.front_size + a.front_off[c];
+    const int *em = a.emap + a.emap_off[c];
+    for (int t = lane; t < nbc * nbc; t += 32) {
+      const int i = t / nbc, j = t - i * nbc;
+      F[em[i] * fs + em[j]] += Fc[(int64_t)(nsc + i) * fc + nsc + j];
+    }
+    __syncwarp();
+  }
+  if (lane < ns) perm[lane] = lane;
+  __syncwarp();
+  // 2. LU with pivoting restricted to the ns x ns block, unblocked right-looking
+  for (int col = 0; col < ns; ++col) {
+    double best = -1.0;
+    int bi = col;
+    for (int r = col + lane; r < ns; r += 32) {
+      const double v = fabs(F[r * fs + col]);
+      if (v > best) { best = v; bi = r; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (!(best > 0.0 && isfinite(best))) {
+      if (lane == 0) atomicCAS(a.status, 0, s + 1);
+      return;
+    }
+    if (bi != col) {
+      for (int c = lane; c < f; c += 32) {
+        const double t = F[col * fs + c];
+        F[col * fs + c] = F[bi * fs + c];
+        F[bi * fs + c] = t;
+      }
+      if (lane == 0) {
+        const int t = perm[col];
+        perm[col] = perm[bi];
+        perm[bi] = t;
+      }
+    }
+    __syncwarp();
+    const double inv = 1.0 / F[col * fs + col];
+    for (int r = col + 1 + lane; r < f; r += 32) {
+      const double l = F[r * fs + col] * inv;
+      F[r * fs + col] = l;
+      double *fr = F + r * fs;
+      const double *fc = F + col * fs;
+      int c = col + 1;
+      for (; c + 4 <= f; c += 4) {  // loads of a group first (the rows cannot alias)
+        const double m0 = fc[c], m1 = fc[c + 1], m2 = fc[c + 2], m3 = fc[c + 3];
+        const double v0 = fr[c], v1 = fr[c + 1], v2 = fr[c + 2], v3 = fr[c + 3];
+        fr[c] = v0 - l * m0;
+        fr[c + 1] = v1 - l * m1;
+        fr[c + 2] = v2 - l * m2;
+        fr[c + 3] = v3 - l * m3;
+      }
+      for (; c < f; ++c) fr[c] -= l * fc[c];
+    }
+    __syncwarp();
+  }
+  // 3. contribution block -> global (the parent's extend-add)
+  for (int t = lane; t < nb * nb; t += 32) {
+    const int i = t / nb, j = t - i * nb;
+    Fg[(int64_t)(ns + i) * f + ns + j] = F[(ns + i) * fs + ns + j];
+  }
+  double *FLT = a.stage + (int64_t)bl * a.stage_size + a.sfl_off[s];
+  double *FUT = a.stage + (int64_t)bl * a.stage_size + a.sfu_off[s];
+  // 4a. L11^{-1} P: lane i solves the unit lower system for e_i (column perm[i])
+  if (lane < ns) {
+    const int ci = perm[lane];
+    double *tc = T + ci * ts;
+    for (int r = 0; r < ns; ++r) {
+      double acc = (r == lane) ? 1.0 : 0.0;
+      if (r > lane)
+        for (int k = lane; k < r; ++k) acc -= F[r * fs + k] * tc[k];
+      tc[r] = acc;
+    }
+  }
+  __syncwarp();
+  for (int t = lane; t < ns * ns; t += 32) {
+    const int ci = t / ns, r = t - ci * ns;
+    FLT[(int64_t)ci * f + r] = T[ci * ts + r];
+  }
+  // 4b. G^T = (L11^{-1} P)^T L21^T -> FLT[c*f + ns + i]
+  for (int t = lane; t < ns * nb; t += 32) {
+    const int c = t / nb, i = t - c * nb;
+    double acc = 0.0;
+    for (int k = 0; k < ns; ++k) acc += T[c * ts + k] * F[(ns + i) * fs + k];
+    FLT[(int64_t)c * f + ns + i] = acc;
+  }
+  __syncwarp();
+  // 4c. U11^{-1}: lane j solves for column j (T[j*ns + i], i <= j)
+  if (lane < ns) {
+    double *tj = T + lane * ts;
+    for (int i = ns - 1; i >= 0; --i) {
+      double acc = 0.0;
+      if (i <= lane) {
+        acc = (i == lane) ? 1.0 : 0.0;
+        for (int k = i + 1; k <= lane; ++k) acc -= F[i * fs + k] * tj[k];
+        acc *= 1.0 / F[i * fs + i];
+      }
+      tj[i] = acc;
+    }
+  }
+  __syncwarp();
+  for (int t = lane; t < ns * ns; t += 32) FUT[t] = T[(t / ns) * ts + t % ns];
+  // 4d. (-U11^{-1} U12)^T -> FUT[(ns+i)*ns + j] = -sum_k U12[k][i] U11inv^T[k][j]
+  for (int t = lane; t < nb * ns; t += 32) {
+    const int i = t / ns, j = t - i * ns;
+    double acc = 0.0;
+    for (int k = 0; k < ns; ++k) acc += F[k * fs + ns + i] * T[k * ts + j];
+    FUT[(int64_t)(ns + i) * ns + j] = -acc;
+  }
+}
+
+static size_t factor_warp_smem_per_warp(int f) {
+  return ((size_t)f * (f | 1) + kWarpFrontNs * (kWarpFrontNs + 1)) * sizeof(double) + kWarpFrontNs * sizeof(int) + 16;
+}
+
 // shared-memory bytes of nd_factor_level_smem for a front (f, ns)
 static size_t factor_smem_bytes(int f, int ns) {
   return ((size_t)f * f + (size_t)ns * ns + 2 * GT * GK) * sizeof(double) + (size_t)(ns + 1) * sizeof(int);
@@ -602,6 +774,26 @@ void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s
   }();
   constexpr size_t kFactorSmemMax = 200 * 1024;
   std::vector<size_t> lvl_smem(p.nlevels, 0);
+  // levels of small fronts (f <= 64, ns <= 32): one warp per front (STMHD_FACTOR_WARP=0 off)
+  static const int warp_env = [] {
+    const char *e = getenv("STMHD_FACTOR_WARP");
+    return e ? atoi(e) : 1;
+  }();
+  std::vector<int> lvl_wf(p.nlevels, 0);  // max front of a warp-per-front level, else 0
+  static bool warp_attr = false;
+  for (int l = 0; l < p.nlevels && warp_env; ++l) {
+    int fmx = 0, nsmx = 0;
+    for (int sn : p.level_sn[l]) {
+      fmx = std::max(fmx, p.ns[sn] + p.nb[sn]);
+      nsmx = std::max(nsmx, p.ns[sn]);
+    }
+    if (fmx > 0 && fmx <= kWarpFrontMax && nsmx <= kWarpFrontNs) lvl_wf[l] = fmx;
+  }
+  if (!warp_attr) {
+    STMHD_CUDA_CHECK(cudaFuncSetAttribute(nd_factor_level_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kFactorSmemMax));
+    warp_attr = true;
+  }
   static size_t smem_attr = 0;
   for (int l = 0; l < p.nlevels && smem_env; ++l) {
     size_t need = 0;
@@ -641,7 +833,13 @@ void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s
       a.stage = stage.as<double>();
       a.stage_size = p.stage_size;
       a.status = status.as<int>();
-      if (lvl_smem[l] > 0)
+      if (lvl_wf[l] > 0) {
+        const size_t pw = (factor_warp_smem_per_warp(lvl_wf[l]) + 15) / 16 * 16;
+        const int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, kFactorSmemMax / pw));
+        const int64_t pairs = (int64_t)cnt * nbch;
+        nd_factor_level_warp<<<(unsigned)((pairs + wpc - 1) / wpc), 32 * wpc, pw * wpc, s>>>(a, cnt, nbch,
+                                                                                           (int)(pw / 8));
+      } else if (lvl_smem[l] > 0)
         nd_factor_level_smem<<<dim3(cnt, nbch), 256, lvl_smem[l], s>>>(a);
       else
         nd_factor_level<<<dim3(cnt, nbch), 256, smem, s>>>(a);
