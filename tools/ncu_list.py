@@ -18,12 +18,19 @@ def main():
             d = dict(zip(hdr, r))
             e = launch.setdefault(d["ID"], {"name": d["Kernel Name"]})
             e[d["Metric Name"]] = d["Metric Value"].replace(",", "")
-    if summ:
+    if summ or "--md" in sys.argv:
         tot = collections.defaultdict(lambda: [0, 0.0])
         for v in launch.values():
             t = tot[v["name"].split("(")[0]]
             t[0] += 1
             t[1] += float(v.get("gpu__time_duration.sum", 0)) / 1e3
+        allus = sum(us for _, us in tot.values())
+        if "--md" in sys.argv:
+            print(f"Total {len(launch)} launches, {allus / 1e3:.1f} ms GPU time.\n")
+            print("| share | launches | avg us | kernel |\n|---:|---:|---:|---|")
+            for k, (n, us) in sorted(tot.items(), key=lambda x: -x[1][1]):
+                print(f"| {100 * us / allus:.2f}% | {n} | {us / n:.1f} | `{k}` |")
+            return
         for k, (n, us) in sorted(tot.items(), key=lambda x: -x[1][1]):
             print(f"{us / 1e3:10.3f} ms {n:6d}  {k}")
         return
