@@ -11,7 +11,7 @@ with their Newton relative stop and adds device throughput columns.
 from __future__ import annotations
 
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 from .errors import ConfigurationError, ConvergenceError, StmhdError
 from .linalg import GmresConfig
@@ -20,6 +20,43 @@ from .solver import NewtonConfig, compute_overhead_ratios, solve_all_at_once, so
 
 CSV_HEADER = "problem,dx,dt,T,Nt,mode,newton,avg_gmres,effective_steps,newton_ratio,gmres_ratio,status,wall_s"
 MODES = ("spacetime", "sequential", "both")
+
+
+@dataclass
+class ExperimentConfig:
+    """Sweep configuration with the reference's fields, defaults, validation and
+    Newton/GMRES settings (cli.py:32-65): Newton abs 1e-10, GMRES rel 1e-2 / abs 1e-14."""
+
+    problem: str = "tearing_mode"
+    dx: list = field(default_factory=lambda: [0.25])
+    dt: list = field(default_factory=lambda: [0.25])
+    t_final: list = field(default_factory=lambda: [1.0])
+    mode: str = "spacetime"
+    precond: str = "triangular"
+    out: str = "results.csv"
+    newton_tol: float = 1e-10
+    gmres_rtol: float = 1e-2
+    gmres_atol: float = 1e-14
+    max_newton: int = 25
+    eps: float = 1e-3
+    seed: int = 0  # reserved; the solver itself is deterministic
+
+    def validate(self):
+        if not self.dx or not self.dt or not self.t_final:
+            raise ConfigurationError("dx, dt, and T sweep lists must be nonempty")
+        if self.mode not in MODES:
+            raise ConfigurationError(f"mode must be one of {MODES}, got '{self.mode}'")
+        if any(v <= 0 for v in list(self.dx) + list(self.dt) + list(self.t_final)):
+            raise ConfigurationError("all dx, dt, T values must be positive")
+        for t in self.t_final:
+            if any(dt > t for dt in self.dt):
+                raise ConfigurationError("dt must not exceed T")
+        Variant(self.precond)
+
+    def newton_config(self) -> NewtonConfig:
+        return NewtonConfig(abs_tol=self.newton_tol, max_iters=self.max_newton,
+                            gmres=GmresConfig(rel_tol=self.gmres_rtol, abs_tol=self.gmres_atol),
+                            variant=Variant(self.precond))
 
 
 @dataclass
@@ -84,9 +121,20 @@ def run_cell(problem_name: str, problem, dx: float, dt: float, t_final: float, m
                          gmres_ratio=None, status=f"failed: {exc}", wall_s=0.0)
 
 
-def run_sweep(problem_name: str, problem, dxs, dts, t_finals, mode: str = "spacetime",
+def run_sweep(problem_name, problem=None, dxs=None, dts=None, t_finals=None, mode: str = "spacetime",
               ncfg: NewtonConfig | None = None) -> list[ResultRow]:
-    """Rows ordered dx outer, then dt, then T (reference cli.py:148-162)."""
+    """Rows ordered dx outer, then dt, then T (reference cli.py:148-162).
+
+    ``run_sweep(ExperimentConfig(...))`` is the reference's call (problem by name with
+    the config's eps, its Newton/GMRES settings and variant); the long form takes the
+    problem object, the sweep lists, the mode and a NewtonConfig."""
+    if isinstance(problem_name, ExperimentConfig):
+        from .problems import by_name
+
+        cfg = problem_name
+        cfg.validate()
+        return run_sweep(cfg.problem, by_name(cfg.problem, eps=cfg.eps), cfg.dx, cfg.dt, cfg.t_final, cfg.mode,
+                         cfg.newton_config())
     if not dxs or not dts or not t_finals:
         raise ConfigurationError("dx, dt, and T sweep lists must be nonempty")
     if any(v <= 0 for v in list(dxs) + list(dts) + list(t_finals)):

@@ -26,6 +26,17 @@ def golden():
     return load
 
 
+@pytest.fixture(scope="session")
+def golden_json():
+    import json
+
+    def load(name):
+        with open(os.path.join(GOLDEN, name + ".json")) as fh:
+            return json.load(fh)
+
+    return load
+
+
 def csr_from(g, prefix):
     import scipy.sparse as sp
 

@@ -44,3 +44,39 @@ def test_sweep_cells_on_device():
     assert r.status == "ok" and r.n_steps == 2 and r.newton >= 1 and r.effective_steps >= 1
     assert np.isfinite(r.newton_ratio) and np.isfinite(r.gmres_ratio)
     assert len(r.to_csv().split(",")) == len(ex.CSV_HEADER.split(","))
+
+
+def test_experiment_config_mirrors_reference():
+    cfg = ex.ExperimentConfig()
+    assert (cfg.problem, cfg.dx, cfg.dt, cfg.t_final, cfg.mode, cfg.precond) == (
+        "tearing_mode", [0.25], [0.25], [1.0], "spacetime", "triangular")
+    n = cfg.newton_config()
+    assert (n.abs_tol, n.max_iters, n.gmres.rel_tol, n.gmres.abs_tol) == (1e-10, 25, 1e-2, 1e-14)
+    for bad in (dict(dx=[]), dict(mode="x"), dict(dt=[-1.0]), dict(dt=[2.0]), dict(precond="nope")):
+        with pytest.raises(Exception):
+            ex.ExperimentConfig(**bad).validate()
+
+
+@pytest.mark.gpu
+def test_sweep_rows_match_reference(golden_json):
+    """Rows of the reference's own harness (tests/golden/make_golden_sweep.py: cli.run_sweep
+    with its ExperimentConfig defaults) reproduced by the device solvers: problem, grid,
+    Nt, mode, Newton counts, effective steps and status exactly; the GMRES averages and
+    the overhead ratios within one GMRES iteration per Newton step."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ref = golden_json("sweep_rows")
+    for name, case in ref.items():
+        rows = ex.run_sweep(ex.ExperimentConfig(**case["config"]))
+        assert len(rows) == len(case["rows"]), name
+        for mine, want in zip(rows, case["rows"]):
+            m = mine.to_csv().split(",")[:-1]
+            w = want.split(",")
+            assert m[:6] == w[:6] and m[6] == w[6] and m[8] == w[8] and m[11] == w[11], (name, m, w)
+            newton = float(w[6]) if w[6] else 1.0
+            assert abs(float(m[7]) - float(w[7])) <= 1.0 + 1e-9, (name, m, w)
+            for i in (9, 10):
+                if w[i]:
+                    assert abs(float(m[i]) - float(w[i])) <= 1.0 / max(newton, 1.0) + 0.05 * float(w[i]), (name, m, w)
