@@ -127,9 +127,19 @@ def test_residual(case, p):
                              torch.as_tensor(g["ic_a"], device="cuda"))
         mine = p.residual(s, d).data.cpu().numpy()
         ref = g[key]
-        # floor: 1e-12 of the largest residual entry of the same slab
-        scale = np.repeat(np.abs(ref).reshape(d.n_steps, -1).max(axis=1), d.layout.slab_size)
-        assert entry_ok(mine, ref, 1e-1 * scale) <= TOL_ENTRY * 10, (name, key)
+        # per entry <= 1e-12 of the rounding scale of the entry's terms: |J||x| bounds the
+        # state-dependent element terms (linear and quadratic), |r(0)| the constant ones
+        # (loads, fluxes, BC values, initial condition), |r| the result itself
+        from oracle import model
+
+        od = _oracle_disc(name)
+        ojac = model.jacobian(model.State(np.asarray(vec).copy(), g["ic_u"], g["ic_a"]), od)
+        z = p.SpaceTimeState(p.BlockVector(d.layout, d.n_steps, np.zeros_like(vec)),
+                             torch.as_tensor(g["ic_u"], device="cuda"), torch.as_tensor(g["ic_a"], device="cuda"))
+        const = np.abs(p.residual(z, d).data.cpu().numpy())
+        scale = ojac.abs_apply(np.asarray(vec)) + const + np.abs(ref)
+        w = np.abs(mine - ref) / np.maximum(scale, 1e-300)
+        assert float(w.max()) <= TOL_ENTRY, (name, key, float(w.max()))
 
 
 def test_jacobian_blocks(case):
@@ -139,9 +149,9 @@ def test_jacobian_blocks(case):
             w = matrix_ok(getattr(b, blk), csr_from(g, f"s{k}_{blk}"))
             assert w <= TOL_ENTRY, (name, k, blk, w)
         assert matrix_ok(pc.f_p[k], csr_from(g, f"s{k}_f_p")) <= TOL_ENTRY
-        assert matrix_ok(pc.c_a[k], csr_from(g, f"s{k}_c_a")) <= 1e-11
+        assert matrix_ok(pc.c_a[k], csr_from(g, f"s{k}_c_a")) <= TOL_ENTRY
     for k, m in enumerate(pc.c_a_sub1):
-        assert matrix_ok(m, csr_from(g, f"sub1_{k}")) <= 1e-11
+        assert matrix_ok(m, csr_from(g, f"sub1_{k}")) <= TOL_ENTRY
     np.testing.assert_allclose(pc.alfven, g["alfven"], rtol=1e-12, atol=1e-15)
 
 
@@ -153,7 +163,7 @@ def test_jacobian_apply(case):
     ost = model.State(g["state"].copy(), g["ic_u"], g["ic_a"])
     scale = model.jacobian(ost, od).abs_apply(g["v"])
     mine = jac.apply(g["v"]).cpu().numpy()
-    assert entry_ok(mine, g["Jv"], scale) <= 4 * TOL_ENTRY
+    assert entry_ok(mine, g["Jv"], scale) <= TOL_ENTRY
 
 
 def test_preconditioner_apply(case):
