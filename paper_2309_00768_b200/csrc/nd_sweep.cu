@@ -1986,7 +1986,7 @@ __global__ void __launch_bounds__(256 * NC) topk_kernel(TopKArgs g) {
 // per lane and k-step feeds 8 MMAs; the front block V is [row][kVS] in shared memory,
 // row stride 72 doubles so the B-fragment loads of a k-step take two wavefronts).
 // Identical operations up to the summation order inside each dot product.
-constexpr int kVS = 72;
+constexpr int kVS = 68;  // row stride 544 B: the four rows of a half-warp B fragment hit distinct banks
 
 // acc[j] += blk rows r0..r0+7 (x K) . V[:, 8j .. 8j+7]; lane holds C(row lane/4,
 // cols 8j + 2(lane%4) + {0,1}).  blk is stored as row chunks [K][R].
@@ -1998,15 +1998,21 @@ __device__ __forceinline__ void topk_mma_tile(const double *__restrict__ blk, in
   const double *vb = V + kq * kVS + (lane >> 2);
   int k = 0;
   const int k16 = K & ~15;
-  double an[4];  // next k-block's A fragments, loaded one block ahead
+  // A fragments two k-blocks ahead (an: next block, an2: the one after): an L2 round
+  // trip is longer than one block's 32 MMAs
+  double an[4], an2[4];
 #pragma unroll
-  for (int s4 = 0; s4 < 4; ++s4) an[s4] = (rok && k16 > 0) ? __ldg(arow + (int64_t)(4 * s4 + kq) * R) : 0.0;
+  for (int s4 = 0; s4 < 4; ++s4) {
+    an[s4] = (rok && k16 > 0) ? __ldg(arow + (int64_t)(4 * s4 + kq) * R) : 0.0;
+    an2[s4] = (rok && 16 < k16) ? __ldg(arow + (int64_t)(16 + 4 * s4 + kq) * R) : 0.0;
+  }
   for (; k < k16; k += 16) {
     double a[4];
 #pragma unroll
     for (int s4 = 0; s4 < 4; ++s4) {
       a[s4] = an[s4];
-      an[s4] = (rok && k + 16 < k16) ? __ldg(arow + (int64_t)(k + 16 + 4 * s4 + kq) * R) : 0.0;
+      an[s4] = an2[s4];
+      an2[s4] = (rok && k + 32 < k16) ? __ldg(arow + (int64_t)(k + 32 + 4 * s4 + kq) * R) : 0.0;
     }
 #pragma unroll
     for (int s4 = 0; s4 < 4; ++s4) {
@@ -2048,29 +2054,34 @@ __global__ void __launch_bounds__(512) topk_mma_kernel(TopKArgs g) {
     for (int si = 0; si < g.ntsn; ++si) {  // forward, postorder
       const TopSN t = g.tsn[si];
       const int f = t.ns + t.nb;
-      // (row, 8-column group) per thread: one index load per row, 8 contiguous values
-      // per thread with all loads of a row in flight
-      for (int e = threadIdx.x; e < f * 8; e += blockDim.x) {
-        const int r = e >> 3, c0 = (e & 7) * 8;
+      // a warp per row, a column pair per lane: one index load per row (broadcast),
+      // coalesced 16-byte global accesses, conflict-free 512-byte shared-memory rows
+      for (int r = wl; r < f; r += nw) {
         const int ti = r < t.ns ? g.tidx[t.first + r] : -1;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) V[r * kVS + c0 + q] = (ti == col0 + c0 + q) ? 1.0 : 0.0;
+        const int c = 2 * lane;
+        *reinterpret_cast<double2 *>(V + r * kVS + c) =
+            make_double2(ti == col0 + c ? 1.0 : 0.0, ti == col0 + c + 1 ? 1.0 : 0.0);
       }
       __syncthreads();
       for (int c = 0; c < t.nchild; ++c) {  // extend-add the top children's updates
         const int4 ch = g.tchild[t.child0 + c];
         const int cb0 = g.tsn[ch.x].tcb_off;
-        for (int e = threadIdx.x; e < ch.z * 8; e += blockDim.x) {
-          const int a = e >> 3, c0 = (e & 7) * 8;
-          const double2 *src = reinterpret_cast<const double2 *>(CBw + (int64_t)(cb0 + a) * CS + c0);
-          double2 vv[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) vv[q] = src[q];
-          double *dst = V + g.emap[ch.y + a] * kVS + c0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            dst[2 * q] += vv[q].x;
-            dst[2 * q + 1] += vv[q].y;
+        for (int a0 = wl; a0 < ch.z; a0 += 2 * nw) {  // two rows per warp in flight
+          const int a1 = a0 + nw;
+          const double2 v0 = reinterpret_cast<const double2 *>(CBw + (int64_t)(cb0 + a0) * CS)[lane];
+          const double2 v1 = a1 < ch.z ? reinterpret_cast<const double2 *>(CBw + (int64_t)(cb0 + a1) * CS)[lane]
+                                       : make_double2(0.0, 0.0);
+          double2 *d0 = reinterpret_cast<double2 *>(V + g.emap[ch.y + a0] * kVS) + lane;
+          double2 w0 = *d0;
+          w0.x += v0.x;
+          w0.y += v0.y;
+          *d0 = w0;
+          if (a1 < ch.z) {
+            double2 *d1 = reinterpret_cast<double2 *>(V + g.emap[ch.y + a1] * kVS) + lane;
+            double2 w1 = *d1;
+            w1.x += v1.x;
+            w1.y += v1.y;
+            *d1 = w1;
           }
         }
         __syncthreads();
@@ -2097,16 +2108,10 @@ __global__ void __launch_bounds__(512) topk_mma_kernel(TopKArgs g) {
     for (int si = g.ntsn - 1; si >= 0; --si) {  // backward, reverse postorder
       const TopSN t = g.tsn[si];
       const int f = t.ns + t.nb;
-      for (int e = threadIdx.x; e < f * 8; e += blockDim.x) {
-        const int r = e >> 3, c0 = (e & 7) * 8;
+      for (int r = wl; r < f; r += nw) {  // own y, or the ancestors' x
         const int pos = r < t.ns ? t.first + r : g.bpos[t.goff + r];
-        const double2 *src = reinterpret_cast<const double2 *>(Xw + (int64_t)g.tidx[pos] * CS + c0);
-        double2 vv[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) vv[q] = src[q];  // own y, or the ancestors' x
-        double2 *dst = reinterpret_cast<double2 *>(V + r * kVS + c0);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = vv[q];
+        reinterpret_cast<double2 *>(V + r * kVS)[lane] =
+            reinterpret_cast<const double2 *>(Xw + (int64_t)g.tidx[pos] * CS)[lane];
       }
       __syncthreads();
       for (int k0 = wl * 8; k0 < t.ns; k0 += nw * 8) {
@@ -2123,18 +2128,12 @@ __global__ void __launch_bounds__(512) topk_mma_kernel(TopKArgs g) {
       }
       __syncthreads();
     }
-    for (int e = threadIdx.x; e < g.nT * 8; e += blockDim.x) {  // row groups of kr: [group][col][kr]
-      const int i = e >> 3, c0 = (e & 7) * 8;
-      const double2 *src = reinterpret_cast<const double2 *>(Xw + (int64_t)i * CS + c0);
-      double2 vv[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) vv[q] = src[q];
+    for (int i = wl; i < g.nT; i += nw) {  // row groups of kr: [group][col][kr]
+      const double2 v = reinterpret_cast<const double2 *>(Xw + (int64_t)i * CS)[lane];
       double *kb = g.K + (int64_t)b * g.kstride + (int64_t)(i - i % g.kr) * g.kpad + i % g.kr;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (col0 + c0 + 2 * q < g.nT) kb[(int64_t)(col0 + c0 + 2 * q) * g.kr] = vv[q].x;
-        if (col0 + c0 + 2 * q + 1 < g.nT) kb[(int64_t)(col0 + c0 + 2 * q + 1) * g.kr] = vv[q].y;
-      }
+      const int c = col0 + 2 * lane;
+      if (c < g.nT) kb[(int64_t)c * g.kr] = v.x;
+      if (c + 1 < g.nT) kb[(int64_t)(c + 1) * g.kr] = v.y;
     }
     __syncthreads();
   }
