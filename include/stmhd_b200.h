@@ -112,7 +112,9 @@ int stmhd_pc_apply(stmhd_pc p, void *stream, int direction, const double *r, dou
    8 magnetic_schur_inverse 9 magnetic_schur_apply 10 apply_pressure_cd 11 solve_pressure_cd */
 int stmhd_pc_op(stmhd_pc p, void *stream, int op, const double *in, double *out);
 /* export per-slab matrix values for inspection: what 0 = C_A values (nt x nnz_ca),
-   1 = sub1 values ((nt-1) x nnz_s1), 2 = sub2 values (nnz_s2) */
+   1 = sub1 values ((nt-1) x nnz_s1), 2 = sub2 values (nnz_s2), 3 = the smallest
+   restricted-pivoting ratios {F_u, C_A} (2 doubles; |pivot| / max |column entry below the
+   diagonal incl. contribution-block rows|, 1 = as good as unrestricted partial pivoting) */
 int stmhd_pc_export(stmhd_pc p, void *stream, int what, double *out);
 
 /* ---- K8: fused Gram-Schmidt / FGMRES vector kernels (linalg.py:163-199) ----

@@ -279,7 +279,11 @@ int stmhd_pc_export(stmhd_pc p, void *stream, int what, double *out) {
   require(p && out, "stmhd_pc_export: bad arguments");
   PC &c = *p->pc;
   const DevBuf *b = what == 0 ? &c.ca_vals : what == 1 ? &c.s1_vals : nullptr;
-  if (what == 2) {
+  if (what == 3) {  // smallest restricted-pivoting ratios of the F_u and C~_A factorisations
+    const double h[2] = {c.fu->min_pivot_ratio, c.ca->min_pivot_ratio};
+    STMHD_CUDA_CHECK(cudaMemcpyAsync(out, h, sizeof(h), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    STMHD_CUDA_CHECK(cudaStreamSynchronize((cudaStream_t)stream));
+  } else if (what == 2) {
     DCsr s2 = c.d->csr("sub2");
     int64_t n = c.d->H("sub2_val").count;
     STMHD_CUDA_CHECK(cudaMemcpyAsync(out, s2.val, n * sizeof(double), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));

@@ -198,7 +198,8 @@ struct NDFactor {
   const NDDevice *dev = nullptr;
   int nbatch = 0;
   DevBuf factors;  // nbatch * factor_size doubles
-  DevBuf status;   // int: 0 ok, 1+ singular (first failing supernode+1)
+  DevBuf status;   // int[2]: 0 ok / 1+ singular (first failing supernode+1); smallest pivot ratio (float bits)
+  mutable float min_pivot_ratio = 1.0f;  // of the last factorisation (check_status)
   uint64_t gen = 0;  // bumped by every factorisation
   // dense inverse of the top Schur complement per batch entry (nd_sweep.cu), built
   // lazily for the sweep plan that uses it: [nbatch][kstride()] doubles (row groups of kr)

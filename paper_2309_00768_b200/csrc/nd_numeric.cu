@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <cstdio>
 
 #include "nd.hpp"
 
@@ -117,9 +119,10 @@ struct FactorArgs {
 
 __global__ void __launch_bounds__(256, 4) nd_factor_level(FactorArgs a) {
   extern __shared__ double smem[];
-  __shared__ double red_v[8];
+  __shared__ double red_v[8], red_c[8];
   __shared__ int red_i[8];
   __shared__ int piv_sh;
+  float prat = 1.0f;  // thread 0: smallest pivot ratio of this front
   const int s = a.lvl_sn[blockIdx.x];
   const int bl = blockIdx.y;  // batch slot within chunk
   const int b = a.batch0 + bl;
@@ -156,25 +159,33 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level(FactorArgs a) {
     for (int jj = 0; jj < pw; ++jj) {
       int col = p0 + jj;
       // pivot search over rows col..ns-1
-      double best = -1.0;
+      double best = -1.0, cbm = 0.0;
       int bi = col;
       for (int r = col + tid; r < ns; r += nt) {
         double v = fabs(F[(int64_t)r * f + col]);
         if (v > best) { best = v; bi = r; }
       }
+      for (int r = ns + tid; r < f; r += nt) cbm = fmax(cbm, fabs(F[(int64_t)r * f + col]));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         double ov = __shfl_xor_sync(0xffffffffu, best, o);
         int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+        cbm = fmax(cbm, __shfl_xor_sync(0xffffffffu, cbm, o));
       }
-      if ((tid & 31) == 0) { red_v[tid >> 5] = best; red_i[tid >> 5] = bi; }
+      if ((tid & 31) == 0) { red_v[tid >> 5] = best; red_i[tid >> 5] = bi; red_c[tid >> 5] = cbm; }
       __syncthreads();
       if (tid == 0) {
-        double bv = red_v[0];
+        double bv = red_v[0], cm = red_c[0];
         int bidx = red_i[0];
-        for (int w = 1; w < nt / 32; ++w)
+        for (int w = 1; w < nt / 32; ++w) {
           if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bidx)) { bv = red_v[w]; bidx = red_i[w]; }
+          cm = fmax(cm, red_c[w]);
+        }
+        // pivot ratio: the chosen pivot against the largest entry of its column below
+        // the diagonal including the contribution-block rows the restricted pivoting
+        // does not search (1 = as good as unrestricted partial pivoting)
+        if (bv > 0.0 && isfinite(bv)) prat = fmin(prat, bv / fmax(bv, cm));
         piv_sh = (bv > 0.0 && isfinite(bv)) ? bidx : -1;
         if (piv_sh >= 0 && piv_sh != col) {
           int t = perm[col]; perm[col] = perm[piv_sh]; perm[piv_sh] = t;
@@ -218,6 +229,7 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level(FactorArgs a) {
     if (tid == 0) atomicCAS(a.status, 0, s + 1);
     return;
   }
+  if (tid == 0) atomicMin(a.status + 1, __float_as_int(prat));  // positive floats order as ints
   // 4. inverse-based factors, column-major in the staging buffer (relaid out
   //    into row-chunk blocks by nd_relayout afterwards):
   //    FLT[t*f + r] = FL[r][t] (FL = [L11^-1 P ; L21 L11^-1 P], f x ns)
@@ -268,9 +280,10 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level(FactorArgs a) {
 // [2*GT*GK] | perm (ints).
 __global__ void __launch_bounds__(256, 4) nd_factor_level_smem(FactorArgs a) {
   extern __shared__ double smem[];
-  __shared__ double red_v[8];
+  __shared__ double red_v[8], red_c[8];
   __shared__ int red_i[8];
   __shared__ int piv_sh;
+  float prat = 1.0f;  // thread 0: smallest pivot ratio of this front
   const int s = a.lvl_sn[blockIdx.x];
   const int bl = blockIdx.y;
   const int b = a.batch0 + bl;
@@ -306,25 +319,30 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level_smem(FactorArgs a) {
     const int pw = min(PB, ns - p0);
     for (int jj = 0; jj < pw; ++jj) {
       const int col = p0 + jj;
-      double best = -1.0;
+      double best = -1.0, cbm = 0.0;
       int bi = col;
       for (int r = col + tid; r < ns; r += nt) {
         const double v = fabs(F[r * f + col]);
         if (v > best) { best = v; bi = r; }
       }
+      for (int r = ns + tid; r < f; r += nt) cbm = fmax(cbm, fabs(F[r * f + col]));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, best, o);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+        cbm = fmax(cbm, __shfl_xor_sync(0xffffffffu, cbm, o));
       }
-      if ((tid & 31) == 0) { red_v[tid >> 5] = best; red_i[tid >> 5] = bi; }
+      if ((tid & 31) == 0) { red_v[tid >> 5] = best; red_i[tid >> 5] = bi; red_c[tid >> 5] = cbm; }
       __syncthreads();
       if (tid == 0) {
-        double bv = red_v[0];
+        double bv = red_v[0], cm = red_c[0];
         int bidx = red_i[0];
-        for (int w = 1; w < nt / 32; ++w)
+        for (int w = 1; w < nt / 32; ++w) {
           if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bidx)) { bv = red_v[w]; bidx = red_i[w]; }
+          cm = fmax(cm, red_c[w]);
+        }
+        if (bv > 0.0 && isfinite(bv)) prat = fmin(prat, bv / fmax(bv, cm));
         piv_sh = (bv > 0.0 && isfinite(bv)) ? bidx : -1;
         if (piv_sh >= 0 && piv_sh != col) {
           const int t = perm[col]; perm[col] = perm[piv_sh]; perm[piv_sh] = t;
@@ -366,6 +384,7 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level_smem(FactorArgs a) {
     if (tid == 0) atomicCAS(a.status, 0, s + 1);
     return;
   }
+  if (tid == 0) atomicMin(a.status + 1, __float_as_int(prat));
   // contribution block back to the global workspace (the parent's extend-add)
   for (int t = tid; t < nb * nb; t += nt) {
     const int i = t / nb, j = t - i * nb;
@@ -475,23 +494,27 @@ __global__ void __launch_bounds__(256) nd_factor_level_warp(FactorArgs a, int cn
   if (lane < ns) perm[lane] = lane;
   __syncwarp();
   // 2. LU with pivoting restricted to the ns x ns block, unblocked right-looking
+  float prat = 1.0f;
   for (int col = 0; col < ns; ++col) {
-    double best = -1.0;
+    double best = -1.0, cbm = 0.0;
     int bi = col;
     for (int r = col + lane; r < ns; r += 32) {
       const double v = fabs(F[r * fs + col]);
       if (v > best) { best = v; bi = r; }
     }
+    for (int r = ns + lane; r < f; r += 32) cbm = fmax(cbm, fabs(F[r * fs + col]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, best, o);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      cbm = fmax(cbm, __shfl_xor_sync(0xffffffffu, cbm, o));
     }
     if (!(best > 0.0 && isfinite(best))) {
       if (lane == 0) atomicCAS(a.status, 0, s + 1);
       return;
     }
+    prat = fminf(prat, (float)(best / fmax(best, cbm)));
     if (bi != col) {
       for (int c = lane; c < f; c += 32) {
         const double t = F[col * fs + c];
@@ -524,6 +547,7 @@ __global__ void __launch_bounds__(256) nd_factor_level_warp(FactorArgs a, int cn
     }
     __syncwarp();
   }
+  if (lane == 0) atomicMin(a.status + 1, __float_as_int(prat));
   // 3. contribution block -> global (the parent's extend-add)
   for (int t = lane; t < nb * nb; t += 32) {
     const int i = t / nb, j = t - i * nb;
@@ -716,8 +740,11 @@ void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s
   ++gen;  // invalidates derived data (dense top inverse)
   if (factors.bytes != (size_t)nbatch * p.factor_size * sizeof(double))
     factors.alloc_async((size_t)nbatch * p.factor_size * sizeof(double), s);
-  if (!status.ptr) status.alloc_async(sizeof(int), s);
-  STMHD_CUDA_CHECK(cudaMemsetAsync(status.ptr, 0, sizeof(int), s));
+  if (!status.ptr) status.alloc_async(2 * sizeof(int), s);
+  {
+    const int init[2] = {0, 0x7f800000};  // ok, smallest pivot ratio = +inf (float bits)
+    STMHD_CUDA_CHECK(cudaMemcpyAsync(status.ptr, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  }
   // chunk the batch so front workspace + staging stay within a budget: the top tree
   // levels have one front per matrix, so a level launch has (fronts x chunk) CTAs --
   // a small chunk leaves most SMs idle on the largest fronts.  Budget: STMHD_FACTOR_WS_GB
@@ -857,10 +884,20 @@ void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s
 }
 
 int NDFactor::check_status(cudaStream_t s) const {
-  int h = 0;
-  STMHD_CUDA_CHECK(cudaMemcpyAsync(&h, status.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+  int h[2] = {0, 0x7f800000};
+  STMHD_CUDA_CHECK(cudaMemcpyAsync(h, status.ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
   STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
-  return h;
+  float r;
+  memcpy(&r, &h[1], sizeof(r));
+  min_pivot_ratio = r;
+  static const double warn_below = [] {
+    const char *e = getenv("STMHD_PIVOT_WARN");
+    return e ? atof(e) : 1e-8;
+  }();
+  if (!h[0] && r < warn_below)
+    fprintf(stderr, "[stmhd] warning: restricted-pivoting ratio %.3g (n=%lld, %d matrices): a contribution-block "
+                    "entry dominates the chosen pivot\n", (double)r, (long long)dev->plan->n, nbatch);
+  return h[0];
 }
 
 // ---------------------------------------------------------------------------

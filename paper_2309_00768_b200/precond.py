@@ -123,6 +123,16 @@ class SpaceTimePreconditioner:
         return [sp.csr_matrix((vals[k], col, rp), shape=(n, n)) for k in range(self.n_steps - 1)]
 
     @property
+    def pivot_ratio(self) -> dict:
+        """Smallest restricted-pivoting ratio of the F_u and C~_A factorisations:
+        |pivot| / max |entry of its column below the diagonal|, contribution-block rows
+        included (the pivot search is restricted to the supernode's diagonal block; 1
+        means as good as unrestricted partial pivoting).  A ratio below 1e-8 is also
+        reported on stderr by the native library (STMHD_PIVOT_WARN)."""
+        v = self._export(3, (2,))
+        return {"F_u": float(v[0]), "C_A": float(v[1])}
+
+    @property
     def c_a_sub2(self):
         return self.disc.c_a_sub2
 
