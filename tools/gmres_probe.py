@@ -20,7 +20,7 @@ m = 50
 V = torch.randn(m + 1, n, dtype=torch.float64, device="cuda")
 Z = torch.empty(m, n, dtype=torch.float64, device="cuda")
 dev = torch.zeros(2 * m + 8, dtype=torch.float64, device="cuda")
-work = torch.empty(1 << 22, dtype=torch.float64, device="cuda")
+work = torch.empty(int(lib.stmhd_gs_work_size(n, m + 1)) + 8, dtype=torch.float64, device="cuda")
 pc._into(V[0], Z[0])
 jac._into(Z[0], V[1])
 torch.cuda.synchronize()
