@@ -53,6 +53,33 @@ int stmhd_disc_create(stmhd_disc *out) {
   CAPI_END
 }
 
+stmhd_disc_s::~stmhd_disc_s() {
+  // release every member first (pooled frees may be queued on the side stream), then
+  // the stream and events; errors are ignored in a destructor
+  if (side) cudaStreamSynchronize(side);
+  jv_plan.reset();
+  lu_mj.reset();
+  lu_ma.reset();
+  lu_mp.reset();
+  lu_kp.reset();
+  dev_fu.reset();
+  dev_ca.reset();
+  dev_fa.reset();
+  dev_fp.reset();
+  dev_mj.reset();
+  dev_ma.reset();
+  dev_mp.reset();
+  dev_kp.reset();
+  clamped = stmhd::DevBuf();
+  dev.clear();
+  if (side) {
+    cudaStreamSynchronize(side);
+    cudaStreamDestroy(side);
+  }
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+}
+
 int stmhd_disc_destroy(stmhd_disc d) {
   CAPI_BEGIN
   delete d;

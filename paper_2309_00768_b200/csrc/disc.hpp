@@ -76,6 +76,11 @@ struct stmhd_disc_s {
   std::unique_ptr<stmhd::NDFactor> lu_mj, lu_ma, lu_mp, lu_kp;
   stmhd::DevBuf clamped;  // nt*slab clamped state workspace
   std::unique_ptr<stmhd::StSpmvPlan> jv_plan;  // J.v row blocks (built at the first apply)
+  // side stream + fork/join events of the P_T^-1 pre-steps (pressure chain), owned by
+  // the discretisation: buffers pooled on it are released before it is destroyed
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  ~stmhd_disc_s();
 
   int64_t I(const char *k) const;
   double R(const char *k) const;

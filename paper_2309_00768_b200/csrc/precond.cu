@@ -388,15 +388,15 @@ void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
   const double *r_u = r, *r_p = r + o_p, *r_j = r + o_j, *r_a = r + o_a;
   // batched (slab-parallel) pre-steps; the pressure chain runs on a second stream,
   // overlapped with the wave right-hand side, and joins before the velocity stage
-  // process-wide side stream and events (never destroyed: pooled buffers allocated on
-  // the side stream may be freed on it after this preconditioner is gone)
-  static cudaStream_t side = nullptr;
-  static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  if (!side) {
-    STMHD_CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    STMHD_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    STMHD_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  // side stream and events owned by the discretisation (it outlives its
+  // preconditioners; buffers pooled on the stream are released before it is destroyed)
+  if (!d->side) {
+    STMHD_CUDA_CHECK(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking));
+    STMHD_CUDA_CHECK(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
+    STMHD_CUDA_CHECK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
   }
+  cudaStream_t side = d->side;
+  cudaEvent_t ev_fork = d->ev_fork, ev_join = d->ev_join;
   STMHD_CUDA_CHECK(cudaEventRecord(ev_fork, s));
   STMHD_CUDA_CHECK(cudaStreamWaitEvent(side, ev_fork, 0));
   pressure_schur_inverse(r_p, slab, x + o_p, slab, side);
