@@ -514,7 +514,9 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   if (sp->dense) {
     const int ng = (sp->ntT + sp->kr - 1) / sp->kr;
     static const int dsplit_env = env_int2("STMHD_SWEEP_DENSE_SPLIT", 1);
+    static const int dpc_env = env_int2("STMHD_SWEEP_DENSE_PC", 0);  // force chunks per piece
     int npc = dsplit_env ? std::max(1, std::min(sp->nch, (W + ng - 1) / ng)) : 1;
+    if (dpc_env > 0) npc = (sp->nch + dpc_env - 1) / dpc_env;
     const int pc = (sp->nch + npc - 1) / npc;  // chunks per piece
     npc = (sp->nch + pc - 1) / pc;
     sp->dpieces = npc;
