@@ -753,10 +753,14 @@ void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s
     const char *e = getenv("STMHD_FACTOR_WS_GB");
     return e ? atoi(e) : 16;
   }();
+  static const int frac_env = [] {  // percent of the free device memory the workspace may take
+    const char *e = getenv("STMHD_FACTOR_WS_FRAC");
+    return e ? atoi(e) : 25;
+  }();
   int64_t budget = (int64_t)std::max(ws_env, 1) << 30;
   {
     size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) budget = std::min<int64_t>(budget, (int64_t)(free_b / 4));
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) budget = std::min<int64_t>(budget, (int64_t)(free_b * frac_env / 100));
     budget = std::max<int64_t>(budget, int64_t(3) << 30);
   }
   int64_t per = (std::max<int64_t>(p.front_size, 1) + p.stage_size) * (int64_t)sizeof(double);
