@@ -37,7 +37,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = ["nvcc", *ARCH, *[f for f in FLAGS if f != "-shared"], "-c", src, "-o", obj]
+        extra = os.environ.get("STMHD_NVCC_EXTRA", "").split()  # experiments, e.g. -DSTMHD_RING=3
+        cmd = ["nvcc", *ARCH, *[f for f in FLAGS if f != "-shared"], *extra, "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
     for src, p in procs:

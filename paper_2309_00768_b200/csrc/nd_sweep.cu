@@ -31,6 +31,12 @@
 
 namespace stmhd {
 
+// TMA ring slots per warp (compile-time: -DSTMHD_RING=n)
+#ifndef STMHD_RING
+#define STMHD_RING 2
+#endif
+constexpr int kRing = STMHD_RING;
+
 static int env_int2(const char *name, int dflt) {
   const char *e = getenv(name);
   return e ? atoi(e) : dflt;
@@ -59,7 +65,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
                                             int mode) const {
   const bool flat = mode >= 3;
   const int slot_sz = sweep_slot(*plan);
-  const int64_t vstride_max = (std::max(max_front, 1) + 15) / 16 * 16 + 2 * slot_sz;
+  const int64_t vstride_max = (std::max(max_front, 1) + 15) / 16 * 16 + kRing * slot_sz;
   const int64_t sub_budget = smem_budget - (int64_t)warps * vstride_max;  // conservative (largest front)
   for (const auto &c : sweep_plans)
     if (c->ncta == ncta && c->warps == warps) return *c;
@@ -596,7 +602,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     int fmax = 1;
     for (int sn = 0; sn < p.nsn; ++sn)
       if (!isK[sn]) fmax = std::max(fmax, p.ns[sn] + p.nb[sn]);
-    sp->vstride = (int)((fmax + 15) / 16 * 16 + 2 * slot_sz);
+    sp->vstride = (int)((fmax + 15) / 16 * 16 + kRing * slot_sz);
     const int64_t need = (int64_t)warps * sp->vstride + 3 * maxlen + maxcb + tdoubles + sp->zlen() + sp->tab_ints / 2 + 4;
     if (!flat && D > 0 && need > smem_budget) {
       const int next = sp->tab_ints ? 1 : (sp->dense ? 2 : 3);
@@ -853,7 +859,7 @@ struct WarpCtx {
   const SweepTask *tl;
   const int *bnd;  // start of every phase level in tl (nl + 1 entries)
   int nt;
-  int jc;                       // chunks consumed (slot jc & 1, mbarrier parity (jc >> 1) & 1)
+  int jc;                       // chunks consumed (slot jc % kRing, mbarrier parity (jc / kRing) & 1)
   int icount, rt, rc, rslab;    // TMA ring cursor (lane 0): two chunks ahead of jc
   // PROF instantiation: cycles in gather / TMA wait / GEMV+store / barriers, tasks, chunks
   long long acc[10];  // PROF: 8 issue cycles (ring_issue after a chunk)
@@ -911,9 +917,9 @@ __device__ __forceinline__ void item_next(const WarpCtx &w, int &t, int &c, int 
 // runs across task, level and slab boundaries (factors do not depend on the data),
 // so a warp's next items are in flight while it waits at a barrier.  (An L2 bulk
 // prefetch cursor further ahead along the same sequence was measured slower.)
-__device__ __forceinline__ void ring_issue(const SweepArgs &a, WarpCtx &w, unsigned long long (*mbar)[2]) {
+__device__ __forceinline__ void ring_issue(const SweepArgs &a, WarpCtx &w, unsigned long long (*mbar)[kRing]) {
   if (w.rslab < a.nslab && w.nt > 0) {
-    const int sl = w.icount & 1;
+    const int sl = w.icount % kRing;
     int dbl;
     const double *src = item_src(a, w.tl[w.rt], w.rc, w.rslab, dbl);
     tma_load(w.slot0 + sl * w.slotsz, src, dbl, &mbar[w.wl][sl]);
@@ -926,9 +932,9 @@ __device__ __forceinline__ void ring_issue(const SweepArgs &a, WarpCtx &w, unsig
 // slot's mbarrier (expected count 32) completes once every lane's copies landed.  A
 // cp.async.bulk issue blocks the issuing warp ~350-430 cycles (tools/tma_ring_probe.cu),
 // on the critical path after every chunk; the per-lane copies issue in ~10 cycles each.
-__device__ __forceinline__ void ring_issue_warp(const SweepArgs &a, WarpCtx &w, unsigned long long (*mbar)[2]) {
+__device__ __forceinline__ void ring_issue_warp(const SweepArgs &a, WarpCtx &w, unsigned long long (*mbar)[kRing]) {
   if (w.rslab < a.nslab && w.nt > 0) {
-    const int sl = w.icount & 1;
+    const int sl = w.icount % kRing;
     int dbl;
     const double *src = item_src(a, w.tl[w.rt], w.rc, w.rslab, dbl);
     double *dst = w.slot0 + sl * w.slotsz;
@@ -942,7 +948,7 @@ __device__ __forceinline__ void ring_issue_warp(const SweepArgs &a, WarpCtx &w, 
 
 // Refill the ring after a consumed item (call from every lane, after the __syncwarp
 // that ends the item's reads).
-__device__ __forceinline__ void ring_next(const SweepArgs &a, WarpCtx &w, unsigned long long (*mbar)[2]) {
+__device__ __forceinline__ void ring_next(const SweepArgs &a, WarpCtx &w, unsigned long long (*mbar)[kRing]) {
   if (a.ldgsts) ring_issue_warp(a, w, mbar);
   else if (w.lane == 0) ring_issue(a, w, mbar);
 }
@@ -973,13 +979,13 @@ __device__ __forceinline__ double chunk_gemv_smem(const double *blk, int KR, int
 template <bool SUB, bool PROF>
 __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask &tk, const double *F,
                                              const double *rhs, const SubView &sv, WarpCtx &w,
-                                             unsigned long long (*mbar)[2]) {
+                                             unsigned long long (*mbar)[kRing]) {
   const int lane = w.lane;
   long long t0 = pclock<PROF>();
   const int4 *g = a.g3p + tk.goff;
   if (tk.flags & 4) {  // front table arrived through the ring
-    mbar_wait(&mbar[w.wl][w.jc & 1], (unsigned)(w.jc >> 1) & 1u);
-    g = reinterpret_cast<const int4 *>(w.slot0 + (w.jc & 1) * w.slotsz);
+    mbar_wait(&mbar[w.wl][w.jc % kRing], (unsigned)(w.jc / kRing) & 1u);
+    g = reinterpret_cast<const int4 *>(w.slot0 + (w.jc % kRing) * w.slotsz);
   }
   const double *cbsrc = SUB ? sv.cbs - sv.cbfirst : a.cbv;
   // fused coupling: subtree rows come from shared memory, top rows from tbuf
@@ -1030,8 +1036,8 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
   double *ydst = SUB ? sv.ys - sv.first : a.ybuf;
   double *cbdst = (!SUB || (tk.flags & 1)) ? a.cbv : sv.cbs - sv.cbfirst;
   for (int c = tk.c0; c < tk.c1; ++c) {
-    const int sl = w.jc & 1;
-    mbar_wait(&mbar[w.wl][sl], (unsigned)(w.jc >> 1) & 1u);
+    const int sl = w.jc % kRing;
+    mbar_wait(&mbar[w.wl][sl], (unsigned)(w.jc / kRing) & 1u);
     const double *blk = w.slot0 + sl * w.slotsz;
     if (PROF) {
       const long long t1 = pclock<PROF>();
@@ -1067,7 +1073,7 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
 // Backward (U) step of one task.
 template <bool SUB, bool PROF>
 __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTask &tk, const double *F, double *x,
-                                              const SubView &sv, WarpCtx &w, unsigned long long (*mbar)[2]) {
+                                              const SubView &sv, WarpCtx &w, unsigned long long (*mbar)[kRing]) {
   const int lane = w.lane;
   long long t0 = pclock<PROF>();
   if (SUB && (tk.flags & 32)) {
@@ -1100,8 +1106,8 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
   }
   const int *bp = a.bpos + tk.goff;
   if (tk.flags & 4) {  // front table arrived through the ring
-    mbar_wait(&mbar[w.wl][w.jc & 1], (unsigned)(w.jc >> 1) & 1u);
-    bp = reinterpret_cast<const int *>(w.slot0 + (w.jc & 1) * w.slotsz);
+    mbar_wait(&mbar[w.wl][w.jc % kRing], (unsigned)(w.jc / kRing) & 1u);
+    bp = reinterpret_cast<const int *>(w.slot0 + (w.jc % kRing) * w.slotsz);
   }
   const double *y = (SUB ? sv.ys - sv.first : a.ybuf) + tk.first;
   if (!(SUB && (tk.flags & 32)))
@@ -1141,8 +1147,8 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
   }
   const int R = tk.R, lgR = __ffs(R) - 1, kl = 32 >> lgR, kq = lane >> lgR;
   for (int c = tk.c0; c < tk.c1; ++c) {
-    const int sl = w.jc & 1;
-    mbar_wait(&mbar[w.wl][sl], (unsigned)(w.jc >> 1) & 1u);
+    const int sl = w.jc % kRing;
+    mbar_wait(&mbar[w.wl][sl], (unsigned)(w.jc / kRing) & 1u);
     const double *blk = w.slot0 + sl * w.slotsz;
     if (PROF) {
       const long long t1 = pclock<PROF>();
@@ -1180,13 +1186,13 @@ __device__ __forceinline__ void backward_task(const SweepArgs &a, const SweepTas
 // (lane = kq * R + r covers columns kq + (32 / R) q of row r).
 template <bool PROF>
 __device__ __forceinline__ void dense_task(const SweepArgs &a, const SweepTask &tk, const double *zs, double *dred,
-                                           WarpCtx &w, unsigned long long (*mbar)[2]) {
+                                           WarpCtx &w, unsigned long long (*mbar)[kRing]) {
   const int lane = w.lane;
   const int R = tk.R, kl = 32 / R;
   double acc = 0.0;
   for (int c = tk.c0; c < tk.c1; ++c) {
-    const int sl = w.jc & 1;
-    mbar_wait(&mbar[w.wl][sl], (unsigned)(w.jc >> 1) & 1u);
+    const int sl = w.jc % kRing;
+    mbar_wait(&mbar[w.wl][sl], (unsigned)(w.jc / kRing) & 1u);
     acc += chunk_gemv_smem(w.slot0 + sl * w.slotsz, R * tk.ns, kl, lane / R, R, zs + (int64_t)c * tk.ns, lane);
     __syncwarp();
     ++w.jc;
@@ -1360,7 +1366,7 @@ __device__ void l2_prefetch_cluster(const SweepMulti &m, int crank) {
 template <bool PROF>
 __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant__ SweepMulti m) {
   extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) unsigned long long mbar[16][2];
+  __shared__ __align__(8) unsigned long long mbar[16][kRing];
   __shared__ SweepArgs sa;
   __shared__ const double *s_src[8];  // coupling sources of the current slab (by source id)
   // grid-family launch (no clusters, software barriers): stages own CTA ranges;
@@ -1398,7 +1404,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   const int lane = w.lane, wl = w.wl;
   // (top-phase task lists are interleaved across CTAs: global warp wl * ncta + crank)
   w.v = sm + wl * a.vstride;
-  w.slot0 = w.v + (a.vstride - 2 * a.slot);
+  w.slot0 = w.v + (a.vstride - kRing * a.slot);
   w.slotsz = a.slot;
   w.jc = w.icount = w.rt = w.rc = w.rslab = 0;
   for (int i = 0; i < 10; ++i) w.acc[i] = 0;
@@ -1448,15 +1454,13 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
   }
   if (lane == 0) {
     const unsigned cnt = a.ldgsts ? 32u : 1u;  // warp-wide cp.async: one arrival per lane
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&mbar[wl][0])), "r"(cnt) : "memory");
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&mbar[wl][1])), "r"(cnt) : "memory");
+    for (int r = 0; r < kRing; ++r)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&mbar[wl][r])), "r"(cnt) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncwarp();
-  if (!a.null_work && w.nt > 0) {  // fill the ring
-    ring_next(a, w, mbar);
-    ring_next(a, w, mbar);
-  }
+  if (!a.null_work && w.nt > 0)  // fill the ring
+    for (int r = 0; r < kRing; ++r) ring_next(a, w, mbar);
   __syncwarp();
   const int64_t n = a.n;
   int step = 0;
