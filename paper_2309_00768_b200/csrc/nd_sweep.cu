@@ -750,6 +750,7 @@ struct SweepArgs {
   unsigned long long *trace;
   unsigned long long *prof;  // PROF instantiation: 6 counters per warp
   unsigned long long *tline; // PROF instantiation: per-warp event timeline of slab 1, CTA 0 (128 per warp)
+  unsigned long long *pcta;  // PROF instantiation: per CTA, slab 1: subtree forward / backward durations (ns)
 };
 
 __device__ __forceinline__ void sweep_barrier(const SweepArgs &a, int crank, unsigned &gphase) {
@@ -1544,6 +1545,8 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
     // phase levels of this warp's list: subtree forward (CTA-local), top forward,
     // top backward (cluster-wide), subtree backward (CTA-local)
     int L = 0;
+    unsigned long long tph0 = 0;
+    if (PROF && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tph0));
     for (int h = 0; h < a.nsub; ++h, ++L) {
       const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
       if (PROF) {
@@ -1553,6 +1556,11 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       for (int ti = w.bnd[L]; ti < t1; ++ti) forward_task<true, PROF>(a, w.tl[ti], F, rhs, sv, w, mbar);
       if (PROF) tl_mark(w, 4);
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+    }
+    if (PROF && threadIdx.x == 0 && a.pcta && k == 1) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.pcta[2 * crank] = t - tph0;
     }
     if (a.nsub || a.prog_hdr) {  // subtree roots' updates and coupled top rows visible
       tb = pclock<PROF>(); sweep_barrier(a, crank, gphase); if (PROF) w.acc[3] += pclock<PROF>() - tb;
@@ -1628,12 +1636,18 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       }
       sweep_trace(a, step, crank);
     }
+    if (PROF && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tph0));
     for (int h = a.nsub - 1; h >= 0; --h, ++L) {
       const int t1 = a.null_work ? w.bnd[L] : w.bnd[L + 1];
       if (PROF) tl_mark(w, 5);
       for (int ti = w.bnd[L]; ti < t1; ++ti) backward_task<true, PROF>(a, w.tl[ti], F, x, sv, w, mbar);
       if (PROF) tl_mark(w, 6);
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
+    }
+    if (PROF && threadIdx.x == 0 && a.pcta && k == 1) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.pcta[2 * crank + 1] = t - tph0;
     }
     if (a.post_hdr && !a.null_work) {
       // post-slab program: rows of another stage's right-hand side from this stage's
@@ -2654,13 +2668,16 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
   }
   static const int prof_on = env_int2("STMHD_SWEEP_PROF", 0);
   DevBuf pr;
-  DevBuf tlb;
+  DevBuf tlb, pcb;
   if (prof_on) {
     pr.alloc((size_t)stg[ts]->ncta * warps * 10 * sizeof(unsigned long long));
     m.st[ts].prof = pr.as<unsigned long long>();
     tlb.alloc((size_t)warps * 128 * sizeof(unsigned long long));
     STMHD_CUDA_CHECK(cudaMemsetAsync(tlb.ptr, 0, tlb.bytes, s));
     m.st[ts].tline = tlb.as<unsigned long long>();
+    pcb.alloc((size_t)2 * stg[ts]->ncta * sizeof(unsigned long long));
+    STMHD_CUDA_CHECK(cudaMemsetAsync(pcb.ptr, 0, pcb.bytes, s));
+    m.st[ts].pcta = pcb.as<unsigned long long>();
   }
   // L2 prefetch cluster (cluster mode): one extra 16-CTA cluster when the device
   // can hold it next to the stages (STMHD_SWEEP_L2PF = prefetch distance in slabs, 0 off)
@@ -2794,6 +2811,13 @@ void sweep_stages_launch(SweepStage *const *stg, int nst, cudaStream_t s) {
     unsigned long long t0 = ~0ull;
     for (auto v : tv)
       if (v) t0 = std::min(t0, v & ((1ull << 56) - 1));
+    {
+      std::vector<unsigned long long> pc((size_t)2 * stg[ts]->ncta);
+      STMHD_CUDA_CHECK(cudaMemcpy(pc.data(), pcb.ptr, pc.size() * 8, cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[pcta] slab 1 subtree fwd/bwd (us) per CTA:");
+      for (int c = 0; c < stg[ts]->ncta; ++c) fprintf(stderr, " %d:%.1f/%.1f", c, pc[2 * c] / 1e3, pc[2 * c + 1] / 1e3);
+      fprintf(stderr, "\n");
+    }
     for (int wv = 0; wv < warps; ++wv) {
       fprintf(stderr, "[tl] w%02d:", wv);
       for (int i = 0; i < 128; ++i) {
