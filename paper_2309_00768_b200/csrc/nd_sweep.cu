@@ -123,7 +123,9 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   // direction than one subtree per CTA, C4/C3 P_T^-1 -8 % -- and one per CTA for a
   // whole-GPU single sweep, where 64 measured 30 % slower on C5)
   static const int maxsub_env = env_int2("STMHD_SWEEP_GRID_SUBTREES", 0);
-  const int maxsub_dflt = ncta < num_sms() ? 64 : ncta;
+  // 2^(levels - 5): leaves the 4 dense-top levels plus 1-2 band levels above the
+  // subtrees (64 at 64^2, 32 at 32^2 -- the measured optima)
+  const int maxsub_dflt = ncta < num_sms() ? std::min(ncta, 1 << std::max(0, std::min(p.nlevels - 5, 20))) : ncta;
   const int max_sub = ncta > 16 ? std::min(maxsub_env > 0 ? maxsub_env : maxsub_dflt, ncta) : ncta;
   std::vector<int> frontier;
   if (D) {

@@ -436,7 +436,10 @@ void PC::apply_inverse_pipelined(const double *r, double *x, cudaStream_t s) {
     const char *e = getenv("STMHD_PC_GRID");
     return e ? atoi(e) : -1;
   }();
-  const bool grid = grid_env == 1 || (grid_env < 0 && 8.0 * (double)fu->dev->plan->factor_size > 24e6 &&
+  // (round 2: with the 2^(levels-5)-subtree plans and early coupling the grid family
+  // also wins at 32^2 -- C2 2.74 -> 2.47 ms -- but not at 16^2, C1 0.26 vs 0.37 ms:
+  // velocity factors above 4 MB per slab take it)
+  const bool grid = grid_env == 1 || (grid_env < 0 && 8.0 * (double)fu->dev->plan->factor_size > 4e6 &&
                                       num_sms() >= 64);
   static const int fu_ctas_env = [] {
     const char *e = getenv("STMHD_PC_FU_CTAS");
