@@ -123,13 +123,12 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   // direction than one subtree per CTA, C4/C3 P_T^-1 -8 % -- and one per CTA for a
   // whole-GPU single sweep, where 64 measured 30 % slower on C5)
   static const int maxsub_env = env_int2("STMHD_SWEEP_GRID_SUBTREES", 0);
-  // a power of two (a balanced frontier of the nested-dissection tree), at most the
-  // CTA count and at most 2^(levels - 5), which leaves the 4 dense-top levels plus 1-2
-  // band levels above the subtrees: 64 at 64^2, 32 at 32^2, 128 for C5's whole-GPU
-  // sweep (measured optima; non-powers of two split the tree unevenly)
+  // the largest power of two <= the CTA count (a balanced frontier of the
+  // nested-dissection tree; 96 or 112 subtrees split it unevenly and measured 30 %
+  // slower): 64 for a 116-CTA stage of the pipelined launch, 128 for a whole-GPU sweep
   int pow2 = 1;
   while (pow2 * 2 <= ncta) pow2 *= 2;
-  const int maxsub_dflt = std::min(pow2, 1 << std::max(0, std::min(p.nlevels - 5, 20)));
+  const int maxsub_dflt = pow2;
   const int max_sub = ncta > 16 ? std::min(maxsub_env > 0 ? maxsub_env : maxsub_dflt, ncta) : ncta;
   std::vector<int> frontier;
   if (D) {
