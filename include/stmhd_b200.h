@@ -168,6 +168,21 @@ int stmhd_lu_info(stmhd_lu lu, int64_t *info5);
 int stmhd_nd_plan_info(int64_t n, const int32_t *rowptr, const int32_t *col, const int32_t *gx,
                        const int32_t *gy, int leaf_max, int64_t *info8);
 
+/* ---- state-independent operators on the device (constops.cu) ----
+   CSR of sum_e P_r(e)^T local[e & 1] P_c(e) on the uniform right-triangulated mesh:
+   the reference's assemble_mass / assemble_stiffness / assemble_divergence
+   (fem.py:211-271) as used by Discretization (problems.py:185-204).  Row space with nr
+   and column space with nc nodes per element; (ne_ptr, ne_code) lists the elements of
+   each row node (code = element * 16 + local row, ascending), elem_c the column nodes
+   per element, local the two orientation matrices [2][nr][nc].  All pointers are HOST
+   arrays (one-time setup): rowptr (n_rows + 1), col / val (capacity entries) and *nnz
+   are written; columns sorted, structural zeros kept, contributions summed in
+   ascending element order.  Synchronises. */
+int stmhd_const_assemble(void *stream, int64_t n_rows, int nr, int nc, int64_t ne,
+                         const int32_t *ne_ptr, const int32_t *ne_code, const int32_t *elem_c,
+                         const double *local, int32_t *rowptr, int32_t *col, double *val,
+                         int64_t capacity, int64_t *nnz);
+
 /* ---- configuration-5 scalar advection-diffusion block (oracle/c5.py) ----
    values[k*nnz + e] = base[e] + sum over the entry's element contributions cinfo
    ({element, local row i, local col j, orientation o}, ranges cptr) of

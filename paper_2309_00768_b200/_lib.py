@@ -60,6 +60,7 @@ _SIGS = {
     "stmhd_spmv_sell_size": (c_i64, [c_vp]),
     "stmhd_spmv_relayout": (c_int, [c_vp, P, c_int, P, c_i64, P]),
     "stmhd_spmv_apply": (c_int, [c_vp, P, c_int, P, c_dbl, c_dbl, P, P]),
+    "stmhd_const_assemble": (c_int, [P, c_i64, c_int, c_int, c_i64, P, P, P, P, P, P, P, c_i64, P]),
     "stmhd_jac_sell_size": (c_i64, [c_vp, P]),
     "stmhd_jac_relayout": (c_int, [c_vp, P, P, P]),
     "stmhd_jac_apply_sell": (c_int, [c_vp, P, P, P, P]),
@@ -67,7 +68,7 @@ _SIGS = {
 
 EXPORTS = tuple(_SIGS)
 # must equal stmhd_abi_version() of the loaded library (include/stmhd_b200.h)
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 def lib_path() -> str:

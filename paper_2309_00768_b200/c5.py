@@ -95,9 +95,12 @@ def c5_host_tables(n: int, dt: float = 1e-2, eps: float = 1e-3) -> dict:
     eid = np.repeat(np.arange(ne), 9)
     keep = ~isbc[rows] & ~isbc[cols]
     ent = np.searchsorted(keys, rows * nn + cols)
-    base = np.zeros(nnz)
-    loc = (np.asarray(T["M1"])[None, :, :] / dt + eps * np.asarray(T["K1"])[o]).reshape(-1)
-    np.add.at(base, ent[keep], loc[keep])
+    # constant part M/dt + eps K: assembled on the device (fem._assemble, csrc/constops.cu),
+    # picked at the entries bc_identity keeps
+    a0 = fem._assemble(p1, p1, np.asarray(T["M1"])[None, :, :] / dt + eps * np.asarray(T["K1"]))
+    akeys = np.repeat(np.arange(nn, dtype=np.int64), np.diff(a0.indptr)) * nn + a0.indices
+    base = a0.data[np.searchsorted(akeys, keys)]
+    base[isbc[prow] | isbc[pcol]] = 0.0
     base[np.searchsorted(keys, bc * nn + bc)] = 1.0
     order = np.argsort(ent[keep], kind="stable")
     ce = ent[keep][order]

@@ -30,7 +30,7 @@ struct stmhd_lu_s {
 
 extern "C" {
 
-int stmhd_abi_version(void) { return 2; }
+int stmhd_abi_version(void) { return 3; }
 int64_t stmhd_launch_count(void) { return stmhd::g_launches.load(); }
 const char *stmhd_last_error(void) { return g_last_error.c_str(); }
 const char *stmhd_last_block(void) { return g_last_block.c_str(); }

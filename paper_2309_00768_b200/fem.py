@@ -226,17 +226,36 @@ def element_tensors(kv: int, kp: int, hx: float, hy: float) -> dict:
     return T
 
 
-# -- constant operators (host scipy, state independent) ---------------------------
+# -- constant operators (state independent; values assembled on the device) ----------
 
 def _assemble(sr: Space, sc: Space, local_by_o, roff=0, coff=0, shape=None):
-    """COO assembly of a per-orientation local matrix (no, nr, nc)."""
+    """CSR of a per-orientation local matrix (no, nr, nc) summed over the elements:
+    reference assemble_mass / assemble_stiffness / assemble_divergence (fem.py:211-271).
+    The pattern and the values come from the device kernels of csrc/constops.cu
+    (C-ABI stmhd_const_assemble); there is no host fallback."""
+    from . import _lib
+
+    lib = _lib.load()
+    loc = np.ascontiguousarray(np.asarray(local_by_o, dtype=np.float64))
+    nr, nc = sr.elem.shape[1], sc.elem.shape[1]
+    assert loc.shape == (2, nr, nc)
     ne = sr.mesh.ne
-    o = np.arange(ne) & 1
-    loc = np.asarray(local_by_o)[o]
-    rows = np.repeat(sr.elem[:, :, None] + roff, sc.elem.shape[1], axis=2)
-    cols = np.repeat(sc.elem[:, None, :] + coff, sr.elem.shape[1], axis=1)
+    ptr, code = sr.node_elements()
+    elem_c = np.ascontiguousarray(sc.elem, dtype=np.int32)
+    cap = int(ne) * nr * nc
+    rowptr = np.empty(sr.n_nodes + 1, np.int32)
+    col = np.empty(cap, np.int32)
+    val = np.empty(cap, np.float64)
+    nnz = np.zeros(1, np.int64)
+    _lib.check(lib.stmhd_const_assemble(_lib.stream_ptr(), sr.n_nodes, nr, nc, ne, _lib.ptr(ptr), _lib.ptr(code),
+                                        _lib.ptr(elem_c), _lib.ptr(loc), _lib.ptr(rowptr), _lib.ptr(col),
+                                        _lib.ptr(val), cap, _lib.ptr(nnz)))
+    n = int(nnz[0])
     shape = shape or (sr.n_nodes, sc.n_nodes)
-    return sp.coo_matrix((loc.ravel(), (rows.ravel(), cols.ravel())), shape=shape).tocsr()
+    rp = rowptr
+    if roff or shape[0] != sr.n_nodes:
+        rp = np.concatenate([np.zeros(roff, np.int32), rowptr, np.full(shape[0] - roff - sr.n_nodes, n, np.int32)])
+    return sp.csr_matrix((val[:n].copy(), col[:n] + np.int32(coff), rp), shape=shape)
 
 
 def blockdiag2(m):

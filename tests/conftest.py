@@ -42,3 +42,17 @@ def csr_from(g, prefix):
 
     return sp.csr_matrix((g[prefix + "_data"], g[prefix + "_indices"], g[prefix + "_indptr"]),
                          shape=tuple(g[prefix + "_shape"]))
+
+
+def host_assemble(sr, sc, local_by_o, roff=0, coff=0, shape=None):
+    """Host stand-in for fem._assemble (the device assembly of the constant operators)
+    so that the CPU-only tests of host tables can build a Discretization without a GPU:
+    the element matrices scattered through scipy's COO -> CSR sum.  Test infrastructure
+    only; tests/test_constops_gpu.py checks the device kernels against the reference."""
+    import scipy.sparse as sp
+
+    loc = np.asarray(local_by_o)[np.arange(sr.mesh.ne) & 1]
+    rows = np.repeat(sr.elem[:, :, None] + roff, sc.elem.shape[1], axis=2)
+    cols = np.repeat(sc.elem[:, None, :] + coff, sr.elem.shape[1], axis=1)
+    return sp.coo_matrix((loc.ravel(), (rows.ravel(), cols.ravel())),
+                         shape=shape or (sr.n_nodes, sc.n_nodes)).tocsr()

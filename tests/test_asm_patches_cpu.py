@@ -11,14 +11,19 @@ import pytest
 def _disc(n):
     import paper_2309_00768_b200.discretization as D
 
-    orig = D.Discretization._build_handle
+    from paper_2309_00768_b200 import fem
+    from conftest import host_assemble
+
+    orig, orig_asm = D.Discretization._build_handle, fem._assemble
     D.Discretization._build_handle = lambda self: None
+    fem._assemble = host_assemble  # no GPU here: host stand-in for the device constant assembly
     try:
         from paper_2309_00768_b200 import problems
 
         d = D.Discretization(problems.baseline_island(1e-2), 2.0 / n, 0.1, 0.2)
     finally:
         D.Discretization._build_handle = orig
+        fem._assemble = orig_asm
     return d
 
 

@@ -29,7 +29,7 @@ def test_library_exports_every_header_symbol():
     assert not missing, missing
     # and the Python binding declares every header symbol
     assert set(syms) <= set(_lib.EXPORTS), set(syms) - set(_lib.EXPORTS)
-    assert lib.stmhd_abi_version() == _lib.ABI_VERSION == 2
+    assert lib.stmhd_abi_version() == _lib.ABI_VERSION == 3
 
 
 def _plan_info(mat, gx, gy, leaf):
@@ -84,7 +84,15 @@ def test_element_tensors_match_oracle_operators():
     d = model.make_disc(configs.baseline_problem("island", 1e-2), 4, 0.1, 3)
     T = fem.element_tensors(2, 1, 0.5, 0.5)
     m = fem.Mesh(-1, 1, -1, 1, 4, 4)
-    ops = fem.constant_operators(fem.Space(m, 2, 2), fem.Space(m, 1), fem.Space(m, 1), T)
+    from conftest import host_assemble as coo
+
+    vel, prs, p1 = fem.Space(m, 2, 2), fem.Space(m, 1), fem.Space(m, 1)
+    ops = {"mass_u": fem.blockdiag2(coo(vel, vel, [T["MV"], T["MV"]])),
+           "stiff_u": fem.blockdiag2(coo(vel, vel, T["KV"])),
+           "mass_p": coo(prs, prs, [T["MP"], T["MP"]]), "stiff_p": coo(prs, prs, T["KP"]),
+           "mass_1": coo(p1, p1, [T["M1"], T["M1"]]), "stiff_1": coo(p1, p1, T["K1"]),
+           "div": sum(coo(prs, vel, T["BD"][:, :, :, c], coff=c * vel.n_nodes, shape=(prs.ndof, vel.ndof))
+                      for c in range(2))}
     for name, ref in (("mass_u", d.mass_u), ("stiff_u", d.stiff_u), ("mass_p", d.mass_p),
                       ("stiff_p", d.stiff_p), ("mass_1", d.mass_j), ("stiff_1", d.stiff_a), ("div", d.div)):
         assert abs(ops[name] - ref).max() <= 1e-14 * abs(ref).max(), name
@@ -176,14 +184,16 @@ def test_overhead_ratio_arithmetic_and_errors():
         compute_overhead_ratios(seq, st)
 
 
-def test_c5_host_tables_match_reference(golden):
+def test_c5_host_tables_match_reference(golden, monkeypatch):
     """The configuration-5 tables the device assembly consumes, contracted on the host
     in numpy, reproduce the reference's F_k (golden, make_golden.py c5_case) and its
     coupling bc_zero(M/dt) -- pattern exactly, values to 1e-12."""
-    from conftest import csr_from
+    from conftest import csr_from, host_assemble
+    from paper_2309_00768_b200 import fem
     from paper_2309_00768_b200.c5 import c5_host_tables
 
     g = golden("c5_tiny")
+    monkeypatch.setattr(fem, "_assemble", host_assemble)  # no GPU here (device path: test_c5_gpu.py)
     h = c5_host_tables(8)
     nn = h["p1"].n_nodes
     el = h["p1"].elem
