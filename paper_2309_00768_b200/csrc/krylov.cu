@@ -2,6 +2,8 @@
 // linalg.py:163-199, replaced by classical Gram-Schmidt with one
 // re-orthogonalisation, CGS2).  Reductions are two-stage with a fixed order,
 // so results are bitwise reproducible run to run.
+#include <cstdlib>
+
 #include "disc.hpp"
 
 namespace stmhd {
@@ -9,6 +11,11 @@ namespace stmhd {
 constexpr int KT = 256;       // threads per block
 constexpr int KE = 4;         // elements per thread
 constexpr int KCH = KT * KE;  // elements per block
+
+static int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
 
 static int nblocks_for(int64_t n) { return (int)std::max<int64_t>(1, (n + KCH - 1) / KCH); }
 
@@ -44,11 +51,64 @@ __global__ void __launch_bounds__(KT) dots_partial(const double *V, int64_t ldv,
   }
 }
 
+// Same sums as dots_partial (per vector: the block's 4 x 256 elements in the same order,
+// same warp and block reductions, so the results are bitwise identical), with KU basis
+// vectors per pass: 4 KU independent loads in flight per thread instead of 4.
+constexpr int KU = 4;
+
+__global__ void __launch_bounds__(KT) dots_partial_u(const double *__restrict__ V, int64_t ldv, int nvec,
+                                                     const double *__restrict__ w, int64_t n, double *partial) {
+  extern __shared__ double sh[];  // nvec * 8
+  const int64_t base = (int64_t)blockIdx.x * KCH + threadIdx.x;
+  double wv[KE];
+  bool ok[KE];
+#pragma unroll
+  for (int q = 0; q < KE; ++q) {
+    const int64_t i = base + q * KT;
+    ok[q] = i < n;
+    wv[q] = ok[q] ? w[i] : 0.0;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int v0 = 0; v0 < nvec; v0 += KU) {
+    double x[KU][KE];
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const double *Vi = V + (int64_t)min(v0 + u, nvec - 1) * ldv + base;
+#pragma unroll
+      for (int q = 0; q < KE; ++q) x[u][q] = ok[q] ? Vi[q * KT] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < KE; ++q)
+        if (ok[q]) acc += x[u][q] * wv[q];
+      acc = warp_sum(acc);
+      if (lane == 0 && v0 + u < nvec) sh[(v0 + u) * 8 + warp] = acc;
+    }
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < nvec; v += KT) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += sh[v * 8 + q];
+    partial[(int64_t)v * gridDim.x + blockIdx.x] = s;
+  }
+}
+
 __global__ void reduce_partial(const double *partial, int nblk, double *out) {
   __shared__ double sh[32];
   const double *p = partial + (int64_t)blockIdx.x * nblk;
   double acc = 0.0;
-  for (int i = threadIdx.x; i < nblk; i += blockDim.x) acc += p[i];
+  int i = threadIdx.x;
+  for (; i + 7 * (int)blockDim.x < nblk; i += 8 * blockDim.x) {  // eight loads in flight, added in order
+    double x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = p[i + q * blockDim.x];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc += x[q];
+  }
+  for (; i < nblk; i += blockDim.x) acc += p[i];
   acc = block_sum(acc, sh);
   if (threadIdx.x == 0) out[blockIdx.x] = acc;
 }
@@ -96,6 +156,81 @@ __global__ void __launch_bounds__(KT) update_partial(const double *V, int64_t ld
       }
       acc = warp_sum(acc);
       if (lane == 0) sh[v * 8 + warp] = acc;
+    }
+  if (do_norm) {
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < KE; ++q) acc += wv[q] * wv[q];
+    acc = warp_sum(acc);
+    if (lane == 0) sh[(do_dots ? nvec : 0) * 8 + warp] = acc;
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < nout; v += KT) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += sh[v * 8 + q];
+    partial[(int64_t)v * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// update_partial with KU basis vectors per pass (same arithmetic in the same order).
+__global__ void __launch_bounds__(KT) update_partial_u(const double *__restrict__ V, int64_t ldv, int nvec,
+                                                       const double *__restrict__ h, double *w, int64_t n,
+                                                       double *partial, int do_dots, int do_norm) {
+  extern __shared__ double sh[];  // (nvec+1)*8 + nvec
+  double *hs = sh + (nvec + 1) * 8;
+  for (int v = threadIdx.x; v < nvec; v += KT) hs[v] = h[v];
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * KCH + threadIdx.x;
+  double wv[KE];
+  bool ok[KE];
+#pragma unroll
+  for (int q = 0; q < KE; ++q) {
+    const int64_t i = base + q * KT;
+    ok[q] = i < n;
+    wv[q] = ok[q] ? w[i] : 0.0;
+  }
+  for (int v0 = 0; v0 < nvec; v0 += KU) {
+    double x[KU][KE];
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const double *Vi = V + (int64_t)min(v0 + u, nvec - 1) * ldv + base;
+#pragma unroll
+      for (int q = 0; q < KE; ++q) x[u][q] = ok[q] ? Vi[q * KT] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      if (v0 + u >= nvec) break;
+      const double hv = hs[v0 + u];
+#pragma unroll
+      for (int q = 0; q < KE; ++q)
+        if (ok[q]) wv[q] -= hv * x[u][q];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < KE; ++q)
+    if (ok[q]) w[base + q * KT] = wv[q];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nout = (do_dots ? nvec : 0) + (do_norm ? 1 : 0);
+  if (!nout) return;
+  if (do_dots)
+    for (int v0 = 0; v0 < nvec; v0 += KU) {
+      double x[KU][KE];
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const double *Vi = V + (int64_t)min(v0 + u, nvec - 1) * ldv + base;
+#pragma unroll
+        for (int q = 0; q < KE; ++q) x[u][q] = ok[q] ? Vi[q * KT] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < KE; ++q)
+          if (ok[q]) acc += x[u][q] * wv[q];
+        acc = warp_sum(acc);
+        if (lane == 0 && v0 + u < nvec) sh[(v0 + u) * 8 + warp] = acc;
+      }
     }
   if (do_norm) {
     double acc = 0.0;
@@ -167,7 +302,9 @@ void gs_dots(cudaStream_t s, const double *V, int64_t ldv, int nvec, const doubl
              double *work) {
   if (nvec <= 0) return;
   int B = nblocks_for(n);
-  dots_partial<<<B, KT, nvec * 8 * sizeof(double), s>>>(V, ldv, nvec, w, n, work);
+  static const int v1 = env_int("STMHD_GS_V1", 0);  // 1: one basis vector per pass (the first version)
+  if (v1) dots_partial<<<B, KT, nvec * 8 * sizeof(double), s>>>(V, ldv, nvec, w, n, work);
+  else dots_partial_u<<<B, KT, nvec * 8 * sizeof(double), s>>>(V, ldv, nvec, w, n, work);
   STMHD_LAUNCH_CHECK();
   reduce_partial<<<nvec, 256, 0, s>>>(work, B, h);
   STMHD_LAUNCH_CHECK();
@@ -177,7 +314,9 @@ void gs_update(cudaStream_t s, const double *V, int64_t ldv, int nvec, const dou
                double *h2, double *nrm2, double *work) {
   int B = nblocks_for(n);
   size_t smem = ((nvec + 1) * 8 + nvec) * sizeof(double);
-  update_partial<<<B, KT, smem, s>>>(V, ldv, nvec, h, w, n, work, h2 != nullptr, nrm2 != nullptr);
+  static const int v1 = env_int("STMHD_GS_V1", 0);
+  if (v1) update_partial<<<B, KT, smem, s>>>(V, ldv, nvec, h, w, n, work, h2 != nullptr, nrm2 != nullptr);
+  else update_partial_u<<<B, KT, smem, s>>>(V, ldv, nvec, h, w, n, work, h2 != nullptr, nrm2 != nullptr);
   STMHD_LAUNCH_CHECK();
   if (h2) {
     reduce_partial<<<nvec, 256, 0, s>>>(work, B, h2);

@@ -836,11 +836,21 @@ void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s
       smem_attr = kFactorSmemMax;
     }
   }
+  // STMHD_FACTOR_TRACE=1: per level of the first chunk, the kernel, front count, largest
+  // front and duration (events; diagnostics only)
+  static const bool ftrace = getenv("STMHD_FACTOR_TRACE") != nullptr;
+  std::vector<cudaEvent_t> fev;
   for (int b0 = 0; b0 < nbatch; b0 += chunk) {
     int nbch = std::min(chunk, nbatch - b0);
     for (int l = 0; l < p.nlevels; ++l) {
       int cnt = (int)p.level_sn[l].size();
       if (!cnt) continue;
+      if (ftrace && b0 == 0) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        fev.push_back(e);
+      }
       FactorArgs a{};
       a.lvl_sn = dev->lvl_sn.as<int>() + lptr[l];
       a.ns = dev->ns.as<int>();
@@ -882,6 +892,36 @@ void NDFactor::factor(const double *values, int64_t value_stride, cudaStream_t s
         dev->fl_off.as<int64_t>(), dev->fu_off.as<int64_t>(), stage.as<double>(), p.stage_size, factors.as<double>(),
         p.factor_size, b0);
     STMHD_LAUNCH_CHECK();
+    if (ftrace && b0 == 0) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, s);
+      fev.push_back(e);
+      cudaEventCreate(&e);
+      cudaEventRecord(e, s);
+      fev.push_back(e);
+      cudaEventSynchronize(e);
+      size_t i = 0;
+      for (int l = 0; l < p.nlevels; ++l) {
+        const int cnt = (int)p.level_sn[l].size();
+        if (!cnt) continue;
+        int mf = 0, mns = 0;
+        for (int sn : p.level_sn[l]) {
+          mf = std::max(mf, p.ns[sn] + p.nb[sn]);
+          mns = std::max(mns, p.ns[sn]);
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, fev[i], fev[i + 1]);
+        fprintf(stderr, "[factor-trace] level %d %s fronts %d x %d max f %d ns %d: %.3f ms\n", l,
+                lvl_wf[l] > 0 ? "warp" : (lvl_smem[l] > 0 ? "smem" : "global"), cnt, nbch, mf, mns, ms);
+        ++i;
+      }
+      float ms = 0;
+      cudaEventElapsedTime(&ms, fev[i], fev[i + 1]);
+      fprintf(stderr, "[factor-trace] relayout %.3f ms (chunk of %d of %d matrices)\n", ms, nbch, nbatch);
+      for (auto e : fev) cudaEventDestroy(e);
+      fev.clear();
+    }
   }
   // keep the workspaces alive until the kernels finish
   STMHD_CUDA_CHECK(cudaStreamSynchronize(s));
