@@ -35,12 +35,12 @@ DCsr stmhd_disc_s::csr(const char *prefix) const {
 }
 
 static std::unique_ptr<NDPlan> make_plan(stmhd_disc_s *d, const std::string &pat, const char *gx, const char *gy,
-                                         const char *map, int leaf) {
+                                         const char *map, int leaf, int merge_depth = -1) {
   const HostArray &rp = d->H((pat + "_rowptr").c_str());
   const HostArray &ci = d->H((pat + "_col").c_str());
   const int32_t *vmap = map ? d->H(map).as<int32_t>() : nullptr;
   auto p = std::make_unique<NDPlan>(nd_analyze(rp.count - 1, rp.as<int32_t>(), ci.as<int32_t>(),
-                                               d->H(gx).as<int32_t>(), d->H(gy).as<int32_t>(), leaf, vmap));
+                                               d->H(gx).as<int32_t>(), d->H(gy).as<int32_t>(), leaf, vmap, merge_depth));
   return p;
 }
 
@@ -120,7 +120,13 @@ int stmhd_disc_finalize(stmhd_disc d, void *stream) {
   for (const char *k : {"nt", "n_u", "n_p", "n_j", "n_a", "nv", "npl", "ne", "nnv", "nnp", "nn1", "nnz_js", "nnz_fp"})
     (void)d->I(k);
   int lf = (int)d->I("leaf_fu"), lc = (int)d->I("leaf_ca"), lk = (int)d->I("leaf_c");
-  d->plan_fu = make_plan(d, "fu", "fu_gx", "fu_gy", "fu_map", lf);
+  // velocity block of the grid-family sweeps (n_u >= 8000: 32^2 P2 meshes and larger): the
+  // separators at tree depth 4 absorb their children (nd_analyze), one grid-wide tree level
+  // fewer per sweep direction between the 64 CTA-local subtrees and the dense top
+  // (STMHD_ND_MERGE_DEPTH: depth, -1 off)
+  int merge_depth = d->I("n_u") >= 8000 ? 4 : -1;
+  if (const char *e = getenv("STMHD_ND_MERGE_DEPTH")) merge_depth = atoi(e);
+  d->plan_fu = make_plan(d, "fu", "fu_gx", "fu_gy", "fu_map", lf, merge_depth);
   d->plan_fa = make_plan(d, "fa", "p1_gx", "p1_gy", "fa_map", lc);
   d->plan_ca = make_plan(d, "ca", "p1_gx", "p1_gy", nullptr, lc);
   d->plan_fp = make_plan(d, "fp", "prs_gx", "prs_gy", nullptr, lc);

@@ -53,12 +53,16 @@ struct NDPlan {
   int64_t sym_nnz = 0;  // nnz of L+U implied by the supernodal structure
   int max_front = 0;
   std::vector<std::vector<int>> level_sn;
+  // amalgamated supernodes (nd_analyze merge_depth) have up to four children; a front row
+  // then takes up to four child updates (the gather tables carry two more slots)
+  int nwide = 0;
+  bool wide(int s) const { return child_ptr[s + 1] - child_ptr[s] > 2; }
 };
 
 // Build the plan.  gx/gy may be null (graph bisection).  value_map (may be null)
 // maps pattern entries to caller value indices.
 NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const int32_t *gx,
-                  const int32_t *gy, int leaf_max, const int32_t *value_map);
+                  const int32_t *gy, int leaf_max, const int32_t *value_map, int merge_depth = -1);
 
 // Work item of the cluster-resident time sweep (nd_sweep.cu), built lazily for a
 // launch shape: a contiguous chunk range of one supernode.  32 bytes, so a warp's
@@ -127,7 +131,8 @@ struct NDSweepPlan {
   int tab_ints = 0;
   DevBuf tab, tab_ptr, tab_nf;
   DevBuf tab_band, tab_band_ptr;  // per-CTA band positions referenced by the backward tables
-  DevBuf g3p;   // int4 per front position: {permuted rhs index or -1, cb1, cb2, 0}
+  DevBuf g3p;   // int4 per front position: {permuted rhs index or -1, cb1, cb2, cb3} (cb3: wide supernodes)
+  DevBuf g4p;   // int per front position: cb4 of wide supernodes (else -1)
   DevBuf bpos;  // int per front position: permuted position of the front entry
   DevBuf bpos4; // bpos per supernode, each block 16-byte aligned (TMA ring table items)
   DevBuf pos;   // n: elimination position of each original index
@@ -150,6 +155,7 @@ struct NDDevice {
       scat_src, scat_dst, fl_off, fu_off, sfl_off, sfu_off, rf, rb, bsz_f, bsz_b, front_off, cbv_off, lvl_sn,
       lvl_ptr;
   // solve work items: int4 {sn, row_begin, row_end, 0} (32-row chunks); per level ranges
+  DevBuf gather4;  // int per front position: fourth child update of wide supernodes
   DevBuf fwd_items, bwd_items, gather3;  // SolveItem lists + flat forward gather table (int4 per front position)
   std::vector<int> fwd_ptr, bwd_ptr;  // host copies of level ranges (nlevels+1)
   DevBuf fwd_ptr_d, bwd_ptr_d;
@@ -187,7 +193,7 @@ struct SweepCoupling {
 // Flat descriptor of one solve work item: everything a warp needs in one load.
 struct alignas(16) SolveItem {
   int s, r0, r1, kl;  // supernode, row range, lanes per row
-  int ns, f, pad0, pad1;
+  int ns, f, wide, pad1;  // wide: the supernode has more than two children (gather3.w / gather4 in use)
   int64_t foff;   // factor offset (FL^T forward, FU^T backward)
   int64_t goff;   // offset of the supernode's front lists (idx / gather3)
   int64_t first;  // elimination position of the first column

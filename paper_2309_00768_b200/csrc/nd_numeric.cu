@@ -692,6 +692,7 @@ void NDDevice::build(const NDPlan &p, cudaStream_t s) {
     SolveItem it{};
     it.s = sn; it.r0 = c * R; it.r1 = std::min(rows, (c + 1) * R); it.kl = 32 / R;
     it.ns = p.ns[sn]; it.f = p.ns[sn] + p.nb[sn];
+    it.wide = p.wide(sn);
     it.foff = off; it.goff = p.idx_off[sn]; it.first = p.first[sn]; it.cboff = p.cbv_off[sn];
     return it;
   };
@@ -712,23 +713,29 @@ void NDDevice::build(const NDPlan &p, cudaStream_t s) {
     }
     bwd_ptr.push_back((int)bw.size());
   }
-  std::vector<int4> g3(p.idx.size(), make_int4(-1, -1, -1, 0));
+  // child update slots per front position: children 0, 1 -> y, z; children 2, 3 of an
+  // amalgamated (wide) supernode -> w and the parallel table g4
+  std::vector<int4> g3(p.idx.size(), make_int4(-1, -1, -1, -1));
+  std::vector<int> g4(std::max<size_t>(p.idx.size(), 1), -1);
   for (int sn = 0; sn < p.nsn; ++sn) {
     int64_t o = p.idx_off[sn];
     for (int t = 0; t < p.ns[sn]; ++t) g3[o + t].x = p.idx[o + t];
     int which = 0;
     for (int ci = p.child_ptr[sn]; ci < p.child_ptr[sn + 1]; ++ci, ++which) {
       int c = p.child_list[ci];
-      require(which < 2, "nd solve: supernode with more than two children");
+      require(which < 4, "nd solve: supernode with more than four children");
       for (int a = 0; a < p.nb[c]; ++a) {
         int pos = p.emap[p.emap_off[c] + a];
         int src = (int)(p.cbv_off[c] + a);
         if (which == 0) g3[o + pos].y = src;
-        else g3[o + pos].z = src;
+        else if (which == 1) g3[o + pos].z = src;
+        else if (which == 2) g3[o + pos].w = src;
+        else g4[o + pos] = src;
       }
     }
   }
   gather3 = upload_vec(g3, s);
+  gather4 = upload_vec(g4, s);
   fwd_items = upload_vec(fw, s);
   bwd_items = upload_vec(bw, s);
   fwd_ptr_d = upload_vec(fwd_ptr, s);
@@ -953,6 +960,7 @@ int NDFactor::check_status(cudaStream_t s) const {
 struct SolveArgs {
   const SolveItem *fwd_items, *bwd_items;
   const int4 *gather3;
+  const int *gather4;
   const int *idx;
   const int *fwd_ptr, *bwd_ptr;
   int nlevels;
@@ -999,7 +1007,7 @@ __device__ void warp_gather(const SolveArgs &a, const double *rhs, const SolveIt
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int t = t0 + 32 * q;
-      gg[q] = t < it.f ? g[t] : make_int4(-1, -1, -1, 0);
+      gg[q] = t < it.f ? g[t] : make_int4(-1, -1, -1, -1);
     }
     double vv[4];
 #pragma unroll
@@ -1008,6 +1016,16 @@ __device__ void warp_gather(const SolveArgs &a, const double *rhs, const SolveIt
       const double c1 = gg[q].y >= 0 ? cb[gg[q].y] : 0.0;
       const double c2 = gg[q].z >= 0 ? cb[gg[q].z] : 0.0;
       vv[q] = (r + c1) + c2;
+    }
+    if (it.wide) {  // amalgamated supernode: children 2 and 3
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int t = t0 + 32 * q;
+        const int g4 = t < it.f ? a.gather4[it.goff + t] : -1;
+        const double c3 = gg[q].w >= 0 ? cb[gg[q].w] : 0.0;
+        const double c4 = g4 >= 0 ? cb[g4] : 0.0;
+        vv[q] += c3 + c4;
+      }
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -1160,7 +1178,12 @@ __global__ void __launch_bounds__(512, 1) nd_solve_cta_multi_kernel(SolveArgs a)
           const double r = gg.x >= 0 ? rhs[gg.x] : 0.0;
           const double c1 = gg.y >= 0 ? cb[gg.y] : 0.0;
           const double c2 = gg.z >= 0 ? cb[gg.z] : 0.0;
-          v[g * vs + t] = (r + c1) + c2;
+          double vv = (r + c1) + c2;
+          if (it.wide) {
+            const int g4 = a.gather4[it.goff + t];
+            vv += (gg.w >= 0 ? cb[gg.w] : 0.0) + (g4 >= 0 ? cb[g4] : 0.0);
+          }
+          v[g * vs + t] = vv;
         }
       }
       __syncwarp();
@@ -1319,6 +1342,7 @@ void NDFactor::solve_nd(const double *rhs, int64_t ld_rhs, double *x, int64_t ld
   a.fwd_items = dev->fwd_items.as<SolveItem>();
   a.bwd_items = dev->bwd_items.as<SolveItem>();
   a.gather3 = dev->gather3.as<int4>();
+  a.gather4 = dev->gather4.as<int>();
   a.idx = dev->idx.as<int>();
   a.fwd_ptr = dev->fwd_ptr_d.as<int>();
   a.bwd_ptr = dev->bwd_ptr_d.as<int>();

@@ -81,7 +81,10 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
       pos[i] = (int)(p.first[sn] + t);
       iperm[p.first[sn] + t] = i;
     }
-  std::vector<int4> g3(p.idx.size(), make_int4(-1, -1, -1, 0));
+  // child update slots per front position: children 0, 1 -> y, z; children 2, 3 of an
+  // amalgamated (wide) supernode -> w and the parallel table g4
+  std::vector<int4> g3(p.idx.size(), make_int4(-1, -1, -1, -1));
+  std::vector<int> g4(std::max<size_t>(p.idx.size(), 1), -1);
   std::vector<int> bpos(p.idx.size());
   for (int sn = 0; sn < p.nsn; ++sn) {
     int64_t o = p.idx_off[sn];
@@ -91,12 +94,14 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     int which = 0;
     for (int ci = p.child_ptr[sn]; ci < p.child_ptr[sn + 1]; ++ci, ++which) {
       int c = p.child_list[ci];
-      require(which < 2, "nd sweep: supernode with more than two children");
+      require(which < 4, "nd sweep: supernode with more than four children");
       for (int a = 0; a < p.nb[c]; ++a) {
         int ps = p.emap[p.emap_off[c] + a];
         int src = (int)(p.cbv_off[c] + a);
         if (which == 0) g3[o + ps].y = src;
-        else g3[o + ps].z = src;
+        else if (which == 1) g3[o + ps].z = src;
+        else if (which == 2) g3[o + ps].w = src;
+        else g4[o + ps] = src;
       }
     }
   }
@@ -188,7 +193,11 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
       maxlen = std::max(maxlen, hi[r] - lo[r]);
       maxcb = std::max(maxcb, cbhi[r] - cblo[r]);
     }
-    if (D == 0 || 3 * maxlen + maxcb <= sub_budget) break;  // ys, xs, rhs_s + cbs
+    // amalgamated (wide) supernodes are handled by the top-level tasks only: a frontier
+    // above them (fewer subtrees than their children) falls back to the all-top schedule
+    bool wide_owned = false;
+    for (int sn = 0; sn < p.nsn && D > 0; ++sn) wide_owned |= owner[sn] >= 0 && p.wide(sn);
+    if (D == 0 || (!wide_owned && 3 * maxlen + maxcb <= sub_budget)) break;  // ys, xs, rhs_s + cbs
     D = 0;
   }
   if (D == 0) maxlen = maxcb = 0;
@@ -239,6 +248,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
     t.rows = (short)x.rows;
     t.R = (unsigned char)x.R;
     t.flags = cb_global ? 1 : 0;
+    if (fwd && p.wide(x.s)) t.flags |= 64;  // gather with the two extra child slots
     t.bsz = (int)(fwd ? p.bsz_f[x.s] : p.bsz_b[x.s]);
     const int64_t tbl_dbl = fwd ? 2LL * f : ((int64_t)f + 3) / 4 * 2;  // table size in doubles
     if (tables_env && tbl_dbl <= slot_dbl) t.flags |= fwd ? 4 : (4 | 8);
@@ -403,10 +413,35 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   std::vector<int> tab_all, tab_ptr(ncta + 1, 0), tab_nf(ncta, 0), tab_band, tab_band_ptr(ncta + 1, 0);
   bool stab = stab_env && mode == 0 && sp->dense && sp->nsub > 0 && maxlen < 32768 && maxcb < 32768 &&
               sp->ntT < 0x4000;
+  // with resident tables the CTA's update block is compact: an update vector written at
+  // subtree level h is read at level h + 1 only, so even and odd levels alternate between
+  // two regions (each as large as its fullest level) instead of every supernode keeping
+  // its own range -- about half the shared memory (C4 64-subtree plan: 1344 -> ~700 doubles)
+  std::vector<int> cbloc(p.nsn, -1);
+  if (stab) {
+    int64_t maxcb2 = 0;
+    for (int c = 0; c < ncta && c < (int)roots.size(); ++c) {
+      std::vector<int64_t> lsum(sp->nsub + 1, 0);
+      for (int sn = 0; sn < p.nsn; ++sn)
+        if (owner[sn] == c && sn != roots[c]) lsum[p.level[sn]] += p.nb[sn];
+      int64_t size[2] = {0, 0};
+      for (int h = 0; h <= sp->nsub; ++h) size[h & 1] = std::max(size[h & 1], lsum[h]);
+      std::vector<int64_t> cur(sp->nsub + 1);
+      for (int h = 0; h <= sp->nsub; ++h) cur[h] = (h & 1) ? size[0] : 0;
+      for (int sn = 0; sn < p.nsn; ++sn)
+        if (owner[sn] == c && sn != roots[c]) {
+          cbloc[sn] = (int)cur[p.level[sn]];
+          cur[p.level[sn]] += p.nb[sn];
+        }
+      maxcb2 = std::max(maxcb2, size[0] + size[1]);
+    }
+    maxcb = maxcb2;
+    sp->sub_cb = maxcb2;
+  }
   if (stab) {
     for (int sn = 0; sn < p.nsn; ++sn) sn_of_first[p.first[sn]] = sn;
     for (int c = 0; c < ncta && c < (int)roots.size(); ++c) {
-      const int64_t sf = info[4 * c], cbf = info[4 * c + 2];
+      const int64_t sf = info[4 * c];
       std::vector<int> fw;
       std::vector<unsigned short> bw;
       for (int sn = 0; sn < p.nsn; ++sn) {
@@ -415,11 +450,15 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
         const int64_t o = p.idx_off[sn];
         if (p.child_ptr[sn + 1] > p.child_ptr[sn]) {
           ftab_off[sn] = (int)fw.size();
-          for (int t = 0; t < f; ++t) {
-            const int y = g3[o + t].y >= 0 ? (int)(g3[o + t].y - cbf) : -1;
-            const int z = g3[o + t].z >= 0 ? (int)(g3[o + t].z - cbf) : -1;
-            fw.push_back((int)((unsigned)(y & 0xffff) | ((unsigned)(z & 0xffff) << 16)));
+          std::vector<int> yz[2] = {std::vector<int>(f, -1), std::vector<int>(f, -1)};
+          int which = 0;
+          for (int ci = p.child_ptr[sn]; ci < p.child_ptr[sn + 1]; ++ci, ++which) {
+            const int ch = p.child_list[ci];
+            require(which < 2 && cbloc[ch] >= 0, "nd sweep: subtree supernode with an unexpected child");
+            for (int a = 0; a < p.nb[ch]; ++a) yz[which][p.emap[p.emap_off[ch] + a]] = cbloc[ch] + a;
           }
+          for (int t = 0; t < f; ++t)
+            fw.push_back((int)((unsigned)(yz[0][t] & 0xffff) | ((unsigned)(yz[1][t] & 0xffff) << 16)));
         }
         btab_off[sn] = (int)bw.size();
         for (int t = p.ns[sn]; t < f; ++t) {
@@ -503,6 +542,8 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
               const int sn = sn_of_first[t.first];
               t.flags &= (unsigned char)~(4 | 8);
               if (fwd) {
+                // compact update block: the kernel adds cboff to cbs - cbfirst
+                if (!(t.flags & 1)) t.cboff = (int)(info[4 * c + 2] + cbloc[sn]);
                 if (ftab_off[sn] < 0) t.flags |= 16;
                 else {
                   t.flags |= 32;
@@ -665,6 +706,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   sp->pos_h = pos;
   sp->iperm_h = iperm;
   sp->g3p = upload_vec(g3, s);
+  sp->g4p = upload_vec(g4, s);
   sp->bpos = upload_vec(bpos, s);
   sp->bpos4 = upload_vec(bpos4, s);
   if (stab) {
@@ -718,6 +760,7 @@ struct SweepArgs {
   int post_per_slab;
   double *post_out;            // another stage's permuted right-hand sides (nslab x post_n)
   const int4 *g3p;
+  const int *g4p;  // fourth child update slot of wide supernodes (task flag 64)
   const int *bpos;
   const int *bpos4;            // 16-byte aligned bpos copy (ring table items)
   int nlevels, nw;
@@ -1011,11 +1054,62 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
       }
       w.v[t] = v;
     }
+  } else if (!SUB) {
+    // top-level task: the GEMV reads the ns column entries and the update needs the
+    // task's own rows beyond them, so only those front entries are gathered
+    // (entry tt of the list is front position tt < ns ? tt : rlo + tt - ns).
+    const int rlo = max((int)tk.ns, tk.c0 * (int)tk.R), rhi = min((int)tk.f, tk.c1 * (int)tk.R);
+    const int ng = tk.ns + max(0, rhi - rlo), sh = rlo - tk.ns;
+    if (tk.flags & 64) {
+      // amalgamated supernode: up to four child updates per entry (slot w of the table
+      // and the parallel g4 table); five entries per lane and pass
+      const int *g4 = a.g4p + tk.goff;
+      for (int b0 = lane; b0 < ng; b0 += 160) {
+        int4 gg[5];
+        int g5[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          const int tt = b0 + 32 * q, te = tt < tk.ns ? tt : tt + sh;
+          gg[q] = tt < ng ? g[te] : make_int4(-1, -1, -1, -1);
+          g5[q] = tt < ng ? g4[te] : -1;
+        }
+        double vv[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+          vv[q] = (((gg[q].x >= 0 ? rsrc[gg[q].x] : 0.0) + (gg[q].y >= 0 ? cbsrc[gg[q].y] : 0.0)) +
+                   (gg[q].z >= 0 ? cbsrc[gg[q].z] : 0.0)) +
+                  ((gg[q].w >= 0 ? cbsrc[gg[q].w] : 0.0) + (g5[q] >= 0 ? cbsrc[g5[q]] : 0.0));
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          const int tt = b0 + 32 * q;
+          if (tt < ng) w.v[tt < tk.ns ? tt : tt + sh] = vv[q];
+        }
+      }
+    } else {
+      for (int b0 = lane; b0 < ng; b0 += 256) {
+        int4 gg[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int tt = b0 + 32 * q;
+          gg[q] = tt < ng ? g[tt < tk.ns ? tt : tt + sh] : make_int4(-1, -1, -1, -1);
+        }
+        double vv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          vv[q] = ((gg[q].x >= 0 ? rsrc[gg[q].x] : 0.0) + (gg[q].y >= 0 ? cbsrc[gg[q].y] : 0.0)) +
+                  (gg[q].z >= 0 ? cbsrc[gg[q].z] : 0.0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int tt = b0 + 32 * q;
+          if (tt < ng) w.v[tt < tk.ns ? tt : tt + sh] = vv[q];
+        }
+      }
+    }
   } else
   for (int b0 = lane; b0 < tk.f; b0 += 256) {
     int4 gg[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) gg[q] = (b0 + 32 * q < tk.f) ? g[b0 + 32 * q] : make_int4(-1, -1, -1, 0);
+    for (int q = 0; q < 8; ++q) gg[q] = (b0 + 32 * q < tk.f) ? g[b0 + 32 * q] : make_int4(-1, -1, -1, -1);
     double vv[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q)
@@ -2355,6 +2449,7 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   a.sub_len = sp.sub_len;
   a.sub_cb = sp.sub_cb;
   a.g3p = sp.g3p.as<int4>();
+  a.g4p = sp.g4p.as<int>();
   a.bpos = sp.bpos.as<int>();
   a.bpos4 = sp.bpos4.as<int>();
   if (sp.tab_ints) {
@@ -2847,7 +2942,8 @@ void nd_sweep(const NDFactor &fac, const double *rhs, int64_t ld_rhs, double *x,
   // cluster mode keeps the cheaper hardware barrier for the MHD blocks
   static const int grid_env = env_int2("STMHD_SWEEP_GRID", -1);
   const double fbytes = 8.0 * (double)fac.dev->plan->factor_size;
-  const bool grid = grid_env == 1 || (grid_env < 0 && fbytes > 32e6);
+  // (amalgamated plans need more subtrees than a 16-CTA cluster has CTAs)
+  const bool grid = grid_env == 1 || (grid_env < 0 && (fbytes > 32e6 || fac.dev->plan->nwide > 0));
   sweep_stage_prepare(*sp, fac, rhs, ld_rhs, x, ld_x, nrhs, cpl, ncpl, nullptr, 0, s, 0,
                       grid ? num_sms() : kCluster, grid);
   SweepStage *one = sp.get();

@@ -178,7 +178,7 @@ class Dissector {
 }  // namespace
 
 NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const int32_t *gx,
-                  const int32_t *gy, int leaf_max, const int32_t *value_map) {
+                  const int32_t *gy, int leaf_max, const int32_t *value_map, int merge_depth) {
   require(n > 0, "nd_analyze: empty matrix");
   Graph g = symmetrize(n, rowptr, col);
   Dissector dis(g, gx, gy, leaf_max);
@@ -186,6 +186,41 @@ NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const in
   std::iota(all.begin(), all.end(), 0);
   int root = dis.build(std::move(all));
   auto &tree = dis.tree;
+
+  // Amalgamation of one tree level (merge_depth >= 0): every separator at that depth
+  // absorbs its two child separators -- one supernode whose columns are the children's
+  // then its own, whose children are the grandchildren (up to four).  The time sweeps
+  // pay a grid-wide step per tree level between the CTA-local subtrees and the dense
+  // top, so one level fewer there is worth the larger front (explicit zeros between the
+  // two absorbed separators).  Only where all four grandchildren exist and have
+  // children themselves (not near the leaves).
+  if (merge_depth >= 0) {
+    std::vector<int> depth(tree.size(), -1), order{root};
+    depth[root] = 0;
+    for (size_t i = 0; i < order.size(); ++i)
+      for (int c : tree[order[i]].children) {
+        depth[c] = depth[order[i]] + 1;
+        order.push_back(c);
+      }
+    for (int t : order) {
+      if (depth[t] != merge_depth || tree[t].children.size() != 2) continue;
+      bool ok = true;
+      std::vector<int> grand;
+      for (int c : tree[t].children) {
+        ok = ok && tree[c].children.size() == 2;
+        for (int gc : tree[c].children) {
+          ok = ok && !tree[gc].children.empty();
+          grand.push_back(gc);
+        }
+      }
+      if (!ok) continue;
+      std::vector<int> cols;
+      for (int c : tree[t].children) cols.insert(cols.end(), tree[c].cols.begin(), tree[c].cols.end());
+      cols.insert(cols.end(), tree[t].cols.begin(), tree[t].cols.end());
+      tree[t].cols = std::move(cols);
+      tree[t].children = std::move(grand);
+    }
+  }
 
   // postorder
   std::vector<int> post;
@@ -376,6 +411,10 @@ NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const in
   for (int s = 0; s < S; ++s) p.nlevels = std::max(p.nlevels, p.level[s] + 1);
   p.level_sn.assign(p.nlevels, {});
   for (int s = 0; s < S; ++s) p.level_sn[p.level[s]].push_back(s);
+  for (int s = 0; s < S; ++s) {
+    require(p.child_ptr[s + 1] - p.child_ptr[s] <= 4, "nd_analyze: supernode with more than four children");
+    p.nwide += p.wide(s);
+  }
   return p;
 }
 
