@@ -35,12 +35,12 @@ DCsr stmhd_disc_s::csr(const char *prefix) const {
 }
 
 static std::unique_ptr<NDPlan> make_plan(stmhd_disc_s *d, const std::string &pat, const char *gx, const char *gy,
-                                         const char *map, int leaf, int merge_depth = -1) {
+                                         const char *map, int leaf, unsigned merge_mask = 0) {
   const HostArray &rp = d->H((pat + "_rowptr").c_str());
   const HostArray &ci = d->H((pat + "_col").c_str());
   const int32_t *vmap = map ? d->H(map).as<int32_t>() : nullptr;
   auto p = std::make_unique<NDPlan>(nd_analyze(rp.count - 1, rp.as<int32_t>(), ci.as<int32_t>(),
-                                               d->H(gx).as<int32_t>(), d->H(gy).as<int32_t>(), leaf, vmap, merge_depth));
+                                               d->H(gx).as<int32_t>(), d->H(gy).as<int32_t>(), leaf, vmap, merge_mask));
   return p;
 }
 
@@ -121,12 +121,13 @@ int stmhd_disc_finalize(stmhd_disc d, void *stream) {
     (void)d->I(k);
   int lf = (int)d->I("leaf_fu"), lc = (int)d->I("leaf_ca"), lk = (int)d->I("leaf_c");
   // velocity block of the grid-family sweeps (n_u >= 8000: 32^2 P2 meshes and larger): the
-  // separators at tree depth 4 absorb their children (nd_analyze), one grid-wide tree level
-  // fewer per sweep direction between the 64 CTA-local subtrees and the dense top
-  // (STMHD_ND_MERGE_DEPTH: depth, -1 off)
-  int merge_depth = d->I("n_u") >= 8000 ? 4 : -1;
-  if (const char *e = getenv("STMHD_ND_MERGE_DEPTH")) merge_depth = atoi(e);
-  d->plan_fu = make_plan(d, "fu", "fu_gx", "fu_gy", "fu_map", lf, merge_depth);
+  // separators at tree depths 4, 6 and 8 absorb their children (nd_analyze) -- one
+  // grid-wide band level fewer per sweep direction between the 64 CTA-local subtrees and
+  // the dense top, and three instead of five CTA-local levels inside a subtree (C4_512
+  // P_T^-1 33.8 -> 30.5 ms for +14 % factor bytes; STMHD_ND_MERGE_MASK: bit d = depth d, 0 off)
+  unsigned merge_mask = d->I("n_u") >= 8000 ? (1u << 4 | 1u << 6 | 1u << 8) : 0u;
+  if (const char *e = getenv("STMHD_ND_MERGE_MASK")) merge_mask = (unsigned)atoi(e);
+  d->plan_fu = make_plan(d, "fu", "fu_gx", "fu_gy", "fu_map", lf, merge_mask);
   d->plan_fa = make_plan(d, "fa", "p1_gx", "p1_gy", "fa_map", lc);
   d->plan_ca = make_plan(d, "ca", "p1_gx", "p1_gy", nullptr, lc);
   d->plan_fp = make_plan(d, "fp", "prs_gx", "prs_gy", nullptr, lc);

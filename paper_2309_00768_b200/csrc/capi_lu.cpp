@@ -1,5 +1,6 @@
 // extern "C" entry points: error state and the generic batched sparse LU
 // (drop-in for reference LUFactor, pkg/src/stmhd/linalg.py:71-96).
+#include <cstdlib>
 #include <cstring>
 
 #include "capi_common.hpp"
@@ -48,7 +49,10 @@ int stmhd_lu_create(int64_t n, const int32_t *rowptr, const int32_t *col, const 
   require(n > 0 && rowptr && col && out && nbatch >= 1, "stmhd_lu_create: bad arguments");
   auto *lu = new stmhd_lu_s();
   try {
-    lu->plan = nd_analyze(n, rowptr, col, gx, gy, leaf_max > 0 ? leaf_max : 64, nullptr);
+    // level amalgamation of the tree (nd_analyze): STMHD_LU_MERGE_MASK, bit d = depth d
+    unsigned merge_mask = 0;
+    if (const char *e = getenv("STMHD_LU_MERGE_MASK")) merge_mask = (unsigned)atoi(e);
+    lu->plan = nd_analyze(n, rowptr, col, gx, gy, leaf_max > 0 ? leaf_max : 64, nullptr, merge_mask);
     lu->dev.build(lu->plan, 0);
     STMHD_CUDA_CHECK(cudaStreamSynchronize(0));
     lu->fac.dev = &lu->dev;

@@ -62,7 +62,7 @@ struct NDPlan {
 // Build the plan.  gx/gy may be null (graph bisection).  value_map (may be null)
 // maps pattern entries to caller value indices.
 NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const int32_t *gx,
-                  const int32_t *gy, int leaf_max, const int32_t *value_map, int merge_depth = -1);
+                  const int32_t *gy, int leaf_max, const int32_t *value_map, unsigned merge_mask = 0);
 
 // Work item of the cluster-resident time sweep (nd_sweep.cu), built lazily for a
 // launch shape: a contiguous chunk range of one supernode.  32 bytes, so a warp's

@@ -135,7 +135,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
   while (pow2 * 2 <= ncta) pow2 *= 2;
   const int maxsub_dflt = pow2;
   const int max_sub = ncta > 16 ? std::min(maxsub_env > 0 ? maxsub_env : maxsub_dflt, ncta) : ncta;
-  std::vector<int> frontier;
+  std::vector<int> frontier, uniform;
   if (D) {
     for (int sn = 0; sn < p.nsn; ++sn)
       if (p.parent[sn] < 0) frontier.push_back(sn);
@@ -151,7 +151,14 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
       const int sn = frontier[best];
       frontier.erase(frontier.begin() + best);
       for (int ci = p.child_ptr[sn]; ci < p.child_ptr[sn + 1]; ++ci) frontier.push_back(p.child_list[ci]);
+      bool same = true;
+      for (int f : frontier) same = same && p.level[f] == p.level[frontier[0]];
+      if (same) uniform = frontier;
     }
+    // amalgamated trees widen by four per level in places: a frontier that ends between
+    // two levels has subtrees of different depths, and the slab time is the deepest
+    // one's -- keep the last frontier whose subtrees all have the same height
+    if (p.nwide > 0 && uniform.size() > 1) frontier = uniform;
     if ((int)frontier.size() > ncta || frontier.size() <= 1) D = 0;
     std::sort(frontier.begin(), frontier.end());
   }
@@ -193,11 +200,7 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
       maxlen = std::max(maxlen, hi[r] - lo[r]);
       maxcb = std::max(maxcb, cbhi[r] - cblo[r]);
     }
-    // amalgamated (wide) supernodes are handled by the top-level tasks only: a frontier
-    // above them (fewer subtrees than their children) falls back to the all-top schedule
-    bool wide_owned = false;
-    for (int sn = 0; sn < p.nsn && D > 0; ++sn) wide_owned |= owner[sn] >= 0 && p.wide(sn);
-    if (D == 0 || (!wide_owned && 3 * maxlen + maxcb <= sub_budget)) break;  // ys, xs, rhs_s + cbs
+    if (D == 0 || 3 * maxlen + maxcb <= sub_budget) break;  // ys, xs, rhs_s + cbs
     D = 0;
   }
   if (D == 0) maxlen = maxcb = 0;
@@ -450,15 +453,19 @@ const NDSweepPlan &NDDevice::get_sweep_plan(int ncta, int warps, int64_t smem_bu
         const int64_t o = p.idx_off[sn];
         if (p.child_ptr[sn + 1] > p.child_ptr[sn]) {
           ftab_off[sn] = (int)fw.size();
-          std::vector<int> yz[2] = {std::vector<int>(f, -1), std::vector<int>(f, -1)};
+          std::vector<int> yz[4] = {std::vector<int>(f, -1), std::vector<int>(f, -1), std::vector<int>(f, -1),
+                                    std::vector<int>(f, -1)};
           int which = 0;
           for (int ci = p.child_ptr[sn]; ci < p.child_ptr[sn + 1]; ++ci, ++which) {
             const int ch = p.child_list[ci];
-            require(which < 2 && cbloc[ch] >= 0, "nd sweep: subtree supernode with an unexpected child");
+            require(which < 4 && cbloc[ch] >= 0, "nd sweep: subtree supernode with an unexpected child");
             for (int a = 0; a < p.nb[ch]; ++a) yz[which][p.emap[p.emap_off[ch] + a]] = cbloc[ch] + a;
           }
-          for (int t = 0; t < f; ++t)
+          // (an amalgamated supernode has two table words per entry: children 0, 1 and 2, 3)
+          for (int t = 0; t < f; ++t) {
             fw.push_back((int)((unsigned)(yz[0][t] & 0xffff) | ((unsigned)(yz[1][t] & 0xffff) << 16)));
+            if (p.wide(sn)) fw.push_back((int)((unsigned)(yz[2][t] & 0xffff) | ((unsigned)(yz[3][t] & 0xffff) << 16)));
+          }
         }
         btab_off[sn] = (int)bw.size();
         for (int t = p.ns[sn]; t < f; ++t) {
@@ -790,6 +797,7 @@ struct SweepArgs {
   int slot;     // doubles per TMA slot (largest chunk block)
   int null_work;  // diagnostics: skip all task work (barrier/loop floor)
   unsigned *gbar;  // grid mode (one CTA per SM, cooperative launch): software grid barrier word
+  int cpl16;       // coupling program: 16 entries per step when a CTA has one item per thread
   int kpref;       // L2 prefetch of the slab's dense-top rows at the slab start
   unsigned long long *progress;  // L2 prefetch cluster: (epoch << 32) | slab in progress (CTA 0)
   int ldgsts;      // ring items by warp-wide cp.async (16 B per lane) instead of one cp.async.bulk
@@ -1045,6 +1053,16 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
     // its children's updates through the resident table
     const int *ft = sv.ftab + tk.goff;
     const bool leaf = tk.flags & 16;
+    if (tk.flags & 64) {  // amalgamated supernode: two table words per entry (four children)
+      for (int t = lane; t < tk.f; t += 32) {
+        double v = t < tk.ns ? rsrc[tk.first + t] : 0.0;
+        const int e = ft[2 * t], e2 = ft[2 * t + 1];
+        const int y = (short)(e & 0xffff), z = (short)(e >> 16), y2 = (short)(e2 & 0xffff), z2 = (short)(e2 >> 16);
+        v = ((v + (y >= 0 ? sv.cbs[y] : 0.0)) + (z >= 0 ? sv.cbs[z] : 0.0)) +
+            ((y2 >= 0 ? sv.cbs[y2] : 0.0) + (z2 >= 0 ? sv.cbs[z2] : 0.0));
+        w.v[t] = v;
+      }
+    } else
     for (int t = lane; t < tk.f; t += 32) {
       double v = t < tk.ns ? rsrc[tk.first + t] : 0.0;
       if (!leaf) {
@@ -1118,6 +1136,16 @@ __device__ __forceinline__ void forward_task(const SweepArgs &a, const SweepTask
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       if (b0 + 32 * q < tk.f) w.v[b0 + 32 * q] = vv[q];
+  }
+  if (SUB && (tk.flags & 64) && !(tk.flags & (16 | 32))) {
+    // amalgamated supernode on the table path of a subtree (no resident tables):
+    // children 2 and 3 (each lane revisits its own entries)
+    const double *cb2 = sv.cbs - sv.cbfirst;
+    const int *g4 = a.g4p + tk.goff;
+    for (int t = lane; t < tk.f; t += 32) {
+      const int gw = g[t].w, g5 = g4[t];
+      w.v[t] += (gw >= 0 ? cb2[gw] : 0.0) + (g5 >= 0 ? cb2[g5] : 0.0);
+    }
   }
   __syncwarp();
   if (PROF) tl_mark(w, 2);
@@ -1312,14 +1340,43 @@ __device__ __forceinline__ void dense_task(const SweepArgs &a, const SweepTask &
 template <int MODE>
 __device__ __forceinline__ void run_program(const int4 hd, const int2 *items, const int *ecol, const double *vk,
                                             const double *rhs, double *out, const SubView &sv, double *tbuf,
-                                            const double *const *srcs) {
+                                            const double *const *srcs, bool wide16 = false) {
   const int nth = blockDim.x;
   constexpr int kIdx = (1 << 28) - 1;
   // threads per item: spread an item's entries over tpi lanes when there are few
   // items (so every load of the step is in flight at once)
   int tpi = 1;
   while (tpi < 32 && hd.y * tpi * 2 <= nth) tpi *= 2;
-  if (tpi == 1) {
+  if (tpi == 1 && hd.y <= nth && wide16) {
+    // one item per thread (a subtree CTA's rows): 16 entries per step -- the step is a
+    // chain of two memory round trips (entry table, then sources), so a 19-entry mass
+    // matrix row takes two steps instead of three; same accumulation order
+    const int it = threadIdx.x;
+    const bool live = it < hd.y;
+    const int2 io = live ? items[hd.x + it] : make_int2(0, -1);
+    double acc = io.y >= 0 ? rhs[io.y] : 0.0;
+    for (int s0 = 0; s0 < hd.w; s0 += 16) {
+      int cc[16];
+      double vv[16], xv[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int64_t id = hd.z + (int64_t)(s0 + q) * hd.y + it;
+        const bool ok = live && s0 + q < hd.w;
+        cc[q] = ok ? __ldg(ecol + id) : 0;
+        vv[q] = ok ? __ldg(vk + id) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) xv[q] = srcs[cc[q] >> 28][cc[q] & kIdx];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc = fma(vv[q], xv[q], acc);
+    }
+    if (live) {
+      const int kind = io.x >> 29, di = io.x & ((1 << 29) - 1);
+      if (MODE == 1) out[io.x] += acc;
+      else if (kind == 0) sv.rhs_s[di] = acc;
+      else tbuf[di] = acc;
+    }
+  } else if (tpi == 1) {
     for (int i0 = threadIdx.x; i0 < hd.y; i0 += 2 * nth) {
       const int it[2] = {i0, i0 + nth};
       const bool live[2] = {true, i0 + nth < hd.y};
@@ -1635,7 +1692,7 @@ __global__ void __launch_bounds__(512, 1) nd_sweep_kernel(const __grid_constant_
       __syncthreads();
       const double *vk = a.prog_vals + (a.prog_per_slab ? (int64_t)k * a.prog_nent : 0);
       long long tp0 = pclock<PROF>();
-      run_program<0>(a.prog_hdr[crank], a.prog_items, a.prog_ecol, vk, rhs, nullptr, sv, a.tbuf, s_src);
+      run_program<0>(a.prog_hdr[crank], a.prog_items, a.prog_ecol, vk, rhs, nullptr, sv, a.tbuf, s_src, a.cpl16 != 0);
       if (PROF) w.acc[9] += pclock<PROF>() - tp0;
       tb = pclock<PROF>(); __syncthreads(); if (PROF) w.acc[3] += pclock<PROF>() - tb;
       sweep_trace(a, step, crank);
@@ -2514,6 +2571,7 @@ void sweep_stage_prepare(SweepStage &st, const NDFactor &fac, const double *rhs,
   a.vstride = vstride;
   a.null_work = env_int2("STMHD_SWEEP_NULL", 0);
   a.ldgsts = env_int2("STMHD_SWEEP_LDGSTS", 0);
+  a.cpl16 = env_int2("STMHD_SWEEP_CPL16", 1);
   a.kpref = env_int2("STMHD_SWEEP_KPREF", 0);  // measured: no gain (dense step not HBM-latency bound)
   a.post_hdr = nullptr;  // set by sweep_stage_set_post for this launch
   a.gbar = nullptr;

@@ -178,7 +178,7 @@ class Dissector {
 }  // namespace
 
 NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const int32_t *gx,
-                  const int32_t *gy, int leaf_max, const int32_t *value_map, int merge_depth) {
+                  const int32_t *gy, int leaf_max, const int32_t *value_map, unsigned merge_mask) {
   require(n > 0, "nd_analyze: empty matrix");
   Graph g = symmetrize(n, rowptr, col);
   Dissector dis(g, gx, gy, leaf_max);
@@ -187,14 +187,14 @@ NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const in
   int root = dis.build(std::move(all));
   auto &tree = dis.tree;
 
-  // Amalgamation of one tree level (merge_depth >= 0): every separator at that depth
-  // absorbs its two child separators -- one supernode whose columns are the children's
-  // then its own, whose children are the grandchildren (up to four).  The time sweeps
-  // pay a grid-wide step per tree level between the CTA-local subtrees and the dense
-  // top, so one level fewer there is worth the larger front (explicit zeros between the
-  // two absorbed separators).  Only where all four grandchildren exist and have
-  // children themselves (not near the leaves).
-  if (merge_depth >= 0) {
+  // Amalgamation of tree levels (bit d of merge_mask: depth d): every separator at such a
+  // depth absorbs its two child separators -- one supernode whose columns are the
+  // children's then its own, whose children are the grandchildren (up to four).  The
+  // time sweeps pay a synchronised step per tree level, so a level fewer is worth the
+  // larger front (explicit zeros between the two absorbed separators).  Depths in the
+  // mask are at least two apart (an absorbed node is never a merge root itself).
+  require((merge_mask & (merge_mask << 1)) == 0, "nd_analyze: adjacent depths in the merge mask");
+  if (merge_mask) {
     std::vector<int> depth(tree.size(), -1), order{root};
     depth[root] = 0;
     for (size_t i = 0; i < order.size(); ++i)
@@ -203,15 +203,12 @@ NDPlan nd_analyze(int64_t n, const int32_t *rowptr, const int32_t *col, const in
         order.push_back(c);
       }
     for (int t : order) {
-      if (depth[t] != merge_depth || tree[t].children.size() != 2) continue;
+      if (depth[t] > 31 || !(merge_mask >> depth[t] & 1u) || tree[t].children.size() != 2) continue;
       bool ok = true;
       std::vector<int> grand;
       for (int c : tree[t].children) {
         ok = ok && tree[c].children.size() == 2;
-        for (int gc : tree[c].children) {
-          ok = ok && !tree[gc].children.empty();
-          grand.push_back(gc);
-        }
+        for (int gc : tree[c].children) grand.push_back(gc);
       }
       if (!ok) continue;
       std::vector<int> cols;
