@@ -166,3 +166,29 @@ def test_lu_amalgamated_tree(pkg, monkeypatch):
     x3 = torch.empty((16, N), dtype=torch.float64, device="cuda")
     h1.solve(torch.as_tensor(rhs2[:16], device="cuda"), x3, 16, N, N)
     assert np.array_equal(x3.cpu().numpy(), x2[:16])  # same per-right-hand-side arithmetic
+
+
+def test_lu_shared_factor_many_rhs(pkg):
+    """Shared factor, >= 2 x SMs right-hand sides (nd_solve_cta_multi_kernel: four
+    right-hand sides per CTA share every factor load -- the constant-operator pre-steps of
+    P_T^-1 at 512 slabs): against SuperLU, and bitwise equal to the one-CTA-per-
+    right-hand-side kernel (same arithmetic per item and right-hand side)."""
+    import torch
+    from paper_2309_00768_b200.linalg import _LUHandle
+
+    mats, pat, vals, gx, gy = _fe_velocity_batch(16, nslab=1)
+    N = pat.shape[0]
+    h = _LUHandle(pat, 1, gx, gy, 32)
+    h.factor(torch.as_tensor(vals[:1], device="cuda"), pat.nnz)
+    nr = 333
+    rhs = RNG.standard_normal((nr, N))
+    x = torch.empty((nr, N), dtype=torch.float64, device="cuda")
+    h.solve(torch.as_tensor(rhs, device="cuda"), x, nr, N, N)
+    x = x.cpu().numpy()
+    lu0 = spla.splu(mats[0].tocsc())
+    for k in (0, 3, 170, nr - 1):
+        ref = lu0.solve(rhs[k])
+        assert np.linalg.norm(x[k] - ref) <= 1e-11 * np.linalg.norm(ref), k
+    x1 = torch.empty((20, N), dtype=torch.float64, device="cuda")
+    h.solve(torch.as_tensor(rhs[-20:], device="cuda"), x1, 20, N, N)
+    assert np.array_equal(x1.cpu().numpy(), x[-20:])
