@@ -49,8 +49,12 @@ int stmhd_lu_create(int64_t n, const int32_t *rowptr, const int32_t *col, const 
   require(n > 0 && rowptr && col && out && nbatch >= 1, "stmhd_lu_create: bad arguments");
   auto *lu = new stmhd_lu_s();
   try {
-    // level amalgamation of the tree (nd_analyze): STMHD_LU_MERGE_MASK, bit d = depth d
-    unsigned merge_mask = 0;
+    // level amalgamation of the tree (nd_analyze; STMHD_LU_MERGE_MASK, bit d = depth d):
+    // batched grid factors of C5's size (256^2 P1: n = 66049) take depths 4 and 8 -- one
+    // grid-wide band level and one CTA-local level fewer per sweep direction (exact
+    // inverse 65.2 -> 59.6 us per slab; the depth-6 merge that pays on the 64^2 P2
+    // velocity block breaks the 128-subtree frontier here and measured slower)
+    unsigned merge_mask = (n >= 32768 && gx && gy && nbatch > 1) ? (1u << 4 | 1u << 8) : 0u;
     if (const char *e = getenv("STMHD_LU_MERGE_MASK")) merge_mask = (unsigned)atoi(e);
     lu->plan = nd_analyze(n, rowptr, col, gx, gy, leaf_max > 0 ? leaf_max : 64, nullptr, merge_mask);
     lu->dev.build(lu->plan, 0);
