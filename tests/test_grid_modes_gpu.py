@@ -73,3 +73,49 @@ def test_sweep_options_match_default(tmp_path, opt):
     for k in ("z", "s"):
         err = np.linalg.norm(a[k] - b[k]) / np.linalg.norm(a[k])
         assert err < 1e-12, (k, opt, err)
+
+
+CHILD_MERGED = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2309_00768_b200 as p
+d = p.discretize(p.baseline_island(1e-2), 2.0 / 32, 0.05, 0.3)   # 32^2 P2/P1, 6 slabs: n_u = 8450 (merged tree)
+st = p.initial_state(d)
+st.vec.data += 1e-3 * torch.randn(st.vec.data.shape, dtype=torch.float64, device="cuda",
+                                  generator=torch.Generator(device="cuda").manual_seed(0))
+jac = p.assemble_jacobian(st, d)
+pc = p.SpaceTimePreconditioner(jac, d, st)
+r = torch.randn(jac.size, dtype=torch.float64, device="cuda", generator=torch.Generator(device="cuda").manual_seed(1))
+z = pc.apply_inverse(r)
+u = pc.solve_velocity(r[: d.n_steps * d.layout.n_u].clone())
+np.savez(sys.argv[2], z=z.cpu().numpy(), s=u.cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("opt", [
+    {"STMHD_SWEEP_GRID": "0", "STMHD_PC_GRID": "0"},  # 16-CTA clusters: the amalgamated separators are subtree roots
+    {"STMHD_SWEEP_GRID": "0", "STMHD_PC_GRID": "0", "STMHD_SWEEP_SMEM_TABLES": "0"},  # ... on the table-in-ring path
+    {"STMHD_SWEEP_DENSE_TOP": "0"},                   # every top level a tree level (wide top-level tasks)
+    {"STMHD_ND_MERGE_MASK": "0"},                     # the plain tree
+])
+def test_amalgamated_tree_launch_modes_match_default(tmp_path, opt):
+    """The amalgamated velocity tree (four-child supernodes, DESIGN 4.4b) through every
+    sweep path: CTA-local subtrees with resident tables and with tables in the ring,
+    top-level tasks with and without the dense top, against the default grid-family
+    launch, and the default against the plain tree."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+    def run(env_extra, name):
+        env = dict(os.environ, **env_extra)
+        out = str(tmp_path / name)
+        subprocess.run([sys.executable, "-c", CHILD_MERGED, ROOT, out], env=env, check=True, timeout=600)
+        return np.load(out)
+
+    a = run({}, "default.npz")
+    b = run(opt, "opt.npz")
+    for k in ("z", "s"):
+        err = np.linalg.norm(a[k] - b[k]) / np.linalg.norm(a[k])
+        assert err < 1e-12, (k, opt, err)
