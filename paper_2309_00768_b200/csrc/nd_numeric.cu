@@ -121,7 +121,6 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level(FactorArgs a) {
   extern __shared__ double smem[];
   __shared__ double red_v[8], red_c[8];
   __shared__ int red_i[8];
-  __shared__ int piv_sh;
   float prat = 1.0f;  // thread 0: smallest pivot ratio of this front
   const int s = a.lvl_sn[blockIdx.x];
   const int bl = blockIdx.y;  // batch slot within chunk
@@ -175,24 +174,27 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level(FactorArgs a) {
       }
       if ((tid & 31) == 0) { red_v[tid >> 5] = best; red_i[tid >> 5] = bi; red_c[tid >> 5] = cbm; }
       __syncthreads();
-      if (tid == 0) {
+      // every thread folds the eight warp results itself (same order, same pivot): no
+      // serial section on thread 0 and no second barrier to broadcast it
+      int piv;
+      {
         double bv = red_v[0], cm = red_c[0];
         int bidx = red_i[0];
         for (int w = 1; w < nt / 32; ++w) {
           if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bidx)) { bv = red_v[w]; bidx = red_i[w]; }
           cm = fmax(cm, red_c[w]);
         }
-        // pivot ratio: the chosen pivot against the largest entry of its column below
-        // the diagonal including the contribution-block rows the restricted pivoting
-        // does not search (1 = as good as unrestricted partial pivoting)
-        if (bv > 0.0 && isfinite(bv)) prat = fmin(prat, bv / fmax(bv, cm));
-        piv_sh = (bv > 0.0 && isfinite(bv)) ? bidx : -1;
-        if (piv_sh >= 0 && piv_sh != col) {
-          int t = perm[col]; perm[col] = perm[piv_sh]; perm[piv_sh] = t;
+        piv = (bv > 0.0 && isfinite(bv)) ? bidx : -1;
+        if (tid == 0) {
+          // pivot ratio: the chosen pivot against the largest entry of its column below
+          // the diagonal including the contribution-block rows the restricted pivoting
+          // does not search (1 = as good as unrestricted partial pivoting)
+          if (piv >= 0) prat = fmin(prat, bv / fmax(bv, cm));
+          if (piv >= 0 && piv != col) {
+            int t = perm[col]; perm[col] = perm[piv]; perm[piv] = t;
+          }
         }
       }
-      __syncthreads();
-      int piv = piv_sh;
       if (piv < 0) { singular = true; break; }
       if (piv != col)
         for (int c = tid; c < f; c += nt) {
@@ -205,9 +207,17 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level(FactorArgs a) {
       int rows = f - col - 1, cols = p0 + pw - col - 1;
       for (int r = tid; r < rows; r += nt) F[(int64_t)(col + 1 + r) * f + col] *= inv;
       __syncthreads();
-      for (int64_t t = tid; t < (int64_t)rows * cols; t += nt) {
-        int r = col + 1 + (int)(t / cols), c = col + 1 + (int)(t % cols);
-        F[(int64_t)r * f + c] -= F[(int64_t)r * f + col] * F[(int64_t)col * f + c];
+      if (cols > 0) {  // rank-1 update of the panel: W (power of two >= cols) threads per row, no divisions
+        int lw = 0;
+        while ((1 << lw) < cols) ++lw;
+        const int c = tid & ((1 << lw) - 1), rstep = nt >> lw;
+        if (c < cols) {
+          const double u = F[(int64_t)col * f + col + 1 + c];
+          for (int r = tid >> lw; r < rows; r += rstep) {
+            double *row = F + (int64_t)(col + 1 + r) * f;
+            row[col + 1 + c] -= row[col] * u;
+          }
+        }
       }
       __syncthreads();
     }
@@ -242,30 +252,35 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level(FactorArgs a) {
     for (int r = 0; r < ns; ++r) FLT[(int64_t)ci * f + r] = (r == i) ? 1.0 : 0.0;
   }
   __syncthreads();
-  for (int r = 1; r < ns; ++r) {
-    for (int i = tid; i < r; i += nt) {
-      int ci = perm[i];
+  // (one thread per column of L11^-1 P, rows in sequence: the same sums in the same
+  // order as a row-by-row sweep with a barrier per row, without the barriers)
+  for (int i = tid; i < ns; i += nt) {
+    double *cl = FLT + (int64_t)perm[i] * f;
+    for (int r = i + 1; r < ns; ++r) {
+      const double *fr = F + (int64_t)r * f;
       double acc = 0.0;
-      for (int k = i; k < r; ++k) acc -= F[(int64_t)r * f + k] * FLT[(int64_t)ci * f + k];
-      FLT[(int64_t)ci * f + r] = acc;
+      for (int k = i; k < r; ++k) acc -= fr[k] * cl[k];
+      cl[r] = acc;
     }
-    __syncthreads();
   }
+  __syncthreads();
   // G^T = (L11^{-1} P)^T L21^T  ->  FLT[c*f + ns + i]
   cta_gemm(ns, nb, ns, 1.0, FLT, f, F + (int64_t)ns * f, f, 0.0, FLT + ns, f, smem, false, true);
   // U11^{-1}: FUT[j*ns + i] for i <= j
   for (int j = tid; j < ns; j += nt)
     for (int i = 0; i < ns; ++i) FUT[(int64_t)j * ns + i] = 0.0;
   __syncthreads();
-  for (int i = ns - 1; i >= 0; --i) {
-    double dinv = 1.0 / F[(int64_t)i * f + i];
-    for (int j = i + tid; j < ns; j += nt) {
+  for (int j = tid; j < ns; j += nt) {  // one thread per column of U11^-1, rows upwards (same sums, no barriers)
+    double *cu = FUT + (int64_t)j * ns;
+    for (int i = j; i >= 0; --i) {
+      const double *fi = F + (int64_t)i * f;
+      const double dinv = 1.0 / fi[i];
       double acc = (i == j) ? 1.0 : 0.0;
-      for (int k = i + 1; k <= j; ++k) acc -= F[(int64_t)i * f + k] * FUT[(int64_t)j * ns + k];
-      FUT[(int64_t)j * ns + i] = acc * dinv;
+      for (int k = i + 1; k <= j; ++k) acc -= fi[k] * cu[k];
+      cu[i] = acc * dinv;
     }
-    __syncthreads();
   }
+  __syncthreads();
   // (-U11^{-1} U12)^T = -U12^T U11^{-T}  ->  FUT[(ns+j)*ns + i]
   cta_gemm(nb, ns, ns, -1.0, F + ns, f, FUT, ns, 0.0, FUT + (int64_t)ns * ns, ns, smem, true, false);
 }
@@ -282,7 +297,6 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level_smem(FactorArgs a) {
   extern __shared__ double smem[];
   __shared__ double red_v[8], red_c[8];
   __shared__ int red_i[8];
-  __shared__ int piv_sh;
   float prat = 1.0f;  // thread 0: smallest pivot ratio of this front
   const int s = a.lvl_sn[blockIdx.x];
   const int bl = blockIdx.y;
@@ -335,21 +349,22 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level_smem(FactorArgs a) {
       }
       if ((tid & 31) == 0) { red_v[tid >> 5] = best; red_i[tid >> 5] = bi; red_c[tid >> 5] = cbm; }
       __syncthreads();
-      if (tid == 0) {
+      int piv;  // (every thread folds the eight warp results itself, as in nd_factor_level)
+      {
         double bv = red_v[0], cm = red_c[0];
         int bidx = red_i[0];
         for (int w = 1; w < nt / 32; ++w) {
           if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bidx)) { bv = red_v[w]; bidx = red_i[w]; }
           cm = fmax(cm, red_c[w]);
         }
-        if (bv > 0.0 && isfinite(bv)) prat = fmin(prat, bv / fmax(bv, cm));
-        piv_sh = (bv > 0.0 && isfinite(bv)) ? bidx : -1;
-        if (piv_sh >= 0 && piv_sh != col) {
-          const int t = perm[col]; perm[col] = perm[piv_sh]; perm[piv_sh] = t;
+        piv = (bv > 0.0 && isfinite(bv)) ? bidx : -1;
+        if (tid == 0) {
+          if (piv >= 0) prat = fmin(prat, bv / fmax(bv, cm));
+          if (piv >= 0 && piv != col) {
+            const int t = perm[col]; perm[col] = perm[piv]; perm[piv] = t;
+          }
         }
       }
-      __syncthreads();
-      const int piv = piv_sh;
       if (piv < 0) { singular = true; break; }
       if (piv != col)
         for (int c = tid; c < f; c += nt) {
@@ -362,9 +377,17 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level_smem(FactorArgs a) {
       const int rows = f - col - 1, cols = p0 + pw - col - 1;
       for (int r = tid; r < rows; r += nt) F[(col + 1 + r) * f + col] *= inv;
       __syncthreads();
-      for (int t = tid; t < rows * cols; t += nt) {
-        const int r = col + 1 + t / cols, c = col + 1 + t % cols;
-        F[r * f + c] -= F[r * f + col] * F[col * f + c];
+      if (cols > 0) {  // rank-1 update of the panel: W (power of two >= cols) threads per row, no divisions
+        int lw = 0;
+        while ((1 << lw) < cols) ++lw;
+        const int c = tid & ((1 << lw) - 1), rstep = nt >> lw;
+        if (c < cols) {
+          const double u = F[col * f + col + 1 + c];
+          for (int r = tid >> lw; r < rows; r += rstep) {
+            double *row = F + (col + 1 + r) * f;
+            row[col + 1 + c] -= row[col] * u;
+          }
+        }
       }
       __syncthreads();
     }
@@ -398,15 +421,16 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level_smem(FactorArgs a) {
     for (int r = 0; r < ns; ++r) T[ci * ns + r] = (r == i) ? 1.0 : 0.0;
   }
   __syncthreads();
-  for (int r = 1; r < ns; ++r) {
-    for (int i = tid; i < r; i += nt) {
-      const int ci = perm[i];
+  for (int i = tid; i < ns; i += nt) {  // one thread per column, rows in sequence (same sums, no barriers)
+    double *cl = T + perm[i] * ns;
+    for (int r = i + 1; r < ns; ++r) {
+      const double *fr = F + r * f;
       double acc = 0.0;
-      for (int k = i; k < r; ++k) acc -= F[r * f + k] * T[ci * ns + k];
-      T[ci * ns + r] = acc;
+      for (int k = i; k < r; ++k) acc -= fr[k] * cl[k];
+      cl[r] = acc;
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (int t = tid; t < ns * ns; t += nt) {
     const int ci = t / ns, r = t - ci * ns;
     FLT[(int64_t)ci * f + r] = T[t];
@@ -416,15 +440,17 @@ __global__ void __launch_bounds__(256, 4) nd_factor_level_smem(FactorArgs a) {
   // U11^{-1} in T (T[j*ns + i] = FUT[j*ns + i])
   for (int t = tid; t < ns * ns; t += nt) T[t] = 0.0;
   __syncthreads();
-  for (int i = ns - 1; i >= 0; --i) {
-    const double dinv = 1.0 / F[i * f + i];
-    for (int j = i + tid; j < ns; j += nt) {
+  for (int j = tid; j < ns; j += nt) {  // one thread per column of U11^-1, rows upwards (same sums, no barriers)
+    double *cu = T + j * ns;
+    for (int i = j; i >= 0; --i) {
+      const double *fi = F + i * f;
+      const double dinv = 1.0 / fi[i];
       double acc = (i == j) ? 1.0 : 0.0;
-      for (int k = i + 1; k <= j; ++k) acc -= F[i * f + k] * T[j * ns + k];
-      T[j * ns + i] = acc * dinv;
+      for (int k = i + 1; k <= j; ++k) acc -= fi[k] * cu[k];
+      cu[i] = acc * dinv;
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (int t = tid; t < ns * ns; t += nt) FUT[t] = T[t];
   // (-U11^{-1} U12)^T = -U12^T U11^{-T}  ->  FUT[(ns+j)*ns + i]
   cta_gemm(nb, ns, ns, -1.0, F + ns, f, T, ns, 0.0, FUT + (int64_t)ns * ns, ns, gs, true, false);
